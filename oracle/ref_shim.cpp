@@ -1,0 +1,389 @@
+// ref_shim.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// extern "C" entry points over the UNMODIFIED reference sources
+// (/root/reference/proj/src/{rng,param_vec,core,objectives,protocols,
+// simulator,transport}.cpp), compiled by oracle/Makefile into
+// oracle/_ref/libdsgd_ref.so.  Used (a) to pin the C restatement in
+// oracle/dsgd_oracle.c bit-for-bit and (b) as the reference CPU arm of
+// bench.py.  Nothing here is product code; nothing is copied from the
+// reference -- this file only calls its public API (protocols.hpp,
+// simulator.hpp, transport.hpp).
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <span>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "dsgd/core.hpp"
+#include "dsgd/objectives.hpp"
+#include "dsgd/protocols.hpp"
+#include "dsgd/rng.hpp"
+#include "dsgd/simulator.hpp"
+#include "dsgd/transport.hpp"
+#include "dsgd_oracle.h"
+
+using namespace dsgd;
+
+namespace {
+
+// An Objective whose stochastic gradient is a fixed vector: the reference's
+// plugin slot (objectives.hpp:33-53) filled the way the GPU path's external
+// gradient buffer fills it.
+class FixedGradientObjective : public Objective {
+ public:
+  explicit FixedGradientObjective(std::vector<double> g) : g_(std::move(g)) {}
+  std::size_t dim() const override { return g_.size(); }
+  double value(const ParamVec&) const override { return 0.0; }
+  ParamVec gradient(const ParamVec&) const override { return ParamVec(g_); }
+  std::pair<double, double> convexity_params() const override { return {1.0, 1.0}; }
+
+ private:
+  std::vector<double> g_;
+};
+
+thread_local std::string g_err;
+
+Hyperparams to_hyper(const dsgdo_hyper& h) {
+  Hyperparams out;
+  out.alpha0 = h.alpha0;
+  out.anneal_factor = h.anneal_factor;
+  out.anneal_at.assign(h.anneal_at, h.anneal_at + h.n_anneal);
+  out.mu = h.mu;
+  out.weight_decay = h.weight_decay;
+  out.beta_gossip = h.beta_gossip;
+  out.beta_ea = h.beta_ea;
+  out.tau = h.tau;
+  return out;
+}
+
+ProtocolKind to_protocol(int p) {
+  switch (p) {
+    case DSGDO_ALLREDUCE: return ProtocolKind::kAllReduce;
+    case DSGDO_ELASTIC: return ProtocolKind::kElasticAvg;
+    case DSGDO_PULL: return ProtocolKind::kPullGossip;
+    case DSGDO_PUSH: return ProtocolKind::kPushGossip;
+    case DSGDO_STALE: return ProtocolKind::kGossipStale;
+    case DSGDO_FRESH: return ProtocolKind::kGossipFresh;
+    default: return ProtocolKind::kAsyncPull;
+  }
+}
+
+SimConfig to_sim(const dsgdo_sim& c) {
+  SimConfig cfg;
+  cfg.protocol = to_protocol(c.protocol);
+  cfg.p = c.p;
+  cfg.hyper = to_hyper(c.hyper);
+  cfg.noise = c.noise_gaussian ? NoiseModel::gaussian_per_coord(c.sigma, c.d)
+                               : NoiseModel::zero(c.d);
+  switch (c.init_kind) {
+    case DSGDO_INIT_ZEROS: cfg.init.kind = InitSpec::Kind::kZeros; break;
+    case DSGDO_INIT_OFFSET_ONES: cfg.init.kind = InitSpec::Kind::kOffsetOnes; break;
+    case DSGDO_INIT_GAUSSIAN: cfg.init.kind = InitSpec::Kind::kGaussianSpread; break;
+    default:
+      cfg.init.kind = InitSpec::Kind::kExplicit;
+      cfg.init.values.assign(c.init_values, c.init_values + c.d);
+  }
+  cfg.init.target_sq_err = c.target_sq_err;
+  cfg.init.scale = c.init_scale;
+  cfg.momentum_scope = c.scope_per_node ? MomentumScope::kPerNode : MomentumScope::kAggregate;
+  if (c.protocol == DSGDO_ASYNC_PULL || c.poisson) {
+    cfg.clock.kind = ClockModel::Kind::kPoisson;
+    cfg.clock.rate_per_node = c.rate_per_node;
+  }
+  cfg.rounds = c.rounds;
+  cfg.events = c.events;
+  cfg.trace_every = 1u << 30;
+  cfg.seed = c.seed;
+  cfg.run_id = c.run_id;
+  return cfg;
+}
+
+void export_nodes(const std::vector<NodeState>& nodes, std::uint64_t d, double* theta,
+                  double* dprev, std::uint64_t* t) {
+  for (std::size_t i = 0; i < nodes.size(); ++i) {
+    std::memcpy(theta + i * d, nodes[i].theta.raw(), sizeof(double) * d);
+    if (dprev) std::memcpy(dprev + i * d, nodes[i].delta_prev.raw(), sizeof(double) * d);
+    if (t) t[i] = nodes[i].t;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+std::uint64_t ref_derive_stream_seed(std::uint64_t seed, const char* run_id, std::uint32_t node,
+                                     int purpose) {
+  return derive_stream_seed(seed, run_id, node, static_cast<StreamPurpose>(purpose));
+}
+
+// Raw draws and samplers from one stream: kind 0 next_u64 (as bits in a
+// double array via memcpy), 1 uniform01, 2 normal, 3 uniform_index(n),
+// 4 exponential(rate = n).
+void ref_stream_draws(std::uint64_t seed, int kind, std::uint32_t n, std::uint64_t count,
+                      void* out) {
+  RngStream s(seed);
+  for (std::uint64_t i = 0; i < count; ++i) {
+    switch (kind) {
+      case 0: static_cast<std::uint64_t*>(out)[i] = s.next_u64(); break;
+      case 1: static_cast<double*>(out)[i] = s.uniform01(); break;
+      case 2: static_cast<double*>(out)[i] = s.normal(); break;
+      case 3: static_cast<std::uint64_t*>(out)[i] = s.uniform_index(n); break;
+      default: static_cast<double*>(out)[i] = s.exponential(static_cast<double>(n)); break;
+    }
+  }
+}
+
+// Full run through the reference drivers (run_simulation). Returns 0, or -1
+// with ref_last_error() set when the reference throws.
+int ref_run(const dsgdo_sim* c, double* theta, double* dprev, std::uint64_t* t,
+            double* center) {
+  try {
+    const SimConfig cfg = to_sim(*c);
+    QuadraticObjective obj(std::vector<double>(c->spectrum, c->spectrum + c->d),
+                           ParamVec(std::vector<double>(c->opt, c->opt + c->d)));
+    const RunResult r = run_simulation(cfg, obj);
+    export_nodes(r.final_nodes, c->d, theta, dprev, t);
+    if (center && r.final_server) {
+      std::memcpy(center, r.final_server->theta_center.raw(), sizeof(double) * c->d);
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// Threaded transport backend (run_transport): the reference's own parallel
+// per-rank worker loop.
+int ref_run_transport(const dsgdo_sim* c, double* theta, double* dprev, std::uint64_t* t,
+                      double* center, std::uint64_t chaos_seed) {
+  try {
+    const SimConfig cfg = to_sim(*c);
+    QuadraticObjective obj(std::vector<double>(c->spectrum, c->spectrum + c->d),
+                           ParamVec(std::vector<double>(c->opt, c->opt + c->d)));
+    TransportOptions opt;
+    opt.chaos_seed = chaos_seed;
+    const RunResult r = run_transport(cfg, obj, opt);
+    export_nodes(r.final_nodes, c->d, theta, dprev, t);
+    if (center && r.final_server) {
+      std::memcpy(center, r.final_server->theta_center.raw(), sizeof(double) * c->d);
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// One round of a protocol from explicit node states.  Node i's streams are
+// make_node(i, theta, seed, run_id)'s, so noise draws are the first ones of
+// (seed, run_id, i, gradient-noise).  obj_kind 0: shared quadratic (spec,
+// opt); 1: per-node fixed gradients gfixed (p*d).  protocol selects:
+//   0 allreduce_round(scope), 1 EA sweep (gated), 2 pull_gossip_round,
+//   3 push_gossip_round, 4 stale (per node vs snapshot), 5 fresh,
+//   6 async_pull_event(i = aux0, j = aux1), 7 local_sgd_step on every node,
+//   8 pull_mix, 9 push_mix.
+int ref_round(int protocol, std::uint32_t p, std::uint64_t d, double* theta, double* dprev,
+              std::uint64_t* t, const std::uint32_t* partner, int obj_kind, const double* spec,
+              const double* opt, const double* gfixed, int noise_gaussian, double sigma,
+              std::uint64_t seed, const char* run_id, const dsgdo_hyper* hp, int per_node,
+              double* center, int gated, std::uint32_t aux0, std::uint32_t aux1) {
+  try {
+    const Hyperparams h = to_hyper(*hp);
+    const NoiseModel noise =
+        noise_gaussian ? NoiseModel::gaussian_per_coord(sigma, d) : NoiseModel::zero(d);
+    std::vector<std::unique_ptr<Objective>> own;
+    std::vector<const Objective*> objs;
+    for (std::uint32_t i = 0; i < p; ++i) {
+      if (obj_kind == DSGDO_OBJ_QUADRATIC) {
+        own.push_back(std::make_unique<QuadraticObjective>(
+            std::vector<double>(spec, spec + d), ParamVec(std::vector<double>(opt, opt + d))));
+      } else {
+        own.push_back(std::make_unique<FixedGradientObjective>(
+            std::vector<double>(gfixed + i * d, gfixed + (i + 1) * d)));
+      }
+      objs.push_back(own.back().get());
+    }
+    std::vector<NodeState> nodes;
+    for (std::uint32_t i = 0; i < p; ++i) {
+      NodeState n = make_node(i, ParamVec(std::vector<double>(theta + i * d, theta + (i + 1) * d)),
+                              seed, run_id);
+      n.delta_prev = ParamVec(std::vector<double>(dprev + i * d, dprev + (i + 1) * d));
+      n.t = t[i];
+      nodes.push_back(std::move(n));
+    }
+    const std::span<const Objective* const> objspan(objs);
+    const std::span<const std::uint32_t> pm(partner, partner ? p : 0);
+    switch (protocol) {
+      case 0:
+        nodes = allreduce_round(std::move(nodes), objspan, noise, h,
+                                per_node ? MomentumScope::kPerNode : MomentumScope::kAggregate);
+        break;
+      case 1: {
+        ServerState server{ParamVec(std::vector<double>(center, center + d)), 0};
+        for (std::uint32_t i = 0; i < p; ++i) {
+          if (gated) {
+            auto [node, update] = ea_client_step(std::move(nodes[i]), server.theta_center,
+                                                 *objs[i], noise, h);
+            nodes[i] = std::move(node);
+            server = ea_server_apply(std::move(server), update);
+          } else {
+            nodes[i] = local_sgd_step(std::move(nodes[i]), *objs[i], noise, h);
+          }
+        }
+        std::memcpy(center, server.theta_center.raw(), sizeof(double) * d);
+        break;
+      }
+      case 2: nodes = pull_gossip_round(std::move(nodes), pm, objspan, noise, h); break;
+      case 3: nodes = push_gossip_round(std::move(nodes), pm, objspan, noise, h); break;
+      case 4: {
+        std::vector<ParamVec> snap;
+        for (const NodeState& n : nodes) snap.push_back(n.theta);
+        for (std::uint32_t i = 0; i < p; ++i)
+          nodes[i] = gossip_stale_step(std::move(nodes[i]), snap[partner[i]], *objs[i], noise, h);
+        break;
+      }
+      case 5: {
+        for (std::uint32_t i = 0; i < p; ++i)
+          nodes[i] = local_sgd_step(std::move(nodes[i]), *objs[i], noise, h);
+        std::vector<ParamVec> stepped;
+        for (const NodeState& n : nodes) stepped.push_back(n.theta);
+        for (std::uint32_t i = 0; i < p; ++i)
+          nodes[i] = gossip_fresh_mix(std::move(nodes[i]), stepped[partner[i]], h.beta_gossip);
+        break;
+      }
+      case 6:
+        nodes = async_pull_event(std::move(nodes), aux0, aux1, *objs[aux0], noise, h);
+        break;
+      case 7:
+        for (std::uint32_t i = 0; i < p; ++i)
+          nodes[i] = local_sgd_step(std::move(nodes[i]), *objs[i], noise, h);
+        break;
+      case 8: nodes = pull_mix(std::move(nodes), pm); break;
+      case 9: nodes = push_mix(std::move(nodes), pm); break;
+      default: g_err = "bad protocol"; return -1;
+    }
+    export_nodes(nodes, d, theta, dprev, t);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// ring_allreduce over p threads on an in-process Network (transport.cpp
+// 183-248); in/out are p*d.
+int ref_ring_allreduce(std::uint32_t p, std::uint64_t d, const double* in, double* out,
+                       std::uint64_t chaos_seed) {
+  try {
+    Network net(p);
+    std::vector<std::thread> threads;
+    std::vector<std::exception_ptr> errs(p);
+    for (std::uint32_t r = 0; r < p; ++r) {
+      threads.emplace_back([&, r] {
+        try {
+          Endpoint ep(&net, r, std::chrono::milliseconds(60000), chaos_seed);
+          const auto res =
+              ring_allreduce(ep, p, std::vector<double>(in + r * d, in + (r + 1) * d), 0);
+          std::memcpy(out + r * d, res.data(), sizeof(double) * d);
+        } catch (...) {
+          errs[r] = std::current_exception();
+        }
+      });
+    }
+    for (auto& th : threads) th.join();
+    for (auto& e : errs)
+      if (e) std::rethrow_exception(e);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// CPU-baseline timing: `rounds` rounds of one protocol through the reference
+// update rules on p nodes of dimension d (quadratic objective, spectrum 1,
+// optimum 0; nodes at N(0,1) spread; zero noise; the bench's hyperparams).
+// mode 0: single-thread simulator rules (allreduce_round / pull_gossip_round
+// with the seeded partner streams / EA sweep, gated every round after 0);
+// mode 1: the threaded transport backend run_transport (p worker threads,
+// +1 EA server thread).  Returns seconds for all rounds, or -1.
+double ref_time_rounds(int protocol, std::uint32_t p, std::uint64_t d, std::uint64_t rounds,
+                       int mode, const dsgdo_hyper* hp) {
+  try {
+    dsgdo_sim c{};
+    c.protocol = protocol;
+    c.p = p;
+    c.d = d;
+    c.hyper = *hp;
+    std::vector<double> spec(d, 1.0), opt(d, 0.0);
+    c.spectrum = spec.data();
+    c.opt = opt.data();
+    c.init_kind = DSGDO_INIT_GAUSSIAN;
+    c.init_scale = 1.0;
+    c.rounds = rounds;
+    c.seed = 1;
+    c.run_id = "run/trial0";
+    SimConfig cfg = to_sim(c);
+    QuadraticObjective obj(spec, ParamVec(opt));
+    using clk = std::chrono::steady_clock;
+    if (mode == 1) {
+      // run_transport also builds the initial nodes and trace records; time
+      // `rounds + 1` and 1 round and keep the difference (per-round cost).
+      cfg.rounds = rounds + 1;
+      auto t0 = clk::now();
+      (void)run_transport(cfg, obj);
+      const double tl = std::chrono::duration<double>(clk::now() - t0).count();
+      cfg.rounds = 1;
+      t0 = clk::now();
+      (void)run_transport(cfg, obj);
+      const double ts = std::chrono::duration<double>(clk::now() - t0).count();
+      return tl - ts;
+    }
+    // Single-thread simulator rules, dispatched exactly as run_sync does
+    // (simulator.cpp:234-351) on gated rounds; nodes built outside the clock.
+    std::vector<NodeState> nodes = make_initial_nodes(cfg, obj);
+    ServerState server;
+    {
+      std::vector<ParamVec> th;
+      for (const NodeState& n : nodes) th.push_back(n.theta);
+      server = ServerState{spatial_mean(th), 0};
+    }
+    const Hyperparams& h = cfg.hyper;
+    std::vector<std::uint32_t> partners(p);
+    const auto t0 = clk::now();
+    for (std::uint64_t r = 1; r <= rounds; ++r) {  // r > 0: every round gated (tau = 1)
+      switch (protocol) {
+        case DSGDO_ALLREDUCE:
+          nodes = allreduce_round(std::move(nodes), obj, cfg.noise, h, cfg.momentum_scope);
+          break;
+        case DSGDO_PULL:
+          for (std::uint32_t i = 0; i < p; ++i) partners[i] = nodes[i].rng.partner.uniform_index(p);
+          nodes = pull_gossip_round(std::move(nodes), partners, obj, cfg.noise, h);
+          break;
+        case DSGDO_ELASTIC:
+          for (std::uint32_t i = 0; i < p; ++i) {
+            auto [node, update] =
+                ea_client_step(std::move(nodes[i]), server.theta_center, obj, cfg.noise, h);
+            nodes[i] = std::move(node);
+            server = ea_server_apply(std::move(server), update);
+          }
+          break;
+        default:
+          for (NodeState& n : nodes) n = local_sgd_step(std::move(n), obj, cfg.noise, h);
+      }
+    }
+    return std::chrono::duration<double>(clk::now() - t0).count();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1.0;
+  }
+}
+
+}  // extern "C"
