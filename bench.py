@@ -1,0 +1,428 @@
+"""Benchmark of the B200 aggregation/update hot path (BASELINE.json).
+
+Workload (BASELINE.json configs[3]): synchronous all-reduce SGD with
+Nesterov momentum, d = 25M fp32 parameters per worker, one worker per GPU
+(p = N), synthetic N(0,1) gradients (a pool of 4 distinct device buffers per
+worker, cycled; every step's working set -- theta, delta, gradient, ~400 MB
+-- exceeds the 126 MB L2, so no flush is needed).  A step is one
+allreduce_round (protocols.cpp:110-131): fused delta kernel ->
+ncclAllReduce over NVLink -> fused apply kernel (N > 1), or the single fused
+round kernel (N = 1).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Prints ONE JSON line (rank 0).  `value` is the whole-job worker
+param-updates/s with inputs resident in HBM; `e2e` is the same metric through
+the C ABI with each step's gradient copied host->device from pinned memory
+and the step's result (the gradient norm, protocols.cpp:34-36) read back.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "worker param-updates/sec and aggregation-step GB/s vs HBM/NVLink roofline"
+UNIT = "param-updates/s"
+D_DEFAULT = 25_000_000
+POOL = 4
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--d", type=int, default=D_DEFAULT)
+    ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
+    ap.add_argument("--no-extras", action="store_true", help="skip the gossip/EASGD extra lines")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# --------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if len(r) > 5 + k and r[5 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ------------------------------------------------------------ reference arm
+def cpu_reference(protocol: int, p: int, d: int, rounds: int, threaded: bool):
+    import oracle as O
+    h = O.HyperParams(alpha0=0.1, anneal_at=(), mu=0.9, weight_decay=1e-4, beta_ea=0.1)
+    return O.ref_time_rounds(protocol, p, d, rounds, threaded, h)
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    import oracle as O
+    p = max(1, args.gpus)
+    d_sample = min(args.d, 4_000_000)
+    threaded = p > 1
+    cpu_reference(O.ALLREDUCE, p, d_sample, max(1, args.warmup), threaded)
+    sec = cpu_reference(O.ALLREDUCE, p, d_sample, max(1, args.steps), threaded)
+    per = sec / max(1, args.steps)
+    value = p * d_sample / per
+    kind = "reference" if O.ref_available() else "port"
+    cores = p if threaded else 1
+    sample = (f"{args.steps} allreduce_round steps of the compiled reference "
+              f"({'run_transport, ring_allreduce over p threads' if threaded else 'simulator rules, 1 thread'})"
+              f", p={p}, d={d_sample} per worker (of {args.d})")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": "all-reduce SGD round, momentum 0.9, wd 1e-4 (configs[3])",
+                       "d_per_worker": d_sample, "p": p, "parallelism": f"dp{p} (threads)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ ours
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1611_04581_b200 import _native as N
+    from paper_1611_04581_b200.engine import Group, Hyperparams
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    d = args.d
+    tdt = torch.float32 if args.dtype == "f32" else torch.float64
+    es = 4 if args.dtype == "f32" else 8
+    h = Hyperparams(alpha0=0.1, anneal_at=(), mu=0.9, weight_decay=1e-4)
+
+    if world > 1:
+        grp = Group.distributed(d, rank, world, local, dtype=args.dtype, grad=True)
+    else:
+        grp = Group(d, 1, dtype=args.dtype, grad=True, device=local)
+    gen = torch.Generator(device=f"cuda:{local}")
+    gen.manual_seed(1234 + rank)
+    pool = [torch.randn(d, generator=gen, device=f"cuda:{local}", dtype=tdt) for _ in range(POOL)]
+    torch.cuda.synchronize()
+    # initial theta: a common start on every worker (N(0,1), rank-0 seed)
+    g0 = torch.Generator(device=f"cuda:{local}")
+    g0.manual_seed(99)
+    theta0 = torch.randn(d, generator=g0, device=f"cuda:{local}", dtype=tdt)
+    torch.cuda.synchronize()
+    grp.copy_in_async(0, N.BUF_THETA, theta0.data_ptr(), d)
+    grp.sync()
+    del theta0
+    import ctypes
+    stream = torch.cuda.ExternalStream(grp.stream(), device=f"cuda:{local}")
+    pool_ptrs = [t.data_ptr() for t in pool]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def rounds(k):
+        grp.run_rounds(N.ALLREDUCE, h, k, grad_pool=pool_ptrs)
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # warm-up
+    rounds(args.warmup)
+    grp.sync()
+    barrier()
+    torch.cuda.synchronize()
+
+    # ---------------- timed region (device-resident inputs)
+    k0, n0 = grp.launch_count()
+    grp.profile(True)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        rounds(args.steps)
+        ev1.record(stream)
+        grp.sync()
+        torch.cuda.synchronize()
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    ms_max = max_over_ranks(ms)
+    k1, n1 = grp.launch_count()
+    prof = {N.KERNEL_NAMES[k]: grp.profile_read(k, reset=True) for k in range(8)}
+    grp.profile(False)
+    step_ms = ms_max / args.steps
+    value = world * d / (step_ms * 1e-3)
+
+    # dominant kernel + roofline (algorithmic bytes per launch)
+    if world == 1:
+        kname, bpp = "allreduce_local", 20   # read theta, delta, g; write theta', delta'
+        kdesc = "k_allreduce_local (p=1): fused delta + mean + apply, 12 B read + 8 B write per param"
+    else:
+        kname, bpp = "ar_delta", 16          # read theta, delta, g; write delta'
+        kdesc = "k_step<ArDelta>: 12 B read + 4 B write per param (then NCCL avg, k_step<Apply> 12 B)"
+    kms, kn = prof.get(kname, (0.0, 0))
+    peak, peak_src = peaks()
+    kavg_ms = kms / max(1, kn)
+    achieved = (bpp * d / (kavg_ms * 1e-3) / 1e9) if kn else None
+    step_bytes = 20 * d if world == 1 else 28 * d
+    roofline = {"bound": "hbm", "kernel": kdesc, "achieved": achieved, "peak": peak,
+                "peak_source": peak_src, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": None,
+                "algorithmic_bytes_per_launch": bpp * d,
+                "kernel_avg_us": kavg_ms * 1e3,
+                "step_hbm_gbs": step_bytes / (step_ms * 1e-3) / 1e9,
+                "share_of_step": (kms / ms) if ms else None}
+    if world > 1:
+        nms, nn = prof.get("nccl_allreduce", (0.0, 0))
+        t_nccl = nms / max(1, nn) * 1e-3
+        roofline["nccl_allreduce_us"] = t_nccl * 1e6
+        roofline["nccl_busbw_gbs"] = 2 * (world - 1) / world * es * d / t_nccl / 1e9 if nn else None
+        roofline["nvlink_peak_gbs"] = 770.0
+    per_kernel = {k: {"ms_total": v[0], "launches": v[1]} for k, v in prof.items() if v[1]}
+
+    # ---------------- end-to-end through the C ABI (host gradients, pinned)
+    e2e = None
+    if True:
+        host = [torch.randn(d, dtype=tdt).pin_memory() for _ in range(2)]
+        norm = ctypes.c_double(0.0)
+        barrier()
+        torch.cuda.synchronize()
+        steps_e2e = max(3, min(args.steps, 20))
+        # warm
+        for s in range(2):
+            grp.upload_async(0, N.BUF_GRAD, host[s % 2].data_ptr(), d)
+            grp.allreduce_round(h, grad="buffer", grad_norm=True)
+        barrier()
+        t0 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for s in range(steps_e2e):
+            grp.upload_async(0, N.BUF_GRAD, host[s % 2].data_ptr(), d)
+            gn = grp.allreduce_round(h, grad="buffer", grad_norm=True)  # D2H of ||g|| (syncs)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        e_ms = max_over_ranks(max(e0.elapsed_time(e1), wall * 1e3))
+        e2e = {"value": world * d / (e_ms / steps_e2e * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": es * d * world, "d2h_bytes_per_step": 8 * world,
+               "steps": steps_e2e, "ms_per_step": e_ms / steps_e2e,
+               "path": "dsgd_upload_async(pinned host gradient) + dsgd_allreduce_round(grad_norm_out)"}
+
+    # ---------------- extras: gossip / EASGD shapes
+    extras = {}
+    if world == 1 and not args.no_extras:
+        extras = run_extras(args, local, h)
+    elif world > 1 and not args.no_extras:
+        extras = run_extras_dist(args, world, rank, local, h, max_over_ranks, barrier)
+
+    # ---------------- CPU baseline (rank 0, N = 1)
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu:
+        try:
+            import oracle as O
+            d_s = d
+            rounds_cpu = 8
+            sec = cpu_reference(O.ALLREDUCE, 1, d_s, rounds_cpu, False)
+            cpu = {"value": d_s / (sec / rounds_cpu), "unit": UNIT, "cores": 1,
+                   "kind": "reference" if O.ref_available() else "port",
+                   "sample": f"{rounds_cpu} allreduce_round (p=1, d={d_s}) of the compiled "
+                             f"reference (oracle/_ref, -O3, fp64), single thread as the simulator"}
+        except Exception as e:  # pragma: no cover
+            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
+                   "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": args.dtype, "data": "synthetic",
+                "config": {"workload": "configs[3]: synchronous all-reduce SGD round (Nesterov "
+                                       "momentum 0.9, wd 1e-4), aggregate momentum scope",
+                           "d_per_worker": d, "p": world, "parallelism": f"dp{world}",
+                           "grad_source": f"pool of {POOL} synthetic N(0,1) device buffers/worker",
+                           "l2": "inputs larger than L2 (~400 MB/step/worker working set)"},
+                "gbs": step_bytes / (step_ms * 1e-3) / 1e9,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": (k1 - k0) + (n1 - n0),
+                "gpu_launches_detail": {"kernels": k1 - k0, "nccl_calls": n1 - n0},
+                "per_kernel": per_kernel, "clocks": clocks.summary(), "extras": extras}
+        print(json.dumps(line), flush=True)
+    grp.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_extras(args, local, h):
+    """configs[1]/[2] shapes with all workers on ONE GPU (node-emulated):
+    pull-gossip 8 x 10M and EASGD 8 x 25M; one fused kernel per round."""
+    import torch
+    from paper_1611_04581_b200 import _native as N
+    from paper_1611_04581_b200.engine import Group
+    out = {}
+    for name, proto, p, d, bpp in (("pull-gossip p=8 x 10M (1 GPU)", N.PULL_GOSSIP, 8, 10_000_000, 24),
+                                   ("elastic-avg p=8 x 25M (1 GPU)", N.ELASTIC_AVG, 8, 25_000_000, 20)):
+        try:
+            grp = Group(d, p, dtype="f32", device=local, center=(proto == N.ELASTIC_AVG))
+            gen = torch.Generator(device=f"cuda:{local}")
+            gen.manual_seed(7)
+            pool = [torch.randn(d, generator=gen, device=f"cuda:{local}") for _ in range(p * 2)]
+            for i in range(p):
+                grp.copy_in_async(i, N.BUF_THETA, pool[i].data_ptr(), d)
+            grp.sync()
+            if proto == N.ELASTIC_AVG:
+                grp.ea_init_center()
+            grp.seed_streams(1, "run/trial0")
+            ptrs = [t.data_ptr() for t in pool]
+            grp.run_rounds(proto, h, 3, grad_pool=ptrs)
+            grp.sync()
+            stream = torch.cuda.ExternalStream(grp.stream(), device=f"cuda:{local}")
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            k = 20
+            e0.record(stream)
+            grp.run_rounds(proto, h, k, grad_pool=ptrs)
+            e1.record(stream)
+            grp.sync()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / k
+            # EASGD: 8 clients x (theta, delta, g read + theta, delta write) + center R/W once
+            byts = p * d * bpp + (8 * d if proto == N.ELASTIC_AVG else 0)
+            out[name] = {"ms_per_round": ms, "param_updates_per_s": p * d / (ms * 1e-3),
+                         "hbm_gbs": byts / (ms * 1e-3) / 1e9,
+                         "bytes_per_param": byts / (p * d)}
+            grp.close()
+            del pool
+            torch.cuda.empty_cache()
+        except Exception as e:  # pragma: no cover
+            out[name] = {"error": str(e)}
+    return out
+
+
+def run_extras_dist(args, world, rank, local, h, max_over_ranks, barrier):
+    """Multi-GPU gossip (10M/worker, NVLink peer reads) and EASGD chain
+    (25M/worker, center on GPU0)."""
+    import torch
+    from paper_1611_04581_b200 import _native as N
+    from paper_1611_04581_b200.engine import Group
+    out = {}
+    for name, proto, d in (("pull-gossip 10M/worker", N.PULL_GOSSIP, 10_000_000),
+                           ("elastic-avg 25M/worker", N.ELASTIC_AVG, 25_000_000)):
+        try:
+            grp = Group.distributed(d, rank, world, local, dtype="f32", nccl=True,
+                                    center=(proto == N.ELASTIC_AVG))
+            gen = torch.Generator(device=f"cuda:{local}")
+            gen.manual_seed(7 + rank)
+            pool = [torch.randn(d, generator=gen, device=f"cuda:{local}") for _ in range(2)]
+            grp.copy_in_async(0, N.BUF_THETA, pool[0].data_ptr(), d)
+            grp.sync()
+            if proto == N.ELASTIC_AVG:
+                grp.ea_init_center()
+            grp.seed_streams(1, "run/trial0")
+            ptrs = [t.data_ptr() for t in pool]
+            grp.run_rounds(proto, h, 3, grad_pool=ptrs)
+            grp.sync()
+            barrier()
+            stream = torch.cuda.ExternalStream(grp.stream(), device=f"cuda:{local}")
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            k = 20
+            torch.cuda.synchronize()
+            barrier()
+            e0.record(stream)
+            grp.run_rounds(proto, h, k, grad_pool=ptrs)
+            e1.record(stream)
+            grp.sync()
+            torch.cuda.synchronize()
+            ms = max_over_ranks(e0.elapsed_time(e1)) / k
+            out[name] = {"ms_per_round": ms, "param_updates_per_s": world * d / (ms * 1e-3)}
+            barrier()
+            grp.close()
+            del pool
+            torch.cuda.empty_cache()
+        except Exception as e:  # pragma: no cover
+            out[name] = {"error": str(e)}
+    return out
+
+
+if __name__ == "__main__":
+    main()

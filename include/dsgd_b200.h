@@ -1,0 +1,309 @@
+/*
+ * dsgd_b200.h -- C ABI of the B200-native parameter-aggregation and update
+ * path of arXiv 1611.04581 (synchronous all-reduce SGD, elastic averaging SGD
+ * and gossiping SGD, all with Nesterov momentum).
+ *
+ * Drop-in boundary.  The reference has no FFI; its boundary is the C++
+ * update-rule interface /root/reference/proj/include/dsgd/protocols.hpp:45-152
+ * plus the per-step worker loops that call it
+ * (src/simulator.cpp:234-369 run_sync, src/transport.cpp:342-479
+ * run_transport worker).  Each entry point below names the reference
+ * function it replaces.  State lives on the device (SoA buffers per node);
+ * the host passes hyperparameters, partner maps and gate bits, exactly the
+ * arguments the reference functions take besides the NodeState vectors.
+ *
+ * Conventions
+ *  - Every function returns dsgd_status; no C++ exception crosses the ABI.
+ *    DSGD_EINVAL mirrors the reference's std::invalid_argument
+ *    (protocols.cpp:43-77, 198-202, 282-284), DSGD_ETIMEOUT its
+ *    TransportError (transport.hpp:57-60); dsgd_last_error() gives the text
+ *    (thread-local).
+ *  - A context (dsgd_ctx) is one process's view of one GPU; it hosts
+ *    n_local nodes (workers).  Group calls are lock-step: every context of a
+ *    group makes the same sequence of round calls (like NCCL collectives).
+ *    A group is either all p nodes in one context (p workers on one GPU) or
+ *    one node per context, one context per GPU (one process per GPU), wired
+ *    with dsgd_ctx_export_handle / dsgd_ctx_connect_peers (CUDA IPC peer
+ *    memory over NVLink) and dsgd_ctx_init_nccl.
+ *  - Arithmetic: DSGD_F64 reproduces the reference fp64 operation order
+ *    bit-for-bit (explicit round-to-nearest intrinsics, no FMA contraction);
+ *    DSGD_F32 runs the same operation order in binary32.
+ */
+#ifndef DSGD_B200_H_
+#define DSGD_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DSGD_B200_ABI_VERSION 1
+#define DSGD_MAX_LOCAL_NODES 32
+#define DSGD_HANDLE_BYTES 256 /* size of one dsgd_ctx_export_handle blob */
+#define DSGD_NCCL_ID_BYTES 128
+
+typedef enum {
+  DSGD_OK = 0,
+  DSGD_EINVAL = 1,   /* std::invalid_argument in the reference */
+  DSGD_ECUDA = 2,    /* CUDA runtime error */
+  DSGD_ENCCL = 3,    /* NCCL error */
+  DSGD_ETIMEOUT = 4, /* TransportError: a peer never arrived */
+  DSGD_ENOMEM = 5,
+  DSGD_ESTATE = 6 /* call out of order (e.g. peers not connected) */
+} dsgd_status;
+
+typedef enum { DSGD_F32 = 0, DSGD_F64 = 1 } dsgd_dtype;
+
+/* ProtocolKind core.hpp:31-39 (same numbering) */
+typedef enum {
+  DSGD_ALLREDUCE = 0,
+  DSGD_ELASTIC_AVG = 1,
+  DSGD_PULL_GOSSIP = 2,
+  DSGD_PUSH_GOSSIP = 3,
+  DSGD_GOSSIP_STALE = 4,
+  DSGD_GOSSIP_FRESH = 5,
+  DSGD_ASYNC_PULL = 6
+} dsgd_protocol;
+
+/* MomentumScope core.hpp:46 */
+typedef enum { DSGD_SCOPE_AGGREGATE = 0, DSGD_SCOPE_PER_NODE = 1 } dsgd_momentum_scope;
+
+/* StreamPurpose rng.hpp:30-37 */
+typedef enum {
+  DSGD_PURPOSE_NOISE = 0,
+  DSGD_PURPOSE_SAMPLE = 1,
+  DSGD_PURPOSE_PARTNER = 2,
+  DSGD_PURPOSE_CLOCK = 3,
+  DSGD_PURPOSE_STRAGGLER = 4,
+  DSGD_PURPOSE_INIT = 5
+} dsgd_purpose;
+
+/* Hyperparams core.hpp:54-70 (anneal_at sorted ascending, n_anneal entries) */
+typedef struct {
+  double alpha0;
+  double anneal_factor;
+  const uint64_t* anneal_at;
+  uint32_t n_anneal;
+  double mu;
+  double weight_decay;
+  double beta_gossip;
+  double beta_ea;
+  uint32_t tau;
+  uint32_t batch;
+} dsgd_hyperparams;
+
+const char* dsgd_last_error(void);
+int dsgd_abi_version(void);
+
+/* ------------------------------------------------------------------ host
+ * Deterministic streams: rng.hpp:50-95 / rng.cpp:24-112 (std::mt19937_64,
+ * explicit samplers).  Peer schedules are drawn on the host, bit-exact. */
+typedef struct dsgd_stream dsgd_stream;
+uint64_t dsgd_derive_stream_seed(uint64_t root_seed, const char* run_id, uint32_t node_id,
+                                 dsgd_purpose purpose);                 /* rng.cpp:93 */
+dsgd_status dsgd_stream_create(uint64_t engine_seed, dsgd_stream** out); /* RngStream(seed) */
+dsgd_status dsgd_stream_make(uint64_t root_seed, const char* run_id, uint32_t node_id,
+                             dsgd_purpose purpose, dsgd_stream** out); /* make_stream */
+dsgd_status dsgd_stream_clone(const dsgd_stream* s, dsgd_stream** out);
+void dsgd_stream_destroy(dsgd_stream* s);
+uint64_t dsgd_stream_next_u64(dsgd_stream* s);
+double dsgd_stream_uniform01(dsgd_stream* s);
+double dsgd_stream_normal(dsgd_stream* s);
+dsgd_status dsgd_stream_uniform_index(dsgd_stream* s, uint32_t n, uint32_t* out);
+dsgd_status dsgd_stream_exponential(dsgd_stream* s, double rate, double* out);
+/* NoiseModel::sample objectives.cpp:175-183: out[k] = sigma * normal() */
+void dsgd_stream_fill_normal(dsgd_stream* s, double sigma, double* out, uint64_t n);
+
+double dsgd_step_size_at(const dsgd_hyperparams* h, uint64_t t); /* core.cpp:82-92 */
+dsgd_status dsgd_hyperparams_validate(const dsgd_hyperparams* h); /* core.cpp:62-80 */
+/* draw_pull_partners / draw_push_targets simulator.cpp:69-88 */
+dsgd_status dsgd_draw_pull_partners(dsgd_stream* const* partner_streams, uint32_t p,
+                                    uint32_t* out);
+dsgd_status dsgd_draw_push_targets(dsgd_stream* const* partner_streams, uint32_t p,
+                                   uint32_t* out);
+
+/* --------------------------------------------------------------- context */
+typedef struct dsgd_ctx dsgd_ctx;
+
+enum {
+  DSGD_CTX_QUADRATIC = 1u << 0, /* device-resident diagonal quadratic objective (s, opt) */
+  DSGD_CTX_GRAD = 1u << 1,      /* own gradient buffer per node (DSGD_BUF_GRAD) */
+  DSGD_CTX_NOISE = 1u << 2,     /* own additive-noise buffer per node (DSGD_BUF_NOISE) */
+  DSGD_CTX_CENTER = 1u << 3     /* EASGD center (on the context hosting node 0) */
+};
+
+typedef struct {
+  int device;
+  uint64_t dim;        /* d */
+  dsgd_dtype dtype;
+  uint32_t p;          /* nodes in the whole group */
+  uint32_t first_node; /* global id of this context's node 0 */
+  uint32_t n_local;    /* nodes hosted here (p, or 1 with one context per GPU) */
+  uint32_t flags;      /* DSGD_CTX_* */
+  void* stream;        /* cudaStream_t to launch on; NULL: the context creates one */
+} dsgd_ctx_desc;
+
+dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out);
+void dsgd_ctx_destroy(dsgd_ctx* ctx);
+dsgd_status dsgd_ctx_stream(dsgd_ctx* ctx, void** stream);
+/* Waits for the context's stream and reports device-side failures (a peer
+ * timeout inside a kernel -> DSGD_ETIMEOUT). */
+dsgd_status dsgd_ctx_sync(dsgd_ctx* ctx);
+
+/* Buffers (device pointers, dtype elements, d per node). */
+typedef enum {
+  DSGD_BUF_THETA = 0, /* current parameters */
+  DSGD_BUF_DELTA = 1, /* delta_prev (momentum memory) */
+  DSGD_BUF_GRAD = 2,
+  DSGD_BUF_NOISE = 3,
+  DSGD_BUF_SPECTRUM = 4,
+  DSGD_BUF_OPT = 5,
+  DSGD_BUF_CENTER = 6
+} dsgd_buffer;
+dsgd_status dsgd_buffer_ptr(dsgd_ctx* ctx, uint32_t local, dsgd_buffer which, void** dev);
+
+/* NodeState io: host fp64 vectors converted to the context dtype. */
+dsgd_status dsgd_set_state(dsgd_ctx* ctx, uint32_t local, const double* theta,
+                           const double* delta_prev, uint64_t t);
+dsgd_status dsgd_get_state(dsgd_ctx* ctx, uint32_t local, double* theta, double* delta_prev,
+                           uint64_t* t);
+dsgd_status dsgd_set_vector(dsgd_ctx* ctx, uint32_t local, dsgd_buffer which,
+                            const double* host);
+dsgd_status dsgd_get_vector(dsgd_ctx* ctx, uint32_t local, dsgd_buffer which, double* host);
+/* Raw asynchronous copies in the context dtype on the context stream (host
+ * memory should be pinned); used by the end-to-end path. */
+dsgd_status dsgd_upload_async(dsgd_ctx* ctx, uint32_t local, dsgd_buffer which,
+                              const void* host, uint64_t count);
+dsgd_status dsgd_download_async(dsgd_ctx* ctx, uint32_t local, dsgd_buffer which, void* host,
+                                uint64_t count);
+/* Copy `count` elements from any device/pinned pointer (cudaMemcpyDefault)
+ * into a context buffer on the context stream, e.g. parameters held by a
+ * framework tensor. */
+dsgd_status dsgd_copy_in_async(dsgd_ctx* ctx, uint32_t local, dsgd_buffer which,
+                               const void* src, uint64_t count);
+dsgd_status dsgd_get_t(dsgd_ctx* ctx, uint32_t local, uint64_t* t);
+dsgd_status dsgd_set_t(dsgd_ctx* ctx, uint32_t local, uint64_t t);
+
+/* ------------------------------------------------------- gradient source
+ * The reference's Objective plugin (objectives.hpp:33-53) evaluated at the
+ * lookahead point theta + mu*delta_prev.  DSGD_GRAD_QUADRATIC evaluates
+ * QuadraticObjective::gradient (objectives.cpp:71-78) inside the update
+ * kernel; DSGD_GRAD_BUFFER reads a per-node device buffer holding the
+ * minibatch gradient (the caller's model fills it).  Weight decay and the
+ * additive noise draw are always applied inside the kernel, in the
+ * reference order (protocols.cpp:27-38, 98). */
+typedef enum { DSGD_GRAD_QUADRATIC = 0, DSGD_GRAD_BUFFER = 1 } dsgd_grad_source;
+
+typedef struct {
+  dsgd_grad_source source;
+  const void* const* grad; /* GRAD_BUFFER: n_local device pointers, or NULL for DSGD_BUF_GRAD */
+  uint32_t use_noise;      /* 1: add DSGD_BUF_NOISE (NoiseModel gaussian); 0: add +0.0 (zero kind) */
+  double* grad_norm_out;   /* optional: raised to max_i ||g_i|| like protocols.cpp:34-36 (syncs) */
+} dsgd_grad_spec;
+
+/* ----------------------------------------------------------- update rules
+ * All are lock-step over every node of the group and advance each node's t. */
+
+/* local_sgd_step protocols.cpp:102-108, on every node */
+dsgd_status dsgd_local_sgd_step(dsgd_ctx* ctx, const dsgd_hyperparams* h,
+                                const dsgd_grad_spec* g);
+/* allreduce_round protocols.cpp:110-131 (one context: pivot-form
+ * spatial_mean, bit-exact with param_vec.cpp:19-40; one context per GPU:
+ * ncclAllReduce over NVLink between a fused delta kernel and a fused apply
+ * kernel, replacing ring_allreduce transport.cpp:183-248). */
+dsgd_status dsgd_allreduce_round(dsgd_ctx* ctx, const dsgd_hyperparams* h,
+                                 const dsgd_grad_spec* g, dsgd_momentum_scope scope);
+/* Synchronous EASGD sweep simulator.cpp:332-351 = ea_client_step
+ * protocols.cpp:140-153 + ea_server_apply 155-159 in node order; center on
+ * the context hosting node 0.  gated = (t > 0 && t % tau == 0). */
+dsgd_status dsgd_ea_round(dsgd_ctx* ctx, const dsgd_hyperparams* h, const dsgd_grad_spec* g,
+                          int gated);
+/* pull_gossip_round protocols.cpp:173-185 (partner_of: p entries);
+ * partner_of == NULL runs the ungated branch (local step on every node). */
+dsgd_status dsgd_pull_gossip_round(dsgd_ctx* ctx, const dsgd_hyperparams* h,
+                                   const dsgd_grad_spec* g, const uint32_t* partner_of);
+/* push_gossip_round protocols.cpp:230-242 (target_of: p entries, no self) */
+dsgd_status dsgd_push_gossip_round(dsgd_ctx* ctx, const dsgd_hyperparams* h,
+                                   const dsgd_grad_spec* g, const uint32_t* target_of);
+/* gated gossip-stale round simulator.cpp:283-292 (gossip_stale_step 252-263) */
+dsgd_status dsgd_gossip_stale_round(dsgd_ctx* ctx, const dsgd_hyperparams* h,
+                                    const dsgd_grad_spec* g, const uint32_t* partner_of);
+/* gated gossip-fresh round simulator.cpp:305-319 (gossip_fresh_step 271-276) */
+dsgd_status dsgd_gossip_fresh_round(dsgd_ctx* ctx, const dsgd_hyperparams* h,
+                                    const dsgd_grad_spec* g, const uint32_t* partner_of);
+/* async_pull_event protocols.cpp:278-297 (nodes i, j global ids; one context) */
+dsgd_status dsgd_async_pull_event(dsgd_ctx* ctx, const dsgd_hyperparams* h,
+                                  const dsgd_grad_spec* g, uint32_t i, uint32_t j);
+/* pull_mix 161-171 / push_mix 195-228 without the SGD step */
+dsgd_status dsgd_pull_mix(dsgd_ctx* ctx, const uint32_t* partner_of);
+dsgd_status dsgd_push_mix(dsgd_ctx* ctx, const uint32_t* target_of);
+/* gossip_fresh_mix protocols.cpp:265-269 (mix_toward with beta, no step) */
+dsgd_status dsgd_gossip_fresh_mix(dsgd_ctx* ctx, const uint32_t* partner_of, double beta);
+/* ea_client_step's update output: when update_out != NULL (n_local device
+ * pointers), the next dsgd_ea_round on a single context also writes each
+ * client's update u_i = beta*(theta_i - c) there. */
+dsgd_status dsgd_ea_set_update_out(dsgd_ctx* ctx, void* const* update_out);
+/* ea_server_apply protocols.cpp:155-159: center += update (device vector) */
+dsgd_status dsgd_ea_server_apply(dsgd_ctx* ctx, const void* update);
+/* EASGD center = spatial_mean of the nodes' current theta (simulator.cpp:62-67) */
+dsgd_status dsgd_ea_init_center(dsgd_ctx* ctx);
+
+/* ------------------------------------------------------ per-step worker loop
+ * run_sync simulator.cpp:234-369 / the run_transport worker
+ * transport.cpp:342-479, per context: alpha from step_size_at, the gate,
+ * partner draws from the reference partner streams (all p, so every
+ * context knows the full map), optional reference noise drawn on the host
+ * and uploaded, the protocol's fused kernels.  Streams are keyed by
+ * (seed, run_id) and persist in the context across calls. */
+typedef struct {
+  dsgd_protocol protocol;
+  dsgd_hyperparams hyper;
+  dsgd_momentum_scope scope;
+  dsgd_grad_spec grad;
+  uint32_t n_grad_pool;          /* >0: round r reads grad_pool[(r % n) * n_local + i] */
+  const void* const* grad_pool;
+  double host_noise_sigma;       /* >0: reference Gaussian noise drawn on the host per step */
+  uint64_t rounds;
+} dsgd_run_desc;
+dsgd_status dsgd_ctx_seed_streams(dsgd_ctx* ctx, uint64_t seed, const char* run_id);
+dsgd_status dsgd_run_rounds(dsgd_ctx* ctx, const dsgd_run_desc* run);
+dsgd_status dsgd_ctx_round(dsgd_ctx* ctx, uint64_t* round); /* rounds completed */
+
+/* ---------------------------------------------- multi-GPU group wiring
+ * One context per GPU (n_local == 1).  Each context exports a fixed-size
+ * blob (CUDA IPC handle of its state arena + layout); the host exchanges
+ * blobs out of band (e.g. torch.distributed all_gather) and connects. */
+dsgd_status dsgd_ctx_export_handle(dsgd_ctx* ctx, void* blob /* DSGD_HANDLE_BYTES */);
+dsgd_status dsgd_ctx_connect_peers(dsgd_ctx* ctx, const void* blobs /* p blobs */);
+dsgd_status dsgd_nccl_unique_id(void* id /* DSGD_NCCL_ID_BYTES */);
+dsgd_status dsgd_ctx_init_nccl(dsgd_ctx* ctx, const void* id, int rank, int nranks);
+/* Spin-wait bound for cross-GPU flags (default 10 s). */
+dsgd_status dsgd_ctx_set_timeout(dsgd_ctx* ctx, double seconds);
+
+/* ----------------------------------------------------------- measurement */
+typedef enum {
+  DSGD_K_STEP = 0,       /* fused local step / pull / stale / mix kernels */
+  DSGD_K_ALLREDUCE = 1,  /* single-context fused all-reduce round */
+  DSGD_K_AR_DELTA = 2,   /* multi-GPU all-reduce: delta kernel */
+  DSGD_K_AR_APPLY = 3,   /* multi-GPU all-reduce: apply kernel */
+  DSGD_K_NCCL = 4,       /* ncclAllReduce */
+  DSGD_K_EA = 5,         /* EASGD fused chain */
+  DSGD_K_PUSH = 6,
+  DSGD_K_OTHER = 7,
+  DSGD_K_COUNT = 8
+} dsgd_kernel_id;
+/* When enabled, every launch is bracketed by CUDA events on the context
+ * stream; read accumulates device time per kernel id (and syncs). */
+dsgd_status dsgd_profile_enable(dsgd_ctx* ctx, int enable);
+dsgd_status dsgd_profile_read(dsgd_ctx* ctx, dsgd_kernel_id k, double* total_ms,
+                              uint64_t* launches, int reset);
+/* Number of kernels (and NCCL calls) this context has launched. */
+dsgd_status dsgd_launch_count(dsgd_ctx* ctx, uint64_t* kernels, uint64_t* nccl_calls);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DSGD_B200_H_ */

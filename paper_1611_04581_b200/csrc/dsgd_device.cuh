@@ -1,0 +1,161 @@
+// dsgd_device.cuh -- device-side building blocks of the B200 update path.
+//
+// * Reference-order arithmetic: every operation of the reference update
+//   rules (protocols.cpp, core.cpp:101, param_vec.cpp) is one explicitly
+//   rounded IEEE op (__fadd_rn/__dmul_rn ...), so nvcc can never contract
+//   a*b+c into an FMA.  The fp64 instantiation therefore reproduces the
+//   reference bit-for-bit and the fp32 one is the same operation order in
+//   binary32 (checked against oracle/ in tests/).
+// * 128-bit vector access (float4 / double2) for the streaming kernels.
+// * Cross-GPU flags: acquire/release at system scope over NVLink-mapped
+//   peer memory, bounded by %globaltimer so a dead peer turns into
+//   DSGD_ETIMEOUT instead of a hung GPU.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dsgd {
+
+constexpr int kMaxLocal = 32;  // == DSGD_MAX_LOCAL_NODES
+constexpr int kMaxWait = 16;
+constexpr int kBlock = 256;
+
+// ---------------------------------------------------------------- arithmetic
+__device__ __forceinline__ float radd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float rsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float rmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float rdiv(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double radd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double rsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double rmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double rdiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// ------------------------------------------------------------ 128-bit vectors
+template <typename T>
+struct Vec {
+  static constexpr int N = 16 / sizeof(T);
+  union {
+    uint4 u;
+    T t[N];
+  };
+};
+
+template <typename T>
+__device__ __forceinline__ Vec<T> ld_vec(const T* p) {  // coherent load (may be written elsewhere)
+  Vec<T> v;
+  v.u = *reinterpret_cast<const uint4*>(p);
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ Vec<T> ld_vec_stream(const T* p) {  // read-once input, evict first
+  Vec<T> v;
+  v.u = __ldcs(reinterpret_cast<const uint4*>(p));
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ Vec<T> ld_vec_ro(const T* p) {  // read-only for the kernel
+  Vec<T> v;
+  v.u = __ldg(reinterpret_cast<const uint4*>(p));
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ void st_vec(T* p, const Vec<T>& v) {
+  *reinterpret_cast<uint4*>(p) = v.u;
+}
+
+// ------------------------------------------------------- cross-GPU flags
+struct WaitSpec {
+  const unsigned long long* ptr[kMaxWait];
+  unsigned long long val[kMaxWait];
+  int n;
+  unsigned long long timeout_ns;
+  unsigned int* error;
+};
+
+struct SignalSpec {
+  unsigned long long* counter;  // own round counter (IPC-visible); null: no signal
+  unsigned long long value;
+  unsigned int* arrive;         // grid arrival counter (own device memory)
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// One thread per CTA polls the flags; the barrier then orders every thread's
+// later peer loads after the acquire.  Returns false on timeout (the error
+// flag is raised and the CTA must skip its work).
+__device__ __forceinline__ bool wait_flag(const unsigned long long* p, unsigned long long need,
+                                          unsigned long long timeout_ns, unsigned int* error) {
+  if (ld_acquire_sys(p) >= need) return true;
+  const unsigned long long t0 = globaltimer();
+  unsigned ns = 32;
+  while (ld_acquire_sys(p) < need) {
+    if (globaltimer() - t0 > timeout_ns) {
+      atomicExch(error, 1u);
+      return false;
+    }
+    __nanosleep(ns);
+    if (ns < 1024) ns <<= 1;
+  }
+  return true;
+}
+
+__device__ __forceinline__ bool block_wait(const WaitSpec& w) {
+  if (w.n == 0) return true;
+  __shared__ int ok;
+  if (threadIdx.x == 0) {
+    int good = 1;
+    for (int i = 0; i < w.n && good; ++i) good = wait_flag(w.ptr[i], w.val[i], w.timeout_ns, w.error);
+    ok = good;
+  }
+  __syncthreads();
+  return ok != 0;
+}
+
+// Every CTA fences its writes at system scope and arrives; the last one to
+// arrive publishes the round counter with a release store.
+__device__ __forceinline__ void block_signal(const SignalSpec& s) {
+  if (s.counter == nullptr) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const unsigned total = gridDim.x * gridDim.y;
+    const unsigned prev = atomicAdd(s.arrive, 1u);
+    if (prev == total - 1) {
+      atomicExch(s.arrive, 0u);
+      __threadfence_system();
+      st_release_sys(s.counter, s.value);
+    }
+  }
+}
+
+// ------------------------------------------------------------ reductions
+__device__ __forceinline__ void block_add_double(double v, double* out) {
+  if (out == nullptr) return;
+  __shared__ double part[kBlock / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) part[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < (int)(blockDim.x >> 5) ? part[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) atomicAdd(out, v);
+  }
+}
+
+}  // namespace dsgd

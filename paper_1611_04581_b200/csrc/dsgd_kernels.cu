@@ -1,0 +1,644 @@
+// dsgd_kernels.cu -- sm_100a kernels of the B200 aggregation/update path.
+//
+// All kernels are HBM-streaming, elementwise-parallel over the parameter
+// dimension d (the work is 0.3-0.5 flop/byte, so tensor cores are
+// irrelevant): 128-bit vectorised coalesced loads/stores, grid-stride over a
+// grid sized to the SM count, every reference pass of a round fused into one
+// sweep over HBM.  The per-element arithmetic is written once (sgd_delta,
+// mix) in the reference's exact operation order; see dsgd_device.cuh.
+#include "dsgd_kernels.cuh"
+
+namespace dsgd {
+
+// compute_local_delta protocols.cpp:85-100 for one coordinate:
+//   la = mu != 0 ? theta + mu*delta_prev : theta          (92-93)
+//   g  = obj.stochastic_gradient(la)                       (30; quadratic: objectives.cpp:75)
+//   g += wd*la  if wd > 0                                  (31-33)
+//   g += xi     (the zero noise kind still adds +0)        (98)
+//   delta = mu*delta_prev - alpha*g                        (core.cpp:101)
+template <typename T>
+__device__ __forceinline__ T sgd_delta(T x, T dp, T gb, T s, T o, T xi, T alpha, T mu, T wd,
+                                       int mu_nz, int wd_pos, int quad, bool norm, double& nacc) {
+  const T la = mu_nz ? radd(x, rmul(mu, dp)) : x;
+  T g = quad ? rmul(s, rsub(la, o)) : gb;
+  if (wd_pos) g = radd(g, rmul(wd, la));
+  if (norm) nacc += (double)g * (double)g;
+  g = radd(g, xi);
+  return rsub(rmul(mu, dp), rmul(alpha, g));
+}
+
+// mix_toward protocols.cpp:42-51: own + beta*(other - own), centred so that
+// other == own leaves own bit-exactly unchanged.
+template <typename T>
+__device__ __forceinline__ T mix(T own, T other, T beta) {
+  return radd(own, rmul(beta, rsub(other, own)));
+}
+
+// ------------------------------------------------------------------ loads
+template <typename T, bool VEC>
+struct Lanes {
+  static constexpr int W = VEC ? Vec<T>::N : 1;
+  T v[W];
+};
+
+template <typename T, bool VEC>
+__device__ __forceinline__ void ld(Lanes<T, VEC>& r, const T* p, uint64_t k) {
+  if constexpr (VEC) {
+    Vec<T> t = ld_vec(p + k);
+#pragma unroll
+    for (int l = 0; l < Vec<T>::N; ++l) r.v[l] = t.t[l];
+  } else {
+    r.v[0] = p[k];
+  }
+}
+template <typename T, bool VEC>
+__device__ __forceinline__ void ld_stream(Lanes<T, VEC>& r, const T* p, uint64_t k) {
+  if constexpr (VEC) {
+    Vec<T> t = ld_vec_stream(p + k);
+#pragma unroll
+    for (int l = 0; l < Vec<T>::N; ++l) r.v[l] = t.t[l];
+  } else {
+    r.v[0] = __ldcs(p + k);
+  }
+}
+template <typename T, bool VEC>
+__device__ __forceinline__ void ld_ro(Lanes<T, VEC>& r, const T* p, uint64_t k) {
+  if constexpr (VEC) {
+    Vec<T> t = ld_vec_ro(p + k);
+#pragma unroll
+    for (int l = 0; l < Vec<T>::N; ++l) r.v[l] = t.t[l];
+  } else {
+    r.v[0] = __ldg(p + k);
+  }
+}
+template <typename T, bool VEC>
+__device__ __forceinline__ void st(T* p, uint64_t k, const Lanes<T, VEC>& r) {
+  if constexpr (VEC) {
+    Vec<T> t;
+#pragma unroll
+    for (int l = 0; l < Vec<T>::N; ++l) t.t[l] = r.v[l];
+    st_vec(p + k, t);
+  } else {
+    p[k] = r.v[0];
+  }
+}
+template <typename T, bool VEC>
+__device__ __forceinline__ void zero(Lanes<T, VEC>& r) {
+#pragma unroll
+  for (int l = 0; l < Lanes<T, VEC>::W; ++l) r.v[l] = T(0);
+}
+
+// Gradient-source inputs of one coordinate group.
+template <typename T, bool VEC>
+__device__ __forceinline__ void ld_grad_inputs(Lanes<T, VEC>& gb, Lanes<T, VEC>& s,
+                                               Lanes<T, VEC>& o, Lanes<T, VEC>& xi,
+                                               const T* grad, const T* spec, const T* opt,
+                                               const T* noise, int quad, uint64_t k) {
+  if (quad) {
+    ld_ro(s, spec, k);
+    ld_ro(o, opt, k);
+  } else {
+    ld_stream(gb, grad, k);
+  }
+  if (noise != nullptr) {
+    ld_stream(xi, noise, k);
+  } else {
+    zero(xi);
+  }
+}
+
+// ------------------------------------------------- fused gossip-family step
+template <typename T, int MODE, bool VEC>
+__device__ __forceinline__ void step_group(const StepArgs<T>& a, const NodeIO<T>& n, uint64_t k,
+                                           bool norm, double& nacc) {
+  using L = Lanes<T, VEC>;
+  constexpr int W = L::W;
+  L x, dp, gb, s, o, xi, xj, ax, out_t, out_d;
+  ld(x, n.theta_in, k);
+  if constexpr (MODE == kModePull || MODE == kModeStale || MODE == kModeMix || MODE == kModeAsync)
+    ld(xj, n.partner, k);
+  if constexpr (MODE == kModeApply) ld(ax, n.aux, k);
+  if constexpr (MODE == kModeStep || MODE == kModePull || MODE == kModeStale ||
+                MODE == kModeArDelta)
+    ld(dp, n.delta, k);
+  if constexpr (MODE != kModeMix && MODE != kModeApply)
+    ld_grad_inputs(gb, s, o, xi, n.grad, a.spec, a.opt, n.noise, a.quad, k);
+#pragma unroll
+  for (int l = 0; l < W; ++l) {
+    if constexpr (MODE == kModeStep) {
+      const T dl = sgd_delta(x.v[l], dp.v[l], gb.v[l], s.v[l], o.v[l], xi.v[l], n.alpha, a.mu,
+                             a.wd, a.mu_nz, a.wd_pos, a.quad, norm, nacc);
+      out_d.v[l] = dl;
+      out_t.v[l] = radd(x.v[l], dl);  // theta += delta_prev  (param_vec.hpp:49)
+    } else if constexpr (MODE == kModePull) {
+      const T m = mix(x.v[l], xj.v[l], a.beta);
+      const T dl = sgd_delta(m, dp.v[l], gb.v[l], s.v[l], o.v[l], xi.v[l], n.alpha, a.mu, a.wd,
+                             a.mu_nz, a.wd_pos, a.quad, norm, nacc);
+      out_d.v[l] = dl;
+      out_t.v[l] = radd(m, dl);
+    } else if constexpr (MODE == kModeStale) {
+      const T dl = sgd_delta(x.v[l], dp.v[l], gb.v[l], s.v[l], o.v[l], xi.v[l], n.alpha, a.mu,
+                             a.wd, a.mu_nz, a.wd_pos, a.quad, norm, nacc);
+      out_d.v[l] = dl;
+      out_t.v[l] = radd(mix(x.v[l], xj.v[l], a.beta), dl);
+    } else if constexpr (MODE == kModeMix) {
+      out_t.v[l] = mix(x.v[l], xj.v[l], a.beta);
+    } else if constexpr (MODE == kModeArDelta) {
+      out_d.v[l] = sgd_delta(x.v[l], dp.v[l], gb.v[l], s.v[l], o.v[l], xi.v[l], n.alpha, a.mu,
+                             a.wd, a.mu_nz, a.wd_pos, a.quad, norm, nacc);
+    } else if constexpr (MODE == kModeApply) {
+      out_t.v[l] = radd(x.v[l], ax.v[l]);
+    } else {  // kModeAsync: no lookahead, no momentum; y = x + (-alpha)*g
+      T g = a.quad ? rmul(s.v[l], rsub(x.v[l], o.v[l])) : gb.v[l];
+      if (a.wd_pos) g = radd(g, rmul(a.wd, x.v[l]));
+      if (norm) nacc += (double)g * (double)g;
+      g = radd(g, xi.v[l]);
+      const T y = radd(x.v[l], rmul(n.alpha, g));  // alpha carries the sign (-alpha)
+      out_t.v[l] = mix(y, xj.v[l], a.beta);
+    }
+  }
+  if constexpr (MODE == kModeArDelta) {
+    st(n.aux, k, out_d);
+    if (n.aux != n.delta) st(n.delta, k, out_d);  // per-node scope keeps the own delta
+  } else {
+    st(n.theta_out, k, out_t);
+    if constexpr (MODE == kModeStep || MODE == kModePull || MODE == kModeStale)
+      st(n.delta, k, out_d);
+  }
+}
+
+template <typename T, int MODE, bool VEC>
+__global__ void __launch_bounds__(kBlock) k_step(const __grid_constant__ StepArgs<T> a) {
+  if (!block_wait(a.wait)) return;
+  const uint32_t node = blockIdx.x / a.blocks_per_node;
+  const uint32_t bid = blockIdx.x - node * a.blocks_per_node;
+  const NodeIO<T>& n = a.node[node];
+  const bool norm = n.norm != nullptr;
+  double nacc = 0.0;
+  constexpr int W = Lanes<T, VEC>::W;
+  const uint64_t nv = a.d / W;
+  const uint64_t stride = (uint64_t)a.blocks_per_node * blockDim.x;
+  const uint64_t first = (uint64_t)bid * blockDim.x + threadIdx.x;
+  // two independent groups per iteration keep 2x the bytes in flight
+  uint64_t v = first;
+  for (; v + stride < nv; v += 2 * stride) {
+    step_group<T, MODE, VEC>(a, n, v * W, norm, nacc);
+    step_group<T, MODE, VEC>(a, n, (v + stride) * W, norm, nacc);
+  }
+  if (v < nv) step_group<T, MODE, VEC>(a, n, v * W, norm, nacc);
+  if constexpr (VEC) {
+    for (uint64_t k = nv * W + first; k < a.d; k += stride)
+      step_group<T, MODE, false>(a, n, k, norm, nacc);
+  }
+  block_add_double(nacc, n.norm);
+  block_signal(a.signal);
+}
+
+template <typename T>
+cudaError_t launch_step(int mode, const StepArgs<T>& a, int vec, uint32_t grid, cudaStream_t s) {
+#define DSGD_STEP_CASE(M)                                                   \
+  case M:                                                                   \
+    if (vec)                                                                \
+      k_step<T, M, true><<<grid, kBlock, 0, s>>>(a);                        \
+    else                                                                    \
+      k_step<T, M, false><<<grid, kBlock, 0, s>>>(a);                       \
+    break;
+  switch (mode) {
+    DSGD_STEP_CASE(kModeStep)
+    DSGD_STEP_CASE(kModePull)
+    DSGD_STEP_CASE(kModeStale)
+    DSGD_STEP_CASE(kModeMix)
+    DSGD_STEP_CASE(kModeArDelta)
+    DSGD_STEP_CASE(kModeApply)
+    DSGD_STEP_CASE(kModeAsync)
+    default:
+      return cudaErrorInvalidValue;
+  }
+#undef DSGD_STEP_CASE
+  return cudaGetLastError();
+}
+
+// ------------------------------------------- single-context all-reduce round
+// allreduce_round protocols.cpp:110-131 for p nodes on one GPU, one pass:
+// every node's delta, the pivot-form mean of param_vec.cpp:26-38
+//   dev = 0; dev += (d_i - d_0) for i = 1..p-1; avg = d_0 + dev * (1/p)
+// and the apply theta_i += avg, delta_prev_i = aggregate ? avg : d_i.
+template <typename T, bool VEC, bool NORM>
+__global__ void __launch_bounds__(kBlock) k_allreduce_local(const __grid_constant__ AllreduceArgs<T> a) {
+  using L = Lanes<T, VEC>;
+  constexpr int W = L::W;
+  double nacc[NORM ? kMaxLocal : 1];
+  if constexpr (NORM)
+    for (uint32_t i = 0; i < a.p; ++i) nacc[i] = 0.0;
+  const uint64_t nv = a.d / W;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += stride) {
+    const uint64_t k = v * W;
+    L d0, dev, avg;
+    zero(dev);
+    for (uint32_t i = 0; i < a.p; ++i) {
+      const NodeIO<T>& n = a.node[i];
+      L x, dp, gb, s, o, xi, di;
+      ld(x, n.theta_in, k);
+      ld(dp, n.delta, k);
+      ld_grad_inputs(gb, s, o, xi, n.grad, a.spec, a.opt, n.noise, a.quad, k);
+      double dummy = 0.0;
+#pragma unroll
+      for (int l = 0; l < W; ++l) {
+        di.v[l] = sgd_delta(x.v[l], dp.v[l], gb.v[l], s.v[l], o.v[l], xi.v[l], n.alpha, a.mu,
+                            a.wd, a.mu_nz, a.wd_pos, a.quad, NORM, NORM ? nacc[i] : dummy);
+        if (i == 0)
+          d0.v[l] = di.v[l];
+        else
+          dev.v[l] = radd(dev.v[l], rsub(di.v[l], d0.v[l]));
+      }
+      if (a.per_node) st(n.delta, k, di);
+    }
+#pragma unroll
+    for (int l = 0; l < W; ++l) avg.v[l] = radd(d0.v[l], rmul(dev.v[l], a.inv_p));
+    for (uint32_t i = 0; i < a.p; ++i) {
+      const NodeIO<T>& n = a.node[i];
+      L x, out;
+      ld(x, n.theta_in, k);
+#pragma unroll
+      for (int l = 0; l < W; ++l) out.v[l] = radd(x.v[l], avg.v[l]);
+      st(n.theta_out, k, out);
+      if (!a.per_node) st(n.delta, k, avg);
+    }
+  }
+  if constexpr (NORM)
+    for (uint32_t i = 0; i < a.p; ++i) block_add_double(nacc[i], a.node[i].norm);
+}
+
+template <typename T>
+cudaError_t launch_allreduce_local(const AllreduceArgs<T>& a, int vec, int norm, uint32_t grid,
+                                   cudaStream_t s) {
+  // the vector kernel covers d - d % W; a scalar launch finishes the tail
+  if (vec) {
+    if (norm)
+      k_allreduce_local<T, true, true><<<grid, kBlock, 0, s>>>(a);
+    else
+      k_allreduce_local<T, true, false><<<grid, kBlock, 0, s>>>(a);
+    const uint64_t W = Vec<T>::N, head = (a.d / W) * W;
+    if (head != a.d) {
+      AllreduceArgs<T> t = a;
+      for (uint32_t i = 0; i < a.p; ++i) {
+        NodeIO<T>& n = t.node[i];
+        n.theta_in += head;
+        n.theta_out += head;
+        n.delta += head;
+        if (n.grad) n.grad += head;
+        if (n.noise) n.noise += head;
+      }
+      if (t.spec) t.spec += head;
+      if (t.opt) t.opt += head;
+      t.d = a.d - head;
+      if (norm)
+        k_allreduce_local<T, false, true><<<1, kBlock, 0, s>>>(t);
+      else
+        k_allreduce_local<T, false, false><<<1, kBlock, 0, s>>>(t);
+    }
+  } else {
+    if (norm)
+      k_allreduce_local<T, false, true><<<grid, kBlock, 0, s>>>(a);
+    else
+      k_allreduce_local<T, false, false><<<grid, kBlock, 0, s>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+// -------------------------------------------------- single-context EASGD
+// Synchronous sweep simulator.cpp:335-346 fused over the p clients: per
+// coordinate the center is one register carried through the clients in node
+// order -- u = beta*(theta_i - c); theta_i -= u; SGD step; c += u
+// (protocols.cpp:148-151, 156) -- so the serial server order costs nothing.
+template <typename T, bool VEC, bool NORM>
+__global__ void __launch_bounds__(kBlock) k_ea_local(const __grid_constant__ EaArgs<T> a) {
+  using L = Lanes<T, VEC>;
+  constexpr int W = L::W;
+  double nacc[NORM ? kMaxLocal : 1];
+  if constexpr (NORM)
+    for (uint32_t i = 0; i < a.p; ++i) nacc[i] = 0.0;
+  const uint64_t nv = a.d / W;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += stride) {
+    const uint64_t k = v * W;
+    L c;
+    ld(c, a.center, k);
+    for (uint32_t i = 0; i < a.p; ++i) {
+      const NodeIO<T>& n = a.node[i];
+      L x, dp, gb, s, o, xi, ot, od, uo;
+      ld(x, n.theta_in, k);
+      ld(dp, n.delta, k);
+      ld_grad_inputs(gb, s, o, xi, n.grad, a.spec, a.opt, n.noise, a.quad, k);
+      double dummy = 0.0;
+#pragma unroll
+      for (int l = 0; l < W; ++l) {
+        T xv = x.v[l];
+        T u = T(0);
+        if (a.gated) {
+          u = rmul(a.beta, rsub(xv, c.v[l]));
+          xv = rsub(xv, u);
+        }
+        const T dl = sgd_delta(xv, dp.v[l], gb.v[l], s.v[l], o.v[l], xi.v[l], n.alpha, a.mu, a.wd,
+                               a.mu_nz, a.wd_pos, a.quad, NORM, NORM ? nacc[i] : dummy);
+        od.v[l] = dl;
+        ot.v[l] = radd(xv, dl);
+        uo.v[l] = u;
+        if (a.gated) c.v[l] = radd(c.v[l], u);
+      }
+      st(n.theta_out, k, ot);
+      st(n.delta, k, od);
+      if (n.aux) st(n.aux, k, uo);  // the client's update (ea_client_step's second result)
+    }
+    if (a.gated) st(a.center, k, c);
+  }
+  if constexpr (NORM)
+    for (uint32_t i = 0; i < a.p; ++i) block_add_double(nacc[i], a.node[i].norm);
+}
+
+template <typename T>
+cudaError_t launch_ea_local(const EaArgs<T>& a, int vec, int norm, uint32_t grid, cudaStream_t s) {
+  if (vec) {
+    if (norm)
+      k_ea_local<T, true, true><<<grid, kBlock, 0, s>>>(a);
+    else
+      k_ea_local<T, true, false><<<grid, kBlock, 0, s>>>(a);
+    const uint64_t W = Vec<T>::N, head = (a.d / W) * W;
+    if (head != a.d) {
+      EaArgs<T> t = a;
+      for (uint32_t i = 0; i < a.p; ++i) {
+        NodeIO<T>& n = t.node[i];
+        n.theta_in += head;
+        n.theta_out += head;
+        n.delta += head;
+        if (n.grad) n.grad += head;
+        if (n.noise) n.noise += head;
+        if (n.aux) n.aux += head;
+      }
+      if (t.spec) t.spec += head;
+      if (t.opt) t.opt += head;
+      t.center += head;
+      t.d = a.d - head;
+      if (norm)
+        k_ea_local<T, false, true><<<1, kBlock, 0, s>>>(t);
+      else
+        k_ea_local<T, false, false><<<1, kBlock, 0, s>>>(t);
+    }
+  } else {
+    if (norm)
+      k_ea_local<T, false, true><<<grid, kBlock, 0, s>>>(a);
+    else
+      k_ea_local<T, false, false><<<grid, kBlock, 0, s>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------- push gossip
+// push_mix protocols.cpp:207-225 then the step: acc = 0; acc += x_k - x_i
+// over senders k ascending; mixed = x_i + acc * (1/count).
+template <typename T, bool VEC>
+__device__ __forceinline__ void push_group(const PushArgs<T>& a, uint32_t node, uint64_t k,
+                                           bool norm, double& nacc) {
+  using L = Lanes<T, VEC>;
+  constexpr int W = L::W;
+  const NodeIO<T>& n = a.node[node];
+  L x, acc, m;
+  ld(x, n.theta_in, k);
+  zero(acc);
+  const uint32_t ns = a.n_senders[node];
+  for (uint32_t j = 0; j < ns; ++j) {
+    L xs;
+    ld(xs, a.senders[node][j], k);
+#pragma unroll
+    for (int l = 0; l < W; ++l) acc.v[l] = radd(acc.v[l], rsub(xs.v[l], x.v[l]));
+  }
+  const T inv = a.inv[node];
+#pragma unroll
+  for (int l = 0; l < W; ++l) m.v[l] = radd(x.v[l], rmul(acc.v[l], inv));
+  if (!a.step) {
+    st(n.theta_out, k, m);
+    return;
+  }
+  L dp, gb, s, o, xi, ot, od;
+  ld(dp, n.delta, k);
+  ld_grad_inputs(gb, s, o, xi, n.grad, a.spec, a.opt, n.noise, a.quad, k);
+#pragma unroll
+  for (int l = 0; l < W; ++l) {
+    const T dl = sgd_delta(m.v[l], dp.v[l], gb.v[l], s.v[l], o.v[l], xi.v[l], n.alpha, a.mu, a.wd,
+                           a.mu_nz, a.wd_pos, a.quad, norm, nacc);
+    od.v[l] = dl;
+    ot.v[l] = radd(m.v[l], dl);
+  }
+  st(n.theta_out, k, ot);
+  st(n.delta, k, od);
+}
+
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(kBlock) k_push(const __grid_constant__ PushArgs<T> a) {
+  if (!block_wait(a.wait)) return;
+  const uint32_t node = blockIdx.x / a.blocks_per_node;
+  const uint32_t bid = blockIdx.x - node * a.blocks_per_node;
+  const bool norm = a.node[node].norm != nullptr;
+  double nacc = 0.0;
+  constexpr int W = Lanes<T, VEC>::W;
+  const uint64_t nv = a.d / W;
+  const uint64_t stride = (uint64_t)a.blocks_per_node * blockDim.x;
+  const uint64_t first = (uint64_t)bid * blockDim.x + threadIdx.x;
+  for (uint64_t v = first; v < nv; v += stride) push_group<T, VEC>(a, node, v * W, norm, nacc);
+  if constexpr (VEC) {
+    for (uint64_t k = nv * W + first; k < a.d; k += stride)
+      push_group<T, false>(a, node, k, norm, nacc);
+  }
+  block_add_double(nacc, a.node[node].norm);
+  block_signal(a.signal);
+}
+
+template <typename T>
+cudaError_t launch_push(const PushArgs<T>& a, int vec, uint32_t grid, cudaStream_t s) {
+  if (vec)
+    k_push<T, true><<<grid, kBlock, 0, s>>>(a);
+  else
+    k_push<T, false><<<grid, kBlock, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------ multi-GPU EASGD chain
+// Rank r of the chain, chunk by chunk: wait until the previous rank (rank 0:
+// the last rank of the previous gated round) has published the running
+// center of this chunk into our c_in, run the client update + step, forward
+// the center to the next rank over NVLink and publish the chunk flag.  The
+// per-coordinate operation order is the single-context sweep's exactly.
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(kBlock) k_ea_chain(const __grid_constant__ EaChainArgs<T> a) {
+  __shared__ int ok;
+  const NodeIO<T>& n = a.node;
+  const bool norm = n.norm != nullptr;
+  double nacc = 0.0;
+  for (uint64_t c = blockIdx.x; c < a.n_chunks; c += gridDim.x) {
+    if (threadIdx.x == 0) ok = wait_flag(&a.flag_in[c], a.need, a.timeout_ns, a.error) ? 1 : 0;
+    __syncthreads();
+    if (!ok) return;
+    const uint64_t base = c * kEaChunk + (uint64_t)threadIdx.x * 4;
+    constexpr int W = Lanes<T, VEC>::W;
+    for (int sub = 0; sub < 4; sub += W) {
+      const uint64_t k = base + sub;
+      if (VEC ? (k + W > a.d) : (k >= a.d)) {
+        if (VEC) {  // ragged tail of the last chunk: scalar
+          for (uint64_t kk = k; kk < base + 4 && kk < a.d; ++kk) {
+            const T cv0 = a.c_in[kk];
+            T xv = n.theta_in[kk];
+            const T u = rmul(a.beta, rsub(xv, cv0));
+            xv = rsub(xv, u);
+            const T gb = a.quad ? T(0) : n.grad[kk];
+            const T sv = a.quad ? a.spec[kk] : T(0), ov = a.quad ? a.opt[kk] : T(0);
+            const T xiv = n.noise ? n.noise[kk] : T(0);
+            const T dl = sgd_delta(xv, n.delta[kk], gb, sv, ov, xiv, n.alpha, a.mu, a.wd, a.mu_nz,
+                                   a.wd_pos, a.quad, norm, nacc);
+            n.delta[kk] = dl;
+            n.theta_out[kk] = radd(xv, dl);
+            a.c_out[kk] = radd(cv0, u);
+          }
+        }
+        break;
+      }
+      using L = Lanes<T, VEC>;
+      L cv, x, dp, gb, s, o, xi, ot, od;
+      ld(cv, a.c_in, k);
+      ld(x, n.theta_in, k);
+      ld(dp, n.delta, k);
+      ld_grad_inputs(gb, s, o, xi, n.grad, a.spec, a.opt, n.noise, a.quad, k);
+#pragma unroll
+      for (int l = 0; l < W; ++l) {
+        const T u = rmul(a.beta, rsub(x.v[l], cv.v[l]));
+        const T xv = rsub(x.v[l], u);
+        const T dl = sgd_delta(xv, dp.v[l], gb.v[l], s.v[l], o.v[l], xi.v[l], n.alpha, a.mu, a.wd,
+                               a.mu_nz, a.wd_pos, a.quad, norm, nacc);
+        od.v[l] = dl;
+        ot.v[l] = radd(xv, dl);
+        cv.v[l] = radd(cv.v[l], u);
+      }
+      st(n.theta_out, k, ot);
+      st(n.delta, k, od);
+      st(a.c_out, k, cv);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      st_release_sys(&a.flag_out[c], a.seq);
+    }
+  }
+  block_add_double(nacc, n.norm);
+}
+
+template <typename T>
+cudaError_t launch_ea_chain(const EaChainArgs<T>& a, int vec, uint32_t grid, cudaStream_t s) {
+  if (vec)
+    k_ea_chain<T, true><<<grid, kBlock, 0, s>>>(a);
+  else
+    k_ea_chain<T, false><<<grid, kBlock, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ spatial mean
+// param_vec.cpp:19-40 over p device vectors (EASGD center init).
+template <typename T>
+struct MeanArgs {
+  const T* x[kMaxLocal];
+  uint32_t p;
+  uint64_t d;
+  T inv_p;
+  T* out;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_spatial_mean(const __grid_constant__ MeanArgs<T> a) {
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < a.d;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const T x0 = a.x[0][k];
+    T dev = T(0);
+    for (uint32_t i = 1; i < a.p; ++i) dev = radd(dev, rsub(a.x[i][k], x0));
+    a.out[k] = radd(x0, rmul(dev, a.inv_p));
+  }
+}
+
+template <typename T>
+cudaError_t launch_spatial_mean(const T* const* x, uint32_t p, uint64_t d, T* out, cudaStream_t s) {
+  if (p == 0 || p > (uint32_t)kMaxLocal) return cudaErrorInvalidValue;
+  MeanArgs<T> a{};
+  for (uint32_t i = 0; i < p; ++i) a.x[i] = x[i];
+  a.p = p;
+  a.d = d;
+  a.inv_p = T(1) / T(p);
+  a.out = out;
+  const uint64_t blocks = (d + kBlock - 1) / kBlock;
+  k_spatial_mean<T><<<(unsigned)(blocks < 4096 ? (blocks ? blocks : 1) : 4096), kBlock, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------- synthetic gradient source
+// Philox4x32-10 counter-based generator + Box-Muller: N(0, sigma^2) synthetic
+// gradients / noise on the device (bench inputs; not bit-compatible with the
+// host mt19937_64 streams, which the parity path uses instead).
+__device__ __forceinline__ uint4 philox(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_fill_normal(T* out, uint64_t n, double sigma,
+                                                        uint64_t seed, uint64_t offset) {
+  const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q * 4 < n;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t ctr = q + offset;
+    const uint4 r = philox(make_uint4((uint32_t)ctr, (uint32_t)(ctr >> 32), 0x6a09e667u, 0xbb67ae85u), key);
+    const float u0 = ((r.x >> 8) + 0.5f) * (1.0f / 16777216.0f);
+    const float u1 = ((r.y >> 8) + 0.5f) * (1.0f / 16777216.0f);
+    const float u2 = ((r.z >> 8) + 0.5f) * (1.0f / 16777216.0f);
+    const float u3 = ((r.w >> 8) + 0.5f) * (1.0f / 16777216.0f);
+    const float r0 = sqrtf(-2.0f * __logf(u0)), r1 = sqrtf(-2.0f * __logf(u2));
+    float s0, c0, s1, c1;
+    __sincosf(6.2831853071795864f * u1, &s0, &c0);
+    __sincosf(6.2831853071795864f * u3, &s1, &c1);
+    const float z[4] = {r0 * c0, r0 * s0, r1 * c1, r1 * s1};
+#pragma unroll
+    for (int l = 0; l < 4; ++l)
+      if (q * 4 + l < n) out[q * 4 + l] = (T)(sigma * (double)z[l]);
+  }
+}
+
+template <typename T>
+cudaError_t launch_fill_normal(T* out, uint64_t n, double sigma, uint64_t seed, uint64_t offset,
+                               cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t need = (n / 4 + kBlock) / kBlock;
+  const uint64_t grid = need < (uint64_t)sms * 8 ? (need ? need : 1) : (uint64_t)sms * 8;
+  k_fill_normal<T><<<(unsigned)grid, kBlock, 0, s>>>(out, n, sigma, seed, offset);
+  return cudaGetLastError();
+}
+
+#define DSGD_INSTANTIATE(T)                                                                        \
+  template cudaError_t launch_step<T>(int, const StepArgs<T>&, int, uint32_t, cudaStream_t);       \
+  template cudaError_t launch_allreduce_local<T>(const AllreduceArgs<T>&, int, int, uint32_t,      \
+                                                 cudaStream_t);                                    \
+  template cudaError_t launch_ea_local<T>(const EaArgs<T>&, int, int, uint32_t, cudaStream_t);     \
+  template cudaError_t launch_push<T>(const PushArgs<T>&, int, uint32_t, cudaStream_t);            \
+  template cudaError_t launch_ea_chain<T>(const EaChainArgs<T>&, int, uint32_t, cudaStream_t);     \
+  template cudaError_t launch_spatial_mean<T>(const T* const*, uint32_t, uint64_t, T*,             \
+                                              cudaStream_t);                                       \
+  template cudaError_t launch_fill_normal<T>(T*, uint64_t, double, uint64_t, uint64_t, cudaStream_t);
+
+DSGD_INSTANTIATE(float)
+DSGD_INSTANTIATE(double)
+
+}  // namespace dsgd

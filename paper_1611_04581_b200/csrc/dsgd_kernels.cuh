@@ -1,0 +1,142 @@
+// dsgd_kernels.cuh -- launch-parameter structs shared by the runtime
+// (dsgd_runtime.cu) and the kernels (dsgd_kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dsgd_device.cuh"
+
+namespace dsgd {
+
+// One node's device buffers for one launch.
+template <typename T>
+struct NodeIO {
+  const T* theta_in;   // theta at the start of the round (snapshot buffer)
+  T* theta_out;        // theta after the round (the other ping-pong buffer)
+  T* delta;            // delta_prev, read then overwritten in place
+  const T* grad;       // minibatch gradient at the lookahead (GRAD_BUFFER)
+  const T* noise;      // additive noise draw, or null (zero noise: adds +0)
+  const T* partner;    // partner's snapshot theta (local or NVLink peer)
+  T* aux;              // all-reduce exchange buffer
+  double* norm;        // sum of g^2 accumulator (grad_norm_out), or null
+  T alpha;             // step_size_at(h, t_i)
+};
+
+// Kernel modes of the fused gossip-family kernel k_step.
+enum StepMode : int {
+  kModeStep = 0,     // local_sgd_step                      protocols.cpp:102-108
+  kModePull = 1,     // mix_toward(x_i, x_j, 1/2) then step  protocols.cpp:161-185
+  kModeStale = 2,    // delta at x_i; mix(x_i,x_j,b) + delta protocols.cpp:252-263
+  kModeMix = 3,      // mix only (pull_mix / gossip_fresh_mix)
+  kModeArDelta = 4,  // compute_local_delta -> aux            protocols.cpp:85-100
+  kModeApply = 5,    // theta += aux (averaged delta)        protocols.cpp:125-129
+  kModeAsync = 6     // async_pull_event                      protocols.cpp:278-297
+};
+
+template <typename T>
+struct StepArgs {
+  NodeIO<T> node[kMaxLocal];
+  const T* spec;  // quadratic spectrum (GRAD_QUADRATIC)
+  const T* opt;   // quadratic optimum
+  uint64_t d;
+  T mu, wd, beta;
+  int mu_nz;   // h.mu != 0  (lookahead taken)       protocols.cpp:90
+  int wd_pos;  // h.weight_decay > 0                 protocols.cpp:31
+  int quad;    // gradient = spec * (la - opt)
+  uint32_t n_local;
+  uint32_t blocks_per_node;
+  WaitSpec wait;
+  SignalSpec signal;
+};
+
+// Single-context all-reduce round (p nodes on one GPU), fused:
+// deltas -> pivot-form spatial mean -> apply.
+template <typename T>
+struct AllreduceArgs {
+  NodeIO<T> node[kMaxLocal];
+  const T* spec;
+  const T* opt;
+  uint64_t d;
+  T mu, wd, inv_p;
+  int mu_nz, wd_pos, quad;
+  int per_node;
+  uint32_t p;
+};
+
+// Single-context EASGD sweep over p nodes in node order.
+template <typename T>
+struct EaArgs {
+  NodeIO<T> node[kMaxLocal];
+  const T* spec;
+  const T* opt;
+  T* center;
+  uint64_t d;
+  T mu, wd, beta;
+  int mu_nz, wd_pos, quad;
+  int gated;
+  uint32_t p;
+};
+
+// Push mix + step: node i averages its own snapshot with every sender's.
+template <typename T>
+struct PushArgs {
+  NodeIO<T> node[kMaxLocal];
+  const T* senders[kMaxLocal][kMaxLocal];  // ascending sender order (protocols.cpp:212)
+  uint32_t n_senders[kMaxLocal];
+  T inv[kMaxLocal];  // 1 / (1 + n_senders)
+  const T* spec;
+  const T* opt;
+  uint64_t d;
+  T mu, wd;
+  int mu_nz, wd_pos, quad;
+  int step;  // 0: push_mix only
+  uint32_t n_local;
+  uint32_t blocks_per_node;
+  WaitSpec wait;
+  SignalSpec signal;
+};
+
+// Multi-GPU EASGD chain: this rank consumes the running center chunk by
+// chunk from its c_in (written by the previous rank over NVLink), applies
+// its client update + SGD step, and forwards the center to the next rank.
+constexpr uint64_t kEaChunk = 1024;  // elements per chunk (kBlock * 4)
+
+template <typename T>
+struct EaChainArgs {
+  NodeIO<T> node;
+  const T* spec;
+  const T* opt;
+  const T* c_in;                         // own memory
+  T* c_out;                              // next rank's c_in (peer) -- rank p-1: rank 0's
+  const unsigned long long* flag_in;     // own chunk flags
+  unsigned long long* flag_out;          // next rank's chunk flags (peer)
+  unsigned long long need;               // wait flag_in[c] >= need
+  unsigned long long seq;                // value published to flag_out[c]
+  uint64_t d;
+  uint64_t n_chunks;
+  T mu, wd, beta;
+  int mu_nz, wd_pos, quad;
+  unsigned long long timeout_ns;
+  unsigned int* error;
+};
+
+// Host-side launchers (explicitly instantiated for float and double).
+template <typename T>
+cudaError_t launch_step(int mode, const StepArgs<T>& a, int vec, uint32_t grid, cudaStream_t s);
+template <typename T>
+cudaError_t launch_allreduce_local(const AllreduceArgs<T>& a, int vec, int norm, uint32_t grid,
+                                   cudaStream_t s);
+template <typename T>
+cudaError_t launch_ea_local(const EaArgs<T>& a, int vec, int norm, uint32_t grid, cudaStream_t s);
+template <typename T>
+cudaError_t launch_push(const PushArgs<T>& a, int vec, uint32_t grid, cudaStream_t s);
+template <typename T>
+cudaError_t launch_ea_chain(const EaChainArgs<T>& a, int vec, uint32_t grid, cudaStream_t s);
+template <typename T>
+cudaError_t launch_spatial_mean(const T* const* x, uint32_t p, uint64_t d, T* out, cudaStream_t s);
+template <typename T>
+cudaError_t launch_fill_normal(T* out, uint64_t n, double sigma, uint64_t seed, uint64_t offset,
+                               cudaStream_t s);
+
+}  // namespace dsgd

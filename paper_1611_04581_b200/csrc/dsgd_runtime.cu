@@ -1,0 +1,1390 @@
+// dsgd_runtime.cu -- the C ABI (include/dsgd_b200.h): device contexts, node
+// state, the protocol rounds, multi-GPU wiring (CUDA IPC peer memory over
+// NVLink + NCCL) and the per-step worker loop.
+//
+// Layout in HBM (per context, SoA, dtype T, d elements per vector):
+//   arena (one cudaMalloc, exported through CUDA IPC):
+//     theta[i][0], theta[i][1]   ping-pong parameters of each local node
+//     c_in                       EASGD running center (node 0's = the server center)
+//     chunk_flags[d / 1024]      EASGD per-chunk "center arrived" counters
+//     round[i]                   per-node completed-round counters (u64)
+//   private allocations: delta[i], grad[i], noise[i], aux[i] (all-reduce
+//   exchange buffer, per-node scope only), spec/opt (quadratic objective),
+//   norm accumulators, arrival counter, error flag.
+// Every round reads theta[cur] and writes theta[cur ^ 1]; a remote partner
+// therefore always reads a snapshot nobody is writing (the reference's
+// pull/push/stale snapshot semantics, protocols.cpp:164-166).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "dsgd_b200.h"
+#include "dsgd_internal.h"
+#include "dsgd_kernels.cuh"
+
+namespace dsgd {
+
+thread_local std::string g_error;
+
+dsgd_status set_error(dsgd_status st, const std::string& msg) {
+  g_error = msg;
+  return st;
+}
+
+}  // namespace dsgd
+
+using dsgd::kMaxLocal;
+using dsgd::kMaxWait;
+using dsgd::set_error;
+
+#define DSGD_CUDA(call)                                                                   \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return set_error(DSGD_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));   \
+  } while (0)
+
+#define DSGD_NCCL(call)                                                                   \
+  do {                                                                                    \
+    ncclResult_t r_ = (call);                                                             \
+    if (r_ != ncclSuccess)                                                                \
+      return set_error(DSGD_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_));   \
+  } while (0)
+
+#define DSGD_TRY(call)                    \
+  do {                                    \
+    dsgd_status s_ = (call);              \
+    if (s_ != DSGD_OK) return s_;         \
+  } while (0)
+
+namespace {
+
+constexpr uint32_t kMagic = 0xD56DB200u;
+
+size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// What a peer needs to address this context's shared arena.
+struct HandleBlob {
+  uint32_t magic;
+  uint32_t abi;
+  uint32_t first_node;
+  uint32_t n_local;
+  uint32_t dtype;
+  uint32_t flags;
+  uint64_t d;
+  int32_t device;
+  int32_t pad;
+  cudaIpcMemHandle_t handle;
+  uint64_t arena_bytes;
+  uint64_t off_theta[2];
+  uint64_t off_c_in;
+  uint64_t off_flags;
+  uint64_t off_round;
+};
+static_assert(sizeof(HandleBlob) <= DSGD_HANDLE_BYTES, "handle blob too large");
+
+struct PeerNode {  // device-addressable view of one node (local or IPC-mapped)
+  char* theta[2] = {nullptr, nullptr};
+  char* c_in = nullptr;
+  unsigned long long* flags = nullptr;
+  unsigned long long* round = nullptr;
+};
+
+struct Prof {
+  int id;
+  cudaEvent_t a, b;
+};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+struct dsgd_ctx {
+  int device = 0;
+  uint64_t d = 0;
+  dsgd_dtype dtype = DSGD_F32;
+  size_t es = 4;
+  uint32_t p = 1, first = 0, n_local = 1, flags = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int sm_count = 148;
+  int blocks_per_sm = 4;
+
+  char* arena = nullptr;
+  size_t arena_bytes = 0;
+  size_t off_theta[kMaxLocal][2] = {};
+  size_t off_c_in = 0, off_flags = 0, off_round = 0;
+  uint64_t n_chunks = 0;
+
+  char* delta[kMaxLocal] = {};
+  char* grad[kMaxLocal] = {};
+  char* noise[kMaxLocal] = {};
+  char* aux[kMaxLocal] = {};
+  char* spec = nullptr;
+  char* opt = nullptr;
+  double* norm = nullptr;        // n_local sums of g^2
+  double* norm_host = nullptr;   // pinned
+  unsigned int* arrive = nullptr;
+  unsigned int* error = nullptr;
+  char* staging = nullptr;       // pinned host staging (d * 8 bytes)
+
+  int cur = 0;                   // theta buffer holding the current state
+  std::vector<uint64_t> t;       // NodeState::t per local node
+  uint64_t rounds_done = 0;      // rounds this context has run (lock-step)
+  uint64_t seq = 0;              // round counters published so far (multi-GPU)
+  uint64_t ea_seq = 0;           // gated EASGD rounds run (multi-GPU chain)
+  void* ea_update_out[kMaxLocal] = {};   // optional ea_client_step update outputs
+  std::vector<uint32_t> prev_readers;  // nodes that read this context's snapshot last round
+  unsigned long long timeout_ns = 30ull * 1000 * 1000 * 1000;
+
+  // multi-GPU
+  bool connected = false;
+  std::vector<PeerNode> peers;   // all p nodes
+  std::vector<void*> ipc_opened;
+  ncclComm_t comm = nullptr;
+
+  // worker-loop streams
+  std::vector<dsgd_stream*> partner_streams;  // all p (every context draws the full map)
+  std::vector<dsgd_stream*> noise_streams;    // local nodes
+  double* noise_host = nullptr;               // d doubles
+
+  // measurement
+  bool profile = false;
+  std::vector<Prof> prof_pending;
+  std::vector<cudaEvent_t> event_pool;
+  double prof_ms[DSGD_K_COUNT] = {};
+  uint64_t prof_launches[DSGD_K_COUNT] = {};
+  uint64_t kernels = 0, nccl_calls = 0;
+
+  char* theta_ptr(uint32_t i, int buf) const { return arena + off_theta[i][buf]; }
+  unsigned long long* round_ptr(uint32_t i) const {
+    return reinterpret_cast<unsigned long long*>(arena + off_round) + i;
+  }
+  bool distributed() const { return n_local < p; }
+};
+
+namespace {
+
+dsgd_status check_ctx(dsgd_ctx* ctx) {
+  if (!ctx) return set_error(DSGD_EINVAL, "null context");
+  return DSGD_OK;
+}
+
+cudaEvent_t take_event(dsgd_ctx* c) {
+  if (!c->event_pool.empty()) {
+    cudaEvent_t e = c->event_pool.back();
+    c->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Brackets one launch with events when profiling.
+struct LaunchScope {
+  dsgd_ctx* c;
+  int id;
+  cudaEvent_t a = nullptr;
+  LaunchScope(dsgd_ctx* ctx, int kid) : c(ctx), id(kid) {
+    if (c->profile) {
+      a = take_event(c);
+      cudaEventRecord(a, c->stream);
+    }
+  }
+  ~LaunchScope() {
+    if (id == DSGD_K_NCCL)
+      c->nccl_calls++;
+    else
+      c->kernels++;
+    if (c->profile) {
+      cudaEvent_t b = take_event(c);
+      cudaEventRecord(b, c->stream);
+      c->prof_pending.push_back({id, a, b});
+    }
+  }
+};
+
+dsgd_status collect_profile(dsgd_ctx* c) {
+  if (c->prof_pending.empty()) return DSGD_OK;
+  DSGD_CUDA(cudaStreamSynchronize(c->stream));
+  for (const Prof& p : c->prof_pending) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, p.a, p.b);
+    c->prof_ms[p.id] += ms;
+    c->prof_launches[p.id] += 1;
+    c->event_pool.push_back(p.a);
+    c->event_pool.push_back(p.b);
+  }
+  c->prof_pending.clear();
+  return DSGD_OK;
+}
+
+uint32_t blocks_for(const dsgd_ctx* c, uint64_t elems_per_node, uint32_t nodes) {
+  const uint64_t want = std::max<uint64_t>(1, (elems_per_node + dsgd::kBlock - 1) / dsgd::kBlock);
+  const uint64_t cap = std::max<uint64_t>(1, (uint64_t)c->sm_count * c->blocks_per_sm / nodes);
+  return (uint32_t)std::min(want, cap);
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+template <typename T>
+T* as(char* p) {
+  return reinterpret_cast<T*>(p);
+}
+
+// Resolved gradient source for one launch.
+struct GradSel {
+  int quad = 0;
+  const void* grad[kMaxLocal] = {};
+  bool noise = false;
+  bool norm = false;
+};
+
+dsgd_status resolve_grad(dsgd_ctx* c, const dsgd_grad_spec* g, GradSel* out) {
+  GradSel s;
+  if (!g) return set_error(DSGD_EINVAL, "null gradient spec");
+  if (g->source == DSGD_GRAD_QUADRATIC) {
+    if (!c->spec) return set_error(DSGD_ESTATE, "no quadratic objective (DSGD_CTX_QUADRATIC)");
+    s.quad = 1;
+  } else if (g->source == DSGD_GRAD_BUFFER) {
+    for (uint32_t i = 0; i < c->n_local; ++i) {
+      s.grad[i] = g->grad ? g->grad[i] : c->grad[i];
+      if (!s.grad[i]) return set_error(DSGD_EINVAL, "missing gradient buffer");
+    }
+  } else {
+    return set_error(DSGD_EINVAL, "unknown gradient source");
+  }
+  if (g->use_noise) {
+    if (!c->noise[0]) return set_error(DSGD_ESTATE, "no noise buffers (DSGD_CTX_NOISE)");
+    s.noise = true;
+  }
+  s.norm = g->grad_norm_out != nullptr;
+  *out = s;
+  return DSGD_OK;
+}
+
+template <typename T>
+void fill_node(dsgd_ctx* c, uint32_t i, const GradSel& gs, const dsgd_hyperparams* h,
+               dsgd::NodeIO<T>* n, bool negate_alpha = false) {
+  n->theta_in = as<T>(c->theta_ptr(i, c->cur));
+  n->theta_out = as<T>(c->theta_ptr(i, c->cur ^ 1));
+  n->delta = as<T>(c->delta[i]);
+  n->grad = gs.quad ? nullptr : static_cast<const T*>(gs.grad[i]);
+  n->noise = gs.noise ? as<T>(c->noise[i]) : nullptr;
+  n->partner = nullptr;
+  n->aux = nullptr;
+  n->norm = gs.norm ? c->norm + i : nullptr;
+  const double alpha = h ? dsgd_step_size_at(h, c->t[i]) : 0.0;
+  n->alpha = (T)(negate_alpha ? -alpha : alpha);
+}
+
+template <typename A>
+void fill_common(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& gs, A* a) {
+  using T = std::remove_pointer_t<decltype(a->spec)>;
+  using TT = std::remove_const_t<T>;
+  a->spec = gs.quad ? as<TT>(c->spec) : nullptr;
+  a->opt = gs.quad ? as<TT>(c->opt) : nullptr;
+  a->d = c->d;
+  a->mu = (TT)h->mu;
+  a->wd = (TT)h->weight_decay;
+  a->mu_nz = h->mu != 0.0;
+  a->wd_pos = h->weight_decay > 0.0;
+  a->quad = gs.quad;
+}
+
+bool all_aligned(dsgd_ctx* c, const GradSel& gs) {
+  for (uint32_t i = 0; i < c->n_local; ++i)
+    if (!gs.quad && !aligned16(gs.grad[i])) return false;
+  return true;
+}
+
+dsgd_status norm_begin(dsgd_ctx* c, const GradSel& gs) {
+  if (gs.norm) DSGD_CUDA(cudaMemsetAsync(c->norm, 0, sizeof(double) * c->n_local, c->stream));
+  return DSGD_OK;
+}
+
+dsgd_status norm_end(dsgd_ctx* c, const GradSel& gs, const dsgd_grad_spec* g) {
+  if (!gs.norm) return DSGD_OK;
+  DSGD_CUDA(cudaMemcpyAsync(c->norm_host, c->norm, sizeof(double) * c->n_local,
+                            cudaMemcpyDeviceToHost, c->stream));
+  DSGD_CUDA(cudaStreamSynchronize(c->stream));
+  for (uint32_t i = 0; i < c->n_local; ++i)
+    *g->grad_norm_out = std::max(*g->grad_norm_out, std::sqrt(c->norm_host[i]));
+  return DSGD_OK;
+}
+
+void finish_round(dsgd_ctx* c, bool flip, bool advance_t = true) {
+  if (flip) c->cur ^= 1;
+  if (advance_t)
+    for (auto& t : c->t) t += 1;
+  c->rounds_done += 1;
+}
+
+dsgd_status check_common_round(dsgd_ctx* c) {
+  for (uint64_t t : c->t)
+    if (t != c->t[0])
+      return set_error(DSGD_EINVAL, "synchronous round requires equal node clocks");
+  return DSGD_OK;
+}
+
+dsgd_status check_map(dsgd_ctx* c, const uint32_t* m) {
+  if (!m) return set_error(DSGD_EINVAL, "null partner map");
+  for (uint32_t i = 0; i < c->p; ++i)
+    if (m[i] >= c->p) return set_error(DSGD_EINVAL, "partner index out of range");
+  return DSGD_OK;
+}
+
+// Wait list of a multi-GPU round that reads `reads` (the partner, or none)
+// and overwrites the snapshot the previous round's pullers read.
+void build_waits(dsgd_ctx* c, const std::vector<uint32_t>& reads, dsgd::WaitSpec* w) {
+  w->n = 0;
+  w->timeout_ns = c->timeout_ns;
+  w->error = c->error;
+  if (!c->distributed()) return;
+  const uint32_t me = c->first;
+  auto add = [&](uint32_t node) {
+    if (node == me) return;
+    for (int k = 0; k < w->n; ++k)
+      if (w->ptr[k] == c->peers[node].round) return;
+    if (w->n < kMaxWait) {
+      w->ptr[w->n] = c->peers[node].round;
+      w->val[w->n] = c->seq;
+      w->n++;
+    }
+  };
+  for (uint32_t j : reads) add(j);            // RAW: partner finished round r-1
+  for (uint32_t k : c->prev_readers) add(k);  // WAR: last round's readers of my snapshot
+}
+
+void build_signal(dsgd_ctx* c, dsgd::SignalSpec* s) {
+  if (!c->distributed()) {
+    s->counter = nullptr;
+    return;
+  }
+  s->counter = c->round_ptr(0);
+  s->value = c->seq + 1;
+  s->arrive = c->arrive;
+}
+
+template <typename T>
+dsgd_status run_step_mode(dsgd_ctx* c, int mode, int kid, const dsgd_hyperparams* h,
+                          const GradSel& gs, const uint32_t* partner_of, T beta,
+                          bool negate_alpha, const std::vector<uint32_t>& reads) {
+  dsgd::StepArgs<T> a{};
+  for (uint32_t i = 0; i < c->n_local; ++i) {
+    fill_node<T>(c, i, gs, h, &a.node[i], negate_alpha);
+    if (partner_of) {
+      const uint32_t j = partner_of[c->first + i];
+      a.node[i].partner = as<T>(c->peers[j].theta[c->cur]);
+    }
+  }
+  if (h) {
+    fill_common(c, h, gs, &a);
+  } else {
+    a.d = c->d;
+  }
+  a.beta = beta;
+  a.n_local = c->n_local;
+  bool vec = all_aligned(c, gs);
+  if (partner_of)
+    for (uint32_t i = 0; i < c->n_local; ++i) vec = vec && aligned16(a.node[i].partner);
+  const uint64_t W = vec ? 16 / sizeof(T) : 1;
+  a.blocks_per_node = blocks_for(c, (c->d / W + 1) / 2, c->n_local);
+  build_waits(c, reads, &a.wait);
+  build_signal(c, &a.signal);
+  const uint32_t grid = a.blocks_per_node * c->n_local;
+  LaunchScope ls(c, kid);
+  DSGD_CUDA(dsgd::launch_step<T>(mode, a, vec ? 1 : 0, grid, c->stream));
+  if (c->distributed()) c->seq += 1;
+  return DSGD_OK;
+}
+
+template <typename T>
+dsgd_status do_local_step(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& gs) {
+  DSGD_TRY(run_step_mode<T>(c, dsgd::kModeStep, DSGD_K_STEP, h, gs, nullptr, T(0), false, {}));
+  c->prev_readers.clear();
+  return DSGD_OK;
+}
+
+template <typename T>
+dsgd_status do_pull(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& gs,
+                    const uint32_t* partner_of, int mode, T beta) {
+  std::vector<uint32_t> reads;
+  for (uint32_t i = 0; i < c->n_local; ++i) reads.push_back(partner_of[c->first + i]);
+  DSGD_TRY(run_step_mode<T>(c, mode, DSGD_K_STEP, h, gs, partner_of, beta, false, reads));
+  c->prev_readers.clear();
+  for (uint32_t k = 0; k < c->p; ++k)
+    if (partner_of[k] == c->first && c->distributed()) c->prev_readers.push_back(k);
+  return DSGD_OK;
+}
+
+template <typename T>
+dsgd_status do_allreduce(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& gs,
+                         dsgd_momentum_scope scope) {
+  if (!c->distributed()) {
+    dsgd::AllreduceArgs<T> a{};
+    for (uint32_t i = 0; i < c->n_local; ++i) fill_node<T>(c, i, gs, h, &a.node[i]);
+    fill_common(c, h, gs, &a);
+    a.inv_p = T(1) / T(c->p);
+    a.per_node = scope == DSGD_SCOPE_PER_NODE;
+    a.p = c->p;
+    const bool vec = all_aligned(c, gs);
+    const uint64_t W = vec ? 16 / sizeof(T) : 1;
+    const uint32_t grid = blocks_for(c, c->d / W, 1);
+    LaunchScope ls(c, DSGD_K_ALLREDUCE);
+    DSGD_CUDA(dsgd::launch_allreduce_local<T>(a, vec, gs.norm, grid, c->stream));
+    c->prev_readers.clear();
+    return DSGD_OK;
+  }
+  if (!c->comm) return set_error(DSGD_ESTATE, "multi-GPU all-reduce needs dsgd_ctx_init_nccl");
+  // delta kernel -> ncclAllReduce(avg) in place on the exchange buffer ->
+  // apply kernel.  Aggregate scope exchanges delta_prev itself, so the
+  // averaged delta lands where the next round's momentum reads it.
+  const bool per_node = scope == DSGD_SCOPE_PER_NODE;
+  if (per_node && !c->aux[0]) DSGD_CUDA(cudaMalloc(&c->aux[0], c->d * c->es));
+  char* xbuf = per_node ? c->aux[0] : c->delta[0];
+  {
+    dsgd::StepArgs<T> a{};
+    fill_node<T>(c, 0, gs, h, &a.node[0]);
+    a.node[0].aux = as<T>(xbuf);
+    fill_common(c, h, gs, &a);
+    a.n_local = 1;
+    const bool vec = all_aligned(c, gs);
+    const uint64_t W = vec ? 16 / sizeof(T) : 1;
+    a.blocks_per_node = blocks_for(c, (c->d / W + 1) / 2, 1);
+    LaunchScope ls(c, DSGD_K_AR_DELTA);
+    DSGD_CUDA(dsgd::launch_step<T>(dsgd::kModeArDelta, a, vec, a.blocks_per_node, c->stream));
+  }
+  {
+    LaunchScope ls(c, DSGD_K_NCCL);
+    DSGD_NCCL(ncclAllReduce(xbuf, xbuf, c->d, sizeof(T) == 4 ? ncclFloat : ncclDouble, ncclAvg,
+                            c->comm, c->stream));
+  }
+  {
+    dsgd::StepArgs<T> a{};
+    fill_node<T>(c, 0, gs, nullptr, &a.node[0]);
+    a.node[0].aux = as<T>(xbuf);
+    a.node[0].norm = nullptr;
+    a.d = c->d;
+    a.n_local = 1;
+    const uint64_t W = 16 / sizeof(T);
+    a.blocks_per_node = blocks_for(c, (c->d / W + 1) / 2, 1);
+    build_signal(c, &a.signal);
+    LaunchScope ls(c, DSGD_K_AR_APPLY);
+    DSGD_CUDA(dsgd::launch_step<T>(dsgd::kModeApply, a, 1, a.blocks_per_node, c->stream));
+    c->seq += 1;
+  }
+  c->prev_readers.clear();
+  return DSGD_OK;
+}
+
+template <typename T>
+dsgd_status do_ea(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& gs, int gated) {
+  if (!c->distributed()) {
+    if (!(c->flags & DSGD_CTX_CENTER)) return set_error(DSGD_ESTATE, "no center (DSGD_CTX_CENTER)");
+    dsgd::EaArgs<T> a{};
+    for (uint32_t i = 0; i < c->n_local; ++i) {
+      fill_node<T>(c, i, gs, h, &a.node[i]);
+      a.node[i].aux = static_cast<T*>(c->ea_update_out[i]);
+    }
+    fill_common(c, h, gs, &a);
+    a.center = as<T>(c->arena + c->off_c_in);
+    a.beta = (T)h->beta_ea;
+    a.gated = gated;
+    a.p = c->p;
+    const bool vec = all_aligned(c, gs);
+    const uint64_t W = vec ? 16 / sizeof(T) : 1;
+    const uint32_t grid = blocks_for(c, c->d / W, 1);
+    LaunchScope ls(c, DSGD_K_EA);
+    DSGD_CUDA(dsgd::launch_ea_local<T>(a, vec, gs.norm, grid, c->stream));
+    c->prev_readers.clear();
+    return DSGD_OK;
+  }
+  if (!gated) return do_local_step<T>(c, h, gs);
+  if (!(c->flags & DSGD_CTX_CENTER) || !c->connected)
+    return set_error(DSGD_ESTATE, "multi-GPU EASGD needs DSGD_CTX_CENTER on every rank and peers");
+  const uint32_t r = c->first;
+  const uint32_t next = (r + 1) % c->p;
+  c->ea_seq += 1;
+  dsgd::EaChainArgs<T> a{};
+  fill_node<T>(c, 0, gs, h, &a.node);
+  a.spec = gs.quad ? as<T>(c->spec) : nullptr;
+  a.opt = gs.quad ? as<T>(c->opt) : nullptr;
+  a.c_in = as<T>(c->arena + c->off_c_in);
+  a.c_out = as<T>(c->peers[next].c_in);
+  a.flag_in = reinterpret_cast<const unsigned long long*>(c->arena + c->off_flags);
+  a.flag_out = c->peers[next].flags;
+  a.need = r == 0 ? c->ea_seq - 1 : c->ea_seq;
+  a.seq = c->ea_seq;
+  a.d = c->d;
+  a.n_chunks = c->n_chunks;
+  a.mu = (T)h->mu;
+  a.wd = (T)h->weight_decay;
+  a.beta = (T)h->beta_ea;
+  a.mu_nz = h->mu != 0.0;
+  a.wd_pos = h->weight_decay > 0.0;
+  a.quad = gs.quad;
+  a.timeout_ns = c->timeout_ns;
+  a.error = c->error;
+  const bool vec = all_aligned(c, gs);
+  const uint32_t grid =
+      (uint32_t)std::min<uint64_t>(c->n_chunks, (uint64_t)c->sm_count * c->blocks_per_sm);
+  LaunchScope ls(c, DSGD_K_EA);
+  DSGD_CUDA(dsgd::launch_ea_chain<T>(a, vec, grid, c->stream));
+  c->prev_readers.clear();
+  return DSGD_OK;
+}
+
+template <typename T>
+dsgd_status do_push(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel* gs,
+                    const uint32_t* target_of) {
+  dsgd::PushArgs<T> a{};
+  std::vector<uint32_t> reads;
+  for (uint32_t i = 0; i < c->n_local; ++i) {
+    const uint32_t me = c->first + i;
+    if (gs) fill_node<T>(c, i, *gs, h, &a.node[i]);
+    else {
+      a.node[i].theta_in = as<T>(c->theta_ptr(i, c->cur));
+      a.node[i].theta_out = as<T>(c->theta_ptr(i, c->cur ^ 1));
+    }
+    uint32_t n = 0;
+    for (uint32_t k = 0; k < c->p; ++k) {
+      if (target_of[k] == me) {
+        a.senders[i][n++] = as<T>(c->peers[k].theta[c->cur]);
+        reads.push_back(k);
+      }
+    }
+    a.n_senders[i] = n;
+    a.inv[i] = T(1) / T(n + 1);
+  }
+  if (gs) {
+    fill_common(c, h, *gs, &a);
+  } else {
+    a.d = c->d;
+  }
+  a.step = gs ? 1 : 0;
+  a.n_local = c->n_local;
+  bool vec = gs ? all_aligned(c, *gs) : true;
+  const uint64_t W = vec ? 16 / sizeof(T) : 1;
+  a.blocks_per_node = blocks_for(c, c->d / W, c->n_local);
+  build_waits(c, reads, &a.wait);
+  build_signal(c, &a.signal);
+  LaunchScope ls(c, DSGD_K_PUSH);
+  DSGD_CUDA(dsgd::launch_push<T>(a, vec, a.blocks_per_node * c->n_local, c->stream));
+  if (c->distributed()) c->seq += 1;
+  // WAR for the next round: my snapshot was read by my push target.
+  c->prev_readers.clear();
+  if (c->distributed()) c->prev_readers.push_back(target_of[c->first]);
+  return DSGD_OK;
+}
+
+template <typename F>
+dsgd_status dispatch(dsgd_ctx* c, F&& f) {
+  DeviceGuard g(c->device);
+  if (c->dtype == DSGD_F32) return f(float{});
+  return f(double{});
+}
+
+dsgd_status ensure_staging(dsgd_ctx* c) {
+  if (!c->staging) DSGD_CUDA(cudaMallocHost(&c->staging, c->d * 4));
+  return DSGD_OK;
+}
+
+dsgd_status upload_vec(dsgd_ctx* c, char* dst, const double* host) {
+  if (c->dtype == DSGD_F64) {
+    DSGD_CUDA(cudaMemcpyAsync(dst, host, c->d * 8, cudaMemcpyHostToDevice, c->stream));
+    DSGD_CUDA(cudaStreamSynchronize(c->stream));
+    return DSGD_OK;
+  }
+  DSGD_TRY(ensure_staging(c));
+  float* st = reinterpret_cast<float*>(c->staging);
+  DSGD_CUDA(cudaStreamSynchronize(c->stream));
+  for (uint64_t k = 0; k < c->d; ++k) st[k] = (float)host[k];
+  DSGD_CUDA(cudaMemcpyAsync(dst, st, c->d * 4, cudaMemcpyHostToDevice, c->stream));
+  DSGD_CUDA(cudaStreamSynchronize(c->stream));
+  return DSGD_OK;
+}
+
+dsgd_status download_vec(dsgd_ctx* c, const char* src, double* host) {
+  DSGD_CUDA(cudaStreamSynchronize(c->stream));
+  if (c->dtype == DSGD_F64) {
+    DSGD_CUDA(cudaMemcpy(host, src, c->d * 8, cudaMemcpyDeviceToHost));
+    return DSGD_OK;
+  }
+  DSGD_TRY(ensure_staging(c));
+  float* st = reinterpret_cast<float*>(c->staging);
+  DSGD_CUDA(cudaMemcpy(st, src, c->d * 4, cudaMemcpyDeviceToHost));
+  for (uint64_t k = 0; k < c->d; ++k) host[k] = (double)st[k];
+  return DSGD_OK;
+}
+
+char* buffer_of(dsgd_ctx* c, uint32_t local, dsgd_buffer which) {
+  switch (which) {
+    case DSGD_BUF_THETA: return c->theta_ptr(local, c->cur);
+    case DSGD_BUF_DELTA: return c->delta[local];
+    case DSGD_BUF_GRAD: return c->grad[local];
+    case DSGD_BUF_NOISE: return c->noise[local];
+    case DSGD_BUF_SPECTRUM: return c->spec;
+    case DSGD_BUF_OPT: return c->opt;
+    case DSGD_BUF_CENTER: return (c->flags & DSGD_CTX_CENTER) ? c->arena + c->off_c_in : nullptr;
+  }
+  return nullptr;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dsgd_last_error(void) { return dsgd::g_error.c_str(); }
+int dsgd_abi_version(void) { return DSGD_B200_ABI_VERSION; }
+
+dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
+  if (!desc || !out) return set_error(DSGD_EINVAL, "null argument");
+  if (desc->dim == 0) return set_error(DSGD_EINVAL, "dim must be >= 1");
+  if (desc->p == 0 || desc->n_local == 0 || desc->n_local > (uint32_t)kMaxLocal ||
+      desc->first_node + desc->n_local > desc->p)
+    return set_error(DSGD_EINVAL, "bad node layout (p, first_node, n_local)");
+  if (desc->n_local != desc->p && desc->n_local != 1)
+    return set_error(DSGD_EINVAL, "a context hosts all p nodes or exactly one");
+  if (desc->dtype != DSGD_F32 && desc->dtype != DSGD_F64) return set_error(DSGD_EINVAL, "dtype");
+  auto c = std::make_unique<dsgd_ctx>();
+  c->device = desc->device;
+  c->d = desc->dim;
+  c->dtype = desc->dtype;
+  c->es = desc->dtype == DSGD_F32 ? 4 : 8;
+  c->p = desc->p;
+  c->first = desc->first_node;
+  c->n_local = desc->n_local;
+  c->flags = desc->flags;
+  c->t.assign(c->n_local, 0);
+  DeviceGuard g(c->device);
+  DSGD_CUDA(cudaSetDevice(c->device));
+  DSGD_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device));
+  if (const char* e = std::getenv("DSGD_BLOCKS_PER_SM")) c->blocks_per_sm = std::max(1, atoi(e));
+  if (desc->stream) {
+    c->stream = static_cast<cudaStream_t>(desc->stream);
+  } else {
+    DSGD_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+  }
+  const size_t vb = align_up(c->d * c->es);
+  size_t off = 0;
+  for (uint32_t i = 0; i < c->n_local; ++i)
+    for (int b = 0; b < 2; ++b) {
+      c->off_theta[i][b] = off;
+      off += vb;
+    }
+  c->n_chunks = (c->d + dsgd::kEaChunk - 1) / dsgd::kEaChunk;
+  c->off_c_in = off;
+  if (c->flags & DSGD_CTX_CENTER) off += vb;
+  c->off_flags = off;
+  if (c->flags & DSGD_CTX_CENTER) off += align_up(c->n_chunks * 8);
+  c->off_round = off;
+  off += align_up(8 * c->n_local);
+  c->arena_bytes = off;
+  DSGD_CUDA(cudaMalloc(&c->arena, c->arena_bytes));
+  DSGD_CUDA(cudaMemset(c->arena, 0, c->arena_bytes));
+  for (uint32_t i = 0; i < c->n_local; ++i) {
+    DSGD_CUDA(cudaMalloc(&c->delta[i], vb));
+    DSGD_CUDA(cudaMemset(c->delta[i], 0, vb));
+    if (c->flags & DSGD_CTX_GRAD) {
+      DSGD_CUDA(cudaMalloc(&c->grad[i], vb));
+      DSGD_CUDA(cudaMemset(c->grad[i], 0, vb));
+    }
+    if (c->flags & DSGD_CTX_NOISE) {
+      DSGD_CUDA(cudaMalloc(&c->noise[i], vb));
+      DSGD_CUDA(cudaMemset(c->noise[i], 0, vb));
+    }
+  }
+  if (c->flags & DSGD_CTX_QUADRATIC) {
+    DSGD_CUDA(cudaMalloc(&c->spec, vb));
+    DSGD_CUDA(cudaMalloc(&c->opt, vb));
+    DSGD_CUDA(cudaMemset(c->spec, 0, vb));
+    DSGD_CUDA(cudaMemset(c->opt, 0, vb));
+  }
+  DSGD_CUDA(cudaMalloc(&c->norm, sizeof(double) * kMaxLocal));
+  DSGD_CUDA(cudaMallocHost(&c->norm_host, sizeof(double) * kMaxLocal));
+  DSGD_CUDA(cudaMalloc(&c->arrive, 256));
+  DSGD_CUDA(cudaMemset(c->arrive, 0, 256));
+  c->error = c->arrive + 32;
+  // local nodes are addressable peers of themselves
+  c->peers.resize(c->p);
+  for (uint32_t i = 0; i < c->n_local; ++i) {
+    PeerNode& pn = c->peers[c->first + i];
+    pn.theta[0] = c->theta_ptr(i, 0);
+    pn.theta[1] = c->theta_ptr(i, 1);
+    pn.round = c->round_ptr(i);
+    if (i == 0 && (c->flags & DSGD_CTX_CENTER)) {
+      pn.c_in = c->arena + c->off_c_in;
+      pn.flags = reinterpret_cast<unsigned long long*>(c->arena + c->off_flags);
+    }
+  }
+  c->connected = !c->distributed();
+  *out = c.release();
+  return DSGD_OK;
+}
+
+void dsgd_ctx_destroy(dsgd_ctx* c) {
+  if (!c) return;
+  DeviceGuard g(c->device);
+  cudaStreamSynchronize(c->stream);
+  if (c->comm) ncclCommDestroy(c->comm);
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  for (uint32_t i = 0; i < c->n_local; ++i) {
+    cudaFree(c->delta[i]);
+    cudaFree(c->grad[i]);
+    cudaFree(c->noise[i]);
+    cudaFree(c->aux[i]);
+  }
+  cudaFree(c->spec);
+  cudaFree(c->opt);
+  cudaFree(c->norm);
+  cudaFreeHost(c->norm_host);
+  cudaFree(c->arrive);
+  cudaFreeHost(c->staging);
+  cudaFree(c->arena);
+  for (auto* s : c->partner_streams) dsgd_stream_destroy(s);
+  for (auto* s : c->noise_streams) dsgd_stream_destroy(s);
+  delete[] c->noise_host;
+  for (const Prof& p : c->prof_pending) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+dsgd_status dsgd_ctx_stream(dsgd_ctx* c, void** stream) {
+  DSGD_TRY(check_ctx(c));
+  *stream = c->stream;
+  return DSGD_OK;
+}
+
+dsgd_status dsgd_ctx_sync(dsgd_ctx* c) {
+  DSGD_TRY(check_ctx(c));
+  DeviceGuard g(c->device);
+  DSGD_CUDA(cudaStreamSynchronize(c->stream));
+  unsigned int err = 0;
+  DSGD_CUDA(cudaMemcpy(&err, c->error, sizeof(err), cudaMemcpyDeviceToHost));
+  if (err) return set_error(DSGD_ETIMEOUT, "a peer flag wait timed out inside a kernel");
+  return DSGD_OK;
+}
+
+dsgd_status dsgd_ctx_set_timeout(dsgd_ctx* c, double seconds) {
+  DSGD_TRY(check_ctx(c));
+  if (!(seconds > 0)) return set_error(DSGD_EINVAL, "timeout must be positive");
+  c->timeout_ns = (unsigned long long)(seconds * 1e9);
+  return DSGD_OK;
+}
+
+dsgd_status dsgd_buffer_ptr(dsgd_ctx* c, uint32_t local, dsgd_buffer which, void** dev) {
+  DSGD_TRY(check_ctx(c));
+  if (local >= c->n_local) return set_error(DSGD_EINVAL, "local node out of range");
+  char* p = buffer_of(c, local, which);
+  if (!p) return set_error(DSGD_ESTATE, "buffer not allocated for this context");
+  *dev = p;
+  return DSGD_OK;
+}
+
+dsgd_status dsgd_set_state(dsgd_ctx* c, uint32_t local, const double* theta,
+                           const double* delta_prev, uint64_t t) {
+  DSGD_TRY(check_ctx(c));
+  if (local >= c->n_local) return set_error(DSGD_EINVAL, "local node out of range");
+  DeviceGuard g(c->device);
+  if (theta) DSGD_TRY(upload_vec(c, c->theta_ptr(local, c->cur), theta));
+  if (delta_prev) DSGD_TRY(upload_vec(c, c->delta[local], delta_prev));
+  c->t[local] = t;
+  return DSGD_OK;
+}
+
+dsgd_status dsgd_get_state(dsgd_ctx* c, uint32_t local, double* theta, double* delta_prev,
+                           uint64_t* t) {
+  DSGD_TRY(check_ctx(c));
+  if (local >= c->n_local) return set_error(DSGD_EINVAL, "local node out of range");
+  DeviceGuard g(c->device);
+  DSGD_TRY(dsgd_ctx_sync(c));
+  if (theta) DSGD_TRY(download_vec(c, c->theta_ptr(local, c->cur), theta));
+  if (delta_prev) DSGD_TRY(download_vec(c, c->delta[local], delta_prev));
+  if (t) *t = c->t[local];
+  return DSGD_OK;
+}
+
+dsgd_status dsgd_set_vector(dsgd_ctx* c, uint32_t local, dsgd_buffer which, const double* host) {
+  DSGD_TRY(check_ctx(c));
+  if (local >= c->n_local) return set_error(DSGD_EINVAL, "local node out of range");
+  char* p = buffer_of(c, local, which);
+  if (!p) return set_error(DSGD_ESTATE, "buffer not allocated for this context");
+  DeviceGuard g(c->device);
+  return upload_vec(c, p, host);
+}
+
+dsgd_status dsgd_get_vector(dsgd_ctx* c, uint32_t local, dsgd_buffer which, double* host) {
+  DSGD_TRY(check_ctx(c));
+  if (local >= c->n_local) return set_error(DSGD_EINVAL, "local node out of range");
+  char* p = buffer_of(c, local, which);
+  if (!p) return set_error(DSGD_ESTATE, "buffer not allocated for this context");
+  DeviceGuard g(c->device);
+  return download_vec(c, p, host);
+}
+
+dsgd_status dsgd_upload_async(dsgd_ctx* c, uint32_t local, dsgd_buffer which, const void* host,
+                              uint64_t count) {
+  DSGD_TRY(check_ctx(c));
+  if (local >= c->n_local || count > c->d) return set_error(DSGD_EINVAL, "range");
+  char* p = buffer_of(c, local, which);
+  if (!p) return set_error(DSGD_ESTATE, "buffer not allocated for this context");
+  DeviceGuard g(c->device);
+  DSGD_CUDA(cudaMemcpyAsync(p, host, count * c->es, cudaMemcpyHostToDevice, c->stream));
+  return DSGD_OK;
+}
+
+dsgd_status dsgd_download_async(dsgd_ctx* c, uint32_t local, dsgd_buffer which, void* host,
+                                uint64_t count) {
+  DSGD_TRY(check_ctx(c));
+  if (local >= c->n_local || count > c->d) return set_error(DSGD_EINVAL, "range");
+  char* p = buffer_of(c, local, which);
+  if (!p) return set_error(DSGD_ESTATE, "buffer not allocated for this context");
+  DeviceGuard g(c->device);
+  DSGD_CUDA(cudaMemcpyAsync(host, p, count * c->es, cudaMemcpyDeviceToHost, c->stream));
+  return DSGD_OK;
+}
+
+dsgd_status dsgd_copy_in_async(dsgd_ctx* c, uint32_t local, dsgd_buffer which, const void* src,
+                               uint64_t count) {
+  DSGD_TRY(check_ctx(c));
+  if (local >= c->n_local || count > c->d || !src) return set_error(DSGD_EINVAL, "range");
+  char* p = buffer_of(c, local, which);
+  if (!p) return set_error(DSGD_ESTATE, "buffer not allocated for this context");
+  DeviceGuard g(c->device);
+  DSGD_CUDA(cudaMemcpyAsync(p, src, count * c->es, cudaMemcpyDefault, c->stream));
+  return DSGD_OK;
+}
+
+dsgd_status dsgd_get_t(dsgd_ctx* c, uint32_t local, uint64_t* t) {
+  DSGD_TRY(check_ctx(c));
+  if (local >= c->n_local) return set_error(DSGD_EINVAL, "local node out of range");
+  *t = c->t[local];
+  return DSGD_OK;
+}
+
+dsgd_status dsgd_set_t(dsgd_ctx* c, uint32_t local, uint64_t t) {
+  DSGD_TRY(check_ctx(c));
+  if (local >= c->n_local) return set_error(DSGD_EINVAL, "local node out of range");
+  c->t[local] = t;
+  return DSGD_OK;
+}
+
+// ----------------------------------------------------------- update rules
+dsgd_status dsgd_local_sgd_step(dsgd_ctx* c, const dsgd_hyperparams* h, const dsgd_grad_spec* g) {
+  DSGD_TRY(check_ctx(c));
+  if (!h) return set_error(DSGD_EINVAL, "null hyperparams");
+  if (!c->connected) return set_error(DSGD_ESTATE, "peers not connected");
+  GradSel gs;
+  DSGD_TRY(resolve_grad(c, g, &gs));
+  return dispatch(c, [&](auto z) -> dsgd_status {
+    using T = decltype(z);
+    DSGD_TRY(norm_begin(c, gs));
+    DSGD_TRY(do_local_step<T>(c, h, gs));
+    finish_round(c, true);
+    return norm_end(c, gs, g);
+  });
+}
+
+dsgd_status dsgd_allreduce_round(dsgd_ctx* c, const dsgd_hyperparams* h, const dsgd_grad_spec* g,
+                                 dsgd_momentum_scope scope) {
+  DSGD_TRY(check_ctx(c));
+  if (!h) return set_error(DSGD_EINVAL, "null hyperparams");
+  if (!c->connected) return set_error(DSGD_ESTATE, "peers not connected");
+  DSGD_TRY(check_common_round(c));
+  GradSel gs;
+  DSGD_TRY(resolve_grad(c, g, &gs));
+  return dispatch(c, [&](auto z) -> dsgd_status {
+    using T = decltype(z);
+    DSGD_TRY(norm_begin(c, gs));
+    DSGD_TRY(do_allreduce<T>(c, h, gs, scope));
+    finish_round(c, true);
+    return norm_end(c, gs, g);
+  });
+}
+
+dsgd_status dsgd_ea_round(dsgd_ctx* c, const dsgd_hyperparams* h, const dsgd_grad_spec* g,
+                          int gated) {
+  DSGD_TRY(check_ctx(c));
+  if (!h) return set_error(DSGD_EINVAL, "null hyperparams");
+  if (!c->connected) return set_error(DSGD_ESTATE, "peers not connected");
+  GradSel gs;
+  DSGD_TRY(resolve_grad(c, g, &gs));
+  return dispatch(c, [&](auto z) -> dsgd_status {
+    using T = decltype(z);
+    DSGD_TRY(norm_begin(c, gs));
+    DSGD_TRY(do_ea<T>(c, h, gs, gated));
+    finish_round(c, true);
+    return norm_end(c, gs, g);
+  });
+}
+
+dsgd_status dsgd_pull_gossip_round(dsgd_ctx* c, const dsgd_hyperparams* h,
+                                   const dsgd_grad_spec* g, const uint32_t* partner_of) {
+  DSGD_TRY(check_ctx(c));
+  if (!h) return set_error(DSGD_EINVAL, "null hyperparams");
+  if (!c->connected) return set_error(DSGD_ESTATE, "peers not connected");
+  DSGD_TRY(check_common_round(c));
+  if (partner_of) DSGD_TRY(check_map(c, partner_of));
+  GradSel gs;
+  DSGD_TRY(resolve_grad(c, g, &gs));
+  return dispatch(c, [&](auto z) -> dsgd_status {
+    using T = decltype(z);
+    DSGD_TRY(norm_begin(c, gs));
+    if (partner_of)
+      DSGD_TRY(do_pull<T>(c, h, gs, partner_of, dsgd::kModePull, T(0.5)));
+    else
+      DSGD_TRY(do_local_step<T>(c, h, gs));
+    finish_round(c, true);
+    return norm_end(c, gs, g);
+  });
+}
+
+dsgd_status dsgd_push_gossip_round(dsgd_ctx* c, const dsgd_hyperparams* h,
+                                   const dsgd_grad_spec* g, const uint32_t* target_of) {
+  DSGD_TRY(check_ctx(c));
+  if (!h) return set_error(DSGD_EINVAL, "null hyperparams");
+  if (!c->connected) return set_error(DSGD_ESTATE, "peers not connected");
+  DSGD_TRY(check_common_round(c));
+  DSGD_TRY(check_map(c, target_of));
+  for (uint32_t k = 0; k < c->p; ++k)
+    if (target_of[k] == k) return set_error(DSGD_EINVAL, "push target must differ from sender");
+  GradSel gs;
+  DSGD_TRY(resolve_grad(c, g, &gs));
+  return dispatch(c, [&](auto z) -> dsgd_status {
+    using T = decltype(z);
+    DSGD_TRY(norm_begin(c, gs));
+    DSGD_TRY(do_push<T>(c, h, &gs, target_of));
+    finish_round(c, true);
+    return norm_end(c, gs, g);
+  });
+}
+
+dsgd_status dsgd_gossip_stale_round(dsgd_ctx* c, const dsgd_hyperparams* h,
+                                    const dsgd_grad_spec* g, const uint32_t* partner_of) {
+  DSGD_TRY(check_ctx(c));
+  if (!h) return set_error(DSGD_EINVAL, "null hyperparams");
+  if (!c->connected) return set_error(DSGD_ESTATE, "peers not connected");
+  DSGD_TRY(check_map(c, partner_of));
+  GradSel gs;
+  DSGD_TRY(resolve_grad(c, g, &gs));
+  return dispatch(c, [&](auto z) -> dsgd_status {
+    using T = decltype(z);
+    DSGD_TRY(norm_begin(c, gs));
+    DSGD_TRY(do_pull<T>(c, h, gs, partner_of, dsgd::kModeStale, (T)h->beta_gossip));
+    finish_round(c, true);
+    return norm_end(c, gs, g);
+  });
+}
+
+dsgd_status dsgd_gossip_fresh_round(dsgd_ctx* c, const dsgd_hyperparams* h,
+                                    const dsgd_grad_spec* g, const uint32_t* partner_of) {
+  DSGD_TRY(check_ctx(c));
+  if (!h) return set_error(DSGD_EINVAL, "null hyperparams");
+  if (!c->connected) return set_error(DSGD_ESTATE, "peers not connected");
+  DSGD_TRY(check_map(c, partner_of));
+  GradSel gs;
+  DSGD_TRY(resolve_grad(c, g, &gs));
+  return dispatch(c, [&](auto z) -> dsgd_status {
+    using T = decltype(z);
+    DSGD_TRY(norm_begin(c, gs));
+    // every node steps (theta' into the other buffer), then mixes with the
+    // partner's post-step theta' (simulator.cpp:305-319)
+    DSGD_TRY(do_local_step<T>(c, h, gs));
+    finish_round(c, true, true);
+    c->rounds_done -= 1;
+    DSGD_TRY(do_pull<T>(c, nullptr, gs, partner_of, dsgd::kModeMix, (T)h->beta_gossip));
+    finish_round(c, true, false);
+    return norm_end(c, gs, g);
+  });
+}
+
+dsgd_status dsgd_async_pull_event(dsgd_ctx* c, const dsgd_hyperparams* h,
+                                  const dsgd_grad_spec* g, uint32_t i, uint32_t j) {
+  DSGD_TRY(check_ctx(c));
+  if (!h) return set_error(DSGD_EINVAL, "null hyperparams");
+  if (c->distributed()) return set_error(DSGD_EINVAL, "async-pull runs on a single context");
+  if (i >= c->p || j >= c->p)
+    return set_error(DSGD_EINVAL, "async_pull_event node index out of range");
+  GradSel gs;
+  DSGD_TRY(resolve_grad(c, g, &gs));
+  return dispatch(c, [&](auto z) -> dsgd_status {
+    using T = decltype(z);
+    DSGD_TRY(norm_begin(c, gs));
+    // in place on node i (only node i changes; j == i reads the pre-event value)
+    dsgd::StepArgs<T> a{};
+    fill_node<T>(c, i, gs, h, &a.node[0], true);
+    a.node[0].theta_out = as<T>(c->theta_ptr(i, c->cur));
+    a.node[0].partner = as<T>(c->theta_ptr(j, c->cur));
+    a.node[0].norm = gs.norm ? c->norm : nullptr;
+    fill_common(c, h, gs, &a);
+    a.beta = (T)h->beta_gossip;
+    a.n_local = 1;
+    const bool vec = (gs.quad || aligned16(gs.grad[i]));
+    if (!gs.quad) a.node[0].grad = static_cast<const T*>(gs.grad[i]);
+    if (gs.noise) a.node[0].noise = as<T>(c->noise[i]);
+    const uint64_t W = vec ? 16 / sizeof(T) : 1;
+    a.blocks_per_node = blocks_for(c, (c->d / W + 1) / 2, 1);
+    {
+      LaunchScope ls(c, DSGD_K_STEP);
+      DSGD_CUDA(dsgd::launch_step<T>(dsgd::kModeAsync, a, vec, a.blocks_per_node, c->stream));
+    }
+    c->t[i] += 1;
+    if (gs.norm) {
+      DSGD_CUDA(cudaMemcpyAsync(c->norm_host, c->norm, sizeof(double), cudaMemcpyDeviceToHost,
+                                c->stream));
+      DSGD_CUDA(cudaStreamSynchronize(c->stream));
+      *g->grad_norm_out = std::max(*g->grad_norm_out, std::sqrt(c->norm_host[0]));
+    }
+    return DSGD_OK;
+  });
+}
+
+dsgd_status dsgd_pull_mix(dsgd_ctx* c, const uint32_t* partner_of) {
+  DSGD_TRY(check_ctx(c));
+  if (!c->connected) return set_error(DSGD_ESTATE, "peers not connected");
+  DSGD_TRY(check_map(c, partner_of));
+  GradSel gs;
+  gs.quad = 1;
+  return dispatch(c, [&](auto z) -> dsgd_status {
+    using T = decltype(z);
+    DSGD_TRY(do_pull<T>(c, nullptr, gs, partner_of, dsgd::kModeMix, T(0.5)));
+    finish_round(c, true, false);
+    return DSGD_OK;
+  });
+}
+
+dsgd_status dsgd_push_mix(dsgd_ctx* c, const uint32_t* target_of) {
+  DSGD_TRY(check_ctx(c));
+  if (!c->connected) return set_error(DSGD_ESTATE, "peers not connected");
+  DSGD_TRY(check_map(c, target_of));
+  for (uint32_t k = 0; k < c->p; ++k)
+    if (target_of[k] == k) return set_error(DSGD_EINVAL, "push target must differ from sender");
+  return dispatch(c, [&](auto z) -> dsgd_status {
+    using T = decltype(z);
+    DSGD_TRY(do_push<T>(c, nullptr, nullptr, target_of));
+    finish_round(c, true, false);
+    return DSGD_OK;
+  });
+}
+
+dsgd_status dsgd_gossip_fresh_mix(dsgd_ctx* c, const uint32_t* partner_of, double beta) {
+  DSGD_TRY(check_ctx(c));
+  if (!c->connected) return set_error(DSGD_ESTATE, "peers not connected");
+  DSGD_TRY(check_map(c, partner_of));
+  GradSel gs;
+  gs.quad = 1;
+  return dispatch(c, [&](auto z) -> dsgd_status {
+    using T = decltype(z);
+    DSGD_TRY(do_pull<T>(c, nullptr, gs, partner_of, dsgd::kModeMix, (T)beta));
+    finish_round(c, true, false);
+    return DSGD_OK;
+  });
+}
+
+dsgd_status dsgd_ea_set_update_out(dsgd_ctx* c, void* const* update_out) {
+  DSGD_TRY(check_ctx(c));
+  for (uint32_t i = 0; i < c->n_local; ++i) c->ea_update_out[i] = update_out ? update_out[i] : nullptr;
+  return DSGD_OK;
+}
+
+dsgd_status dsgd_ea_server_apply(dsgd_ctx* c, const void* update) {
+  DSGD_TRY(check_ctx(c));
+  if (!(c->flags & DSGD_CTX_CENTER) || c->first != 0)
+    return set_error(DSGD_ESTATE, "the server center lives on the context hosting node 0");
+  if (!update) return set_error(DSGD_EINVAL, "null update");
+  return dispatch(c, [&](auto z) -> dsgd_status {
+    using T = decltype(z);
+    dsgd::StepArgs<T> a{};
+    T* center = as<T>(c->arena + c->off_c_in);
+    a.node[0].theta_in = center;
+    a.node[0].theta_out = center;  // in place: each element read then written by one thread
+    a.node[0].aux = static_cast<T*>(const_cast<void*>(update));
+    a.d = c->d;
+    a.n_local = 1;
+    const bool vec = aligned16(update);
+    const uint64_t W = vec ? 16 / sizeof(T) : 1;
+    a.blocks_per_node = blocks_for(c, (c->d / W + 1) / 2, 1);
+    LaunchScope ls(c, DSGD_K_OTHER);
+    DSGD_CUDA(dsgd::launch_step<T>(dsgd::kModeApply, a, vec, a.blocks_per_node, c->stream));
+    return DSGD_OK;
+  });
+}
+
+dsgd_status dsgd_ea_init_center(dsgd_ctx* c) {
+  DSGD_TRY(check_ctx(c));
+  if (!(c->flags & DSGD_CTX_CENTER)) return set_error(DSGD_ESTATE, "no center (DSGD_CTX_CENTER)");
+  return dispatch(c, [&](auto z) -> dsgd_status {
+    using T = decltype(z);
+    T* center = as<T>(c->arena + c->off_c_in);
+    if (!c->distributed()) {
+      const T* xs[kMaxLocal];
+      for (uint32_t i = 0; i < c->n_local; ++i) xs[i] = as<T>(c->theta_ptr(i, c->cur));
+      LaunchScope ls(c, DSGD_K_OTHER);
+      DSGD_CUDA(dsgd::launch_spatial_mean<T>(xs, c->p, c->d, center, c->stream));
+      return DSGD_OK;
+    }
+    if (!c->comm) return set_error(DSGD_ESTATE, "multi-GPU center init needs NCCL");
+    // mean over ranks (NCCL average; not the reference's pivot order) into a
+    // scratch buffer; only node 0's context owns the server center.  (Other
+    // ranks' c_in are written by their chain predecessor only.)
+    if (!c->aux[0]) DSGD_CUDA(cudaMalloc(&c->aux[0], c->d * c->es));
+    {
+      LaunchScope ls(c, DSGD_K_NCCL);
+      DSGD_NCCL(ncclAllReduce(c->theta_ptr(0, c->cur), c->aux[0], c->d,
+                              sizeof(T) == 4 ? ncclFloat : ncclDouble, ncclAvg, c->comm,
+                              c->stream));
+    }
+    if (c->first == 0)
+      DSGD_CUDA(cudaMemcpyAsync(center, c->aux[0], c->d * c->es, cudaMemcpyDeviceToDevice,
+                                c->stream));
+    return DSGD_OK;
+  });
+}
+
+// --------------------------------------------------------- worker loop
+dsgd_status dsgd_ctx_seed_streams(dsgd_ctx* c, uint64_t seed, const char* run_id) {
+  DSGD_TRY(check_ctx(c));
+  for (auto* s : c->partner_streams) dsgd_stream_destroy(s);
+  for (auto* s : c->noise_streams) dsgd_stream_destroy(s);
+  c->partner_streams.assign(c->p, nullptr);
+  c->noise_streams.assign(c->n_local, nullptr);
+  for (uint32_t i = 0; i < c->p; ++i)
+    DSGD_TRY(dsgd_stream_make(seed, run_id, i, DSGD_PURPOSE_PARTNER, &c->partner_streams[i]));
+  for (uint32_t i = 0; i < c->n_local; ++i)
+    DSGD_TRY(dsgd_stream_make(seed, run_id, c->first + i, DSGD_PURPOSE_NOISE,
+                              &c->noise_streams[i]));
+  return DSGD_OK;
+}
+
+dsgd_status dsgd_ctx_round(dsgd_ctx* c, uint64_t* round) {
+  DSGD_TRY(check_ctx(c));
+  *round = c->rounds_done;
+  return DSGD_OK;
+}
+
+dsgd_status dsgd_run_rounds(dsgd_ctx* c, const dsgd_run_desc* run) {
+  DSGD_TRY(check_ctx(c));
+  if (!run) return set_error(DSGD_EINVAL, "null run descriptor");
+  const dsgd_protocol proto = run->protocol;
+  const bool needs_partners = proto == DSGD_PULL_GOSSIP || proto == DSGD_GOSSIP_STALE ||
+                              proto == DSGD_GOSSIP_FRESH || proto == DSGD_PUSH_GOSSIP;
+  if (needs_partners && c->partner_streams.size() != c->p)
+    return set_error(DSGD_ESTATE, "dsgd_ctx_seed_streams first");
+  if (proto == DSGD_ASYNC_PULL) return set_error(DSGD_EINVAL, "async-pull is event-driven");
+  if (run->host_noise_sigma > 0.0) {
+    if (!c->noise[0]) return set_error(DSGD_ESTATE, "host noise needs DSGD_CTX_NOISE");
+    if (c->noise_streams.size() != c->n_local)
+      return set_error(DSGD_ESTATE, "dsgd_ctx_seed_streams first");
+    if (!c->noise_host) c->noise_host = new double[c->d];
+  }
+  const dsgd_hyperparams* h = &run->hyper;
+  std::vector<uint32_t> map(c->p);
+  std::vector<const void*> grads(c->n_local);
+  for (uint64_t r = 0; r < run->rounds; ++r) {
+    const uint64_t t = c->t[0];
+    const bool gated = t > 0 && t % h->tau == 0;  // simulator.cpp:25
+    dsgd_grad_spec g = run->grad;
+    if (run->n_grad_pool > 0) {
+      const uint64_t slot = c->rounds_done % run->n_grad_pool;
+      for (uint32_t i = 0; i < c->n_local; ++i) grads[i] = run->grad_pool[slot * c->n_local + i];
+      g.source = DSGD_GRAD_BUFFER;
+      g.grad = grads.data();
+    }
+    if (run->host_noise_sigma > 0.0) {
+      // NoiseModel::sample on each local node's reference noise stream
+      for (uint32_t i = 0; i < c->n_local; ++i) {
+        dsgd_stream_fill_normal(c->noise_streams[i], run->host_noise_sigma, c->noise_host, c->d);
+        DSGD_TRY(dsgd_set_vector(c, i, DSGD_BUF_NOISE, c->noise_host));
+      }
+      g.use_noise = 1;
+    }
+    dsgd_status st = DSGD_OK;
+    switch (proto) {
+      case DSGD_ALLREDUCE:
+        st = dsgd_allreduce_round(c, h, &g, run->scope);
+        break;
+      case DSGD_ELASTIC_AVG:
+        st = dsgd_ea_round(c, h, &g, gated ? 1 : 0);
+        break;
+      case DSGD_PULL_GOSSIP:
+      case DSGD_GOSSIP_STALE:
+      case DSGD_GOSSIP_FRESH:
+        if (gated) {
+          DSGD_TRY(dsgd_draw_pull_partners(c->partner_streams.data(), c->p, map.data()));
+          st = proto == DSGD_PULL_GOSSIP    ? dsgd_pull_gossip_round(c, h, &g, map.data())
+               : proto == DSGD_GOSSIP_STALE ? dsgd_gossip_stale_round(c, h, &g, map.data())
+                                            : dsgd_gossip_fresh_round(c, h, &g, map.data());
+        } else {
+          st = dsgd_pull_gossip_round(c, h, &g, nullptr);
+        }
+        break;
+      case DSGD_PUSH_GOSSIP:
+        if (gated && c->p > 1) {
+          DSGD_TRY(dsgd_draw_push_targets(c->partner_streams.data(), c->p, map.data()));
+          st = dsgd_push_gossip_round(c, h, &g, map.data());
+        } else {
+          st = dsgd_pull_gossip_round(c, h, &g, nullptr);
+        }
+        break;
+      default:
+        return set_error(DSGD_EINVAL, "unknown protocol");
+    }
+    if (st != DSGD_OK) return st;
+  }
+  return DSGD_OK;
+}
+
+// -------------------------------------------------------- multi-GPU wiring
+dsgd_status dsgd_ctx_export_handle(dsgd_ctx* c, void* blob) {
+  DSGD_TRY(check_ctx(c));
+  if (!blob) return set_error(DSGD_EINVAL, "null blob");
+  DeviceGuard g(c->device);
+  HandleBlob b{};
+  b.magic = kMagic;
+  b.abi = DSGD_B200_ABI_VERSION;
+  b.first_node = c->first;
+  b.n_local = c->n_local;
+  b.dtype = c->dtype;
+  b.flags = c->flags;
+  b.d = c->d;
+  b.device = c->device;
+  DSGD_CUDA(cudaIpcGetMemHandle(&b.handle, c->arena));
+  b.arena_bytes = c->arena_bytes;
+  b.off_theta[0] = c->off_theta[0][0];
+  b.off_theta[1] = c->off_theta[0][1];
+  b.off_c_in = c->off_c_in;
+  b.off_flags = c->off_flags;
+  b.off_round = c->off_round;
+  std::memset(blob, 0, DSGD_HANDLE_BYTES);
+  std::memcpy(blob, &b, sizeof(b));
+  return DSGD_OK;
+}
+
+dsgd_status dsgd_ctx_connect_peers(dsgd_ctx* c, const void* blobs) {
+  DSGD_TRY(check_ctx(c));
+  if (!blobs) return set_error(DSGD_EINVAL, "null blobs");
+  if (!c->distributed()) {
+    c->connected = true;
+    return DSGD_OK;
+  }
+  DeviceGuard g(c->device);
+  const char* base = static_cast<const char*>(blobs);
+  for (uint32_t k = 0; k < c->p; ++k) {
+    HandleBlob b;
+    std::memcpy(&b, base + (size_t)k * DSGD_HANDLE_BYTES, sizeof(b));
+    if (b.magic != kMagic || b.abi != DSGD_B200_ABI_VERSION)
+      return set_error(DSGD_EINVAL, "bad handle blob");
+    if (b.first_node != k || b.n_local != 1)
+      return set_error(DSGD_EINVAL, "blob order must be node order, one node per context");
+    if (b.d != c->d || b.dtype != (uint32_t)c->dtype)
+      return set_error(DSGD_EINVAL, "peer dimension/dtype mismatch");
+    if ((b.flags & DSGD_CTX_CENTER) != (c->flags & DSGD_CTX_CENTER))
+      return set_error(DSGD_EINVAL, "DSGD_CTX_CENTER must match on every rank");
+    if (k == c->first) continue;
+    if (b.device != c->device) {
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, c->device, b.device);
+      if (can) {
+        cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+          return set_error(DSGD_ECUDA, std::string("enable peer access: ") + cudaGetErrorString(e));
+        cudaGetLastError();
+      }
+    }
+    void* mapped = nullptr;
+    DSGD_CUDA(cudaIpcOpenMemHandle(&mapped, b.handle, cudaIpcMemLazyEnablePeerAccess));
+    c->ipc_opened.push_back(mapped);
+    char* m = static_cast<char*>(mapped);
+    PeerNode& pn = c->peers[k];
+    pn.theta[0] = m + b.off_theta[0];
+    pn.theta[1] = m + b.off_theta[1];
+    pn.round = reinterpret_cast<unsigned long long*>(m + b.off_round);
+    if (b.flags & DSGD_CTX_CENTER) {
+      pn.c_in = m + b.off_c_in;
+      pn.flags = reinterpret_cast<unsigned long long*>(m + b.off_flags);
+    }
+  }
+  c->connected = true;
+  return DSGD_OK;
+}
+
+dsgd_status dsgd_nccl_unique_id(void* id) {
+  if (!id) return set_error(DSGD_EINVAL, "null id");
+  static_assert(sizeof(ncclUniqueId) == DSGD_NCCL_ID_BYTES, "nccl id size");
+  ncclUniqueId u;
+  DSGD_NCCL(ncclGetUniqueId(&u));
+  std::memcpy(id, &u, sizeof(u));
+  return DSGD_OK;
+}
+
+dsgd_status dsgd_ctx_init_nccl(dsgd_ctx* c, const void* id, int rank, int nranks) {
+  DSGD_TRY(check_ctx(c));
+  if (!id || nranks <= 0 || rank < 0 || rank >= nranks)
+    return set_error(DSGD_EINVAL, "bad nccl rank/size");
+  if ((uint32_t)nranks != c->p || (uint32_t)rank != c->first)
+    return set_error(DSGD_EINVAL, "NCCL ranks must equal node ids (one node per context)");
+  DeviceGuard g(c->device);
+  ncclUniqueId u;
+  std::memcpy(&u, id, sizeof(u));
+  DSGD_NCCL(ncclCommInitRank(&c->comm, nranks, u, rank));
+  return DSGD_OK;
+}
+
+// ------------------------------------------------------------ measurement
+dsgd_status dsgd_profile_enable(dsgd_ctx* c, int enable) {
+  DSGD_TRY(check_ctx(c));
+  DeviceGuard g(c->device);
+  if (!enable) DSGD_TRY(collect_profile(c));
+  c->profile = enable != 0;
+  return DSGD_OK;
+}
+
+dsgd_status dsgd_profile_read(dsgd_ctx* c, dsgd_kernel_id k, double* total_ms, uint64_t* launches,
+                              int reset) {
+  DSGD_TRY(check_ctx(c));
+  if ((int)k < 0 || k >= DSGD_K_COUNT) return set_error(DSGD_EINVAL, "kernel id");
+  DeviceGuard g(c->device);
+  DSGD_TRY(collect_profile(c));
+  if (total_ms) *total_ms = c->prof_ms[k];
+  if (launches) *launches = c->prof_launches[k];
+  if (reset) {
+    c->prof_ms[k] = 0;
+    c->prof_launches[k] = 0;
+  }
+  return DSGD_OK;
+}
+
+dsgd_status dsgd_launch_count(dsgd_ctx* c, uint64_t* kernels, uint64_t* nccl_calls) {
+  DSGD_TRY(check_ctx(c));
+  if (kernels) *kernels = c->kernels;
+  if (nccl_calls) *nccl_calls = c->nccl_calls;
+  return DSGD_OK;
+}
+
+}  // extern "C"
