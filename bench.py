@@ -72,10 +72,13 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 10:   # sampler is live
+                time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
@@ -203,31 +206,42 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # warm-up
-    rounds(args.warmup)
+    # warm-up (also sizes the clock-sampling load below)
+    t_w = time.perf_counter()
+    rounds(max(3, args.warmup))
     grp.sync()
+    est = max_over_ranks((time.perf_counter() - t_w) / max(3, args.warmup))
     barrier()
     torch.cuda.synchronize()
+    load_rounds = int(min(20000, max(50, 0.6 / max(est, 1e-6))))  # same count on every rank
+
+    def load():
+        # untimed sustained load around the (milliseconds-long) timed region so
+        # the nvidia-smi samples see the GPU under this kernel
+        rounds(load_rounds)
+        grp.sync()
 
     # ---------------- timed region (device-resident inputs)
-    k0, n0 = grp.launch_count()
-    grp.profile(True)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
+        load()
         barrier()
         torch.cuda.synchronize()
+        grp.profile(True)
+        k0, n0 = grp.launch_count()
         ev0.record(stream)
         rounds(args.steps)
         ev1.record(stream)
         grp.sync()
         torch.cuda.synchronize()
+        k1, n1 = grp.launch_count()
+        prof = {N.KERNEL_NAMES[k]: grp.profile_read(k, reset=True) for k in range(8)}
         barrier()
+        grp.profile(False)
+        load()
     ms = ev0.elapsed_time(ev1)
     ms_max = max_over_ranks(ms)
-    k1, n1 = grp.launch_count()
-    prof = {N.KERNEL_NAMES[k]: grp.profile_read(k, reset=True) for k in range(8)}
-    grp.profile(False)
     step_ms = ms_max / args.steps
     value = world * d / (step_ms * 1e-3)
 
@@ -324,7 +338,10 @@ def main():
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": (k1 - k0) + (n1 - n0),
                 "gpu_launches_detail": {"kernels": k1 - k0, "nccl_calls": n1 - n0},
-                "per_kernel": per_kernel, "clocks": clocks.summary(), "extras": extras}
+                "per_kernel": per_kernel,
+                "clocks": dict(clocks.summary(), window="nvidia-smi -lms 50 over ~0.6 s of the same "
+                               "rounds before and after the timed region, and during it"),
+                "extras": extras}
         print(json.dumps(line), flush=True)
     grp.close()
     if world > 1:

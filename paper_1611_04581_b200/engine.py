@@ -385,18 +385,10 @@ class Group:
                     nccl: bool = True, **kw) -> "Group":
         """One node per process/GPU; wires IPC peers and NCCL through the
         already-initialised torch.distributed process group (any backend)."""
-        import torch.distributed as dist
         g = cls(d, p=world, dtype=dtype, device=device, first_node=rank, n_local=1, **kw)
-        if world > 1:
-            blobs = [None] * world
-            dist.all_gather_object(blobs, g.export_handle())
-            g.connect_peers(blobs)
-            if nccl:
-                uid = [cls.nccl_unique_id() if rank == 0 else None]
-                dist.broadcast_object_list(uid, src=0)
-                g.init_nccl(uid[0], rank, world)
-        else:
-            g.connect_peers([g.export_handle()])
+        g.connect_peers(exchange_blobs(g.export_handle(), rank, world))
+        if nccl and world > 1:
+            g.init_nccl(broadcast_nccl_id(rank, world), rank, world)
         return g
 
     # --------------------------------------------------------- measurement
@@ -414,3 +406,29 @@ class Group:
         n = C.c_uint64()
         N.check(self.lib.dsgd_launch_count(self._ctx, C.byref(k), C.byref(n)))
         return k.value, n.value
+
+
+# ------------------------------------------------------ out-of-band wiring
+def exchange_blobs(blob: bytes, rank: int, world: int) -> list:
+    """All-gather the per-context handle blobs in node order over the
+    torch.distributed group (the host-side half of dsgd_ctx_connect_peers)."""
+    if len(blob) != N.HANDLE_BYTES:
+        raise N.InvalidArgument("handle blob size")
+    if world == 1:
+        return [blob]
+    import torch.distributed as dist
+    blobs = [None] * world
+    dist.all_gather_object(blobs, (rank, blob))
+    blobs.sort(key=lambda x: x[0])
+    if [r for r, _ in blobs] != list(range(world)):
+        raise N.InvalidArgument("ranks must be 0..world-1")
+    return [b for _, b in blobs]
+
+
+def broadcast_nccl_id(rank: int, world: int, make=None) -> bytes:
+    """Rank 0 creates the NCCL unique id, everyone receives it."""
+    import torch.distributed as dist
+    uid = [(make or Group.nccl_unique_id)() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(uid, src=0)
+    return uid[0]

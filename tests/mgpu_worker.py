@@ -1,0 +1,88 @@
+"""Multi-GPU parity worker (launched by tests/test_multigpu.py under
+torchrun, one process per GPU).  Each rank hosts one node; after a run the
+ranks all-gather their states and rank 0 compares with the oracle."""
+import json
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    import torch
+    import torch.distributed as dist
+
+    import oracle as O
+    from paper_1611_04581_b200 import driver as D
+    from paper_1611_04581_b200 import protocols as P
+    from paper_1611_04581_b200.engine import Group, Hyperparams
+
+    rank, world, local = (int(os.environ[k]) for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dtype = sys.argv[1] if len(sys.argv) > 1 else "f64"
+    results = {}
+    names = {"all-reduce": O.ALLREDUCE, "elastic-avg": O.ELASTIC, "pull-gossip": O.PULL,
+             "push-gossip": O.PUSH, "gossip-stale": O.STALE, "gossip-fresh": O.FRESH}
+    for proto, oid in names.items():
+        d = 1031
+        hk = dict(alpha0=0.05, anneal_at=(20,), mu=0.9, weight_decay=1e-4, beta_gossip=0.4,
+                  beta_ea=0.15, tau=1)
+        cfg = O.SimConfig(protocol=oid, p=world, hyper=O.HyperParams(**hk), sigma=0.05,
+                          spectrum=list(np.linspace(0.5, 2.0, d)),
+                          init_kind=O.INIT_OFFSET_ONES if proto == "all-reduce" else O.INIT_GAUSSIAN,
+                          rounds=25, per_node_scope=False, run_id=f"mg/{proto}")
+        obj = P.QuadraticObjective(cfg.spectrum)
+        dcfg = D.SimConfig(protocol=proto, p=world, hyper=Hyperparams(**hk),
+                           noise=P.NoiseModel.gaussian_per_coord(0.05, d),
+                           init=D.InitSpec("offset-ones" if proto == "all-reduce" else "gaussian-spread"),
+                           momentum_scope="aggregate",
+                           rounds=25, run_id=f"mg/{proto}")
+        thetas = D.make_initial_nodes(dcfg, obj)
+        g = Group.distributed(d, rank, world, local, dtype=dtype, quadratic=True, noise=True,
+                              center=proto == "elastic-avg")
+        g.set_timeout(20.0)
+        g.set_quadratic(obj.spectrum)
+        g.set_state(0, thetas[rank])
+        if proto == "elastic-avg" and rank == 0:
+            # the reference's pivot-form spatial mean of the initial thetas
+            c = thetas[0].copy()
+            dev = np.zeros(d)
+            for i in range(1, world):
+                dev = dev + (thetas[i] - thetas[0])
+            c = thetas[0] + dev * (1.0 / world)
+            g.set_center(c)
+        dist.barrier()
+        g.seed_streams(1, f"mg/{proto}")
+        g.run_rounds(D.PROTOCOLS[proto], Hyperparams(**hk), 25, scope="aggregate",
+                     grad="quadratic", host_noise_sigma=0.05)
+        g.sync()
+        th, dp, t = g.get_state(0)
+        center = g.get_center() if proto == "elastic-avg" and rank == 0 else None
+        allst = [None] * world
+        dist.all_gather_object(allst, (th, dp, t))
+        if rank == 0:
+            npd = np.float64 if dtype == "f64" else np.float32
+            oth, odp, ot, oc = O.run(cfg, dtype=npd)
+            dev_th = np.array([s[0] for s in allst]).astype(npd)
+            exact = dev_th.tobytes() == oth.tobytes()
+            rel = float(np.abs(dev_th.astype(float) - oth.astype(float)).max() /
+                        np.abs(oth).max())
+            same_ranks = all(np.array_equal(allst[0][0], s[0]) for s in allst)
+            cexact = None
+            if center is not None:
+                cexact = center.astype(npd).tobytes() == oc.tobytes()
+            results[proto] = {"bit_exact": exact, "max_rel": rel, "ranks_identical": same_ranks,
+                              "center_exact": cexact}
+        dist.barrier()
+        g.close()
+    if rank == 0:
+        print("RESULT " + json.dumps(results), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
