@@ -1,0 +1,30 @@
+"""The C++ drop-in header (include/dsgd_b200.hpp) compiles and links
+against libdsgd_b200.so (CPU), and a reference-style C++ caller reproduces
+test_protocols.cpp hand values on the GPU."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SRC = os.path.join(ROOT, "tests", "cpp", "reference_style.cpp")
+LIBDIR = os.path.join(ROOT, "paper_1611_04581_b200")
+
+
+def build(tmp_path):
+    exe = os.path.join(str(tmp_path), "reference_style")
+    subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"), SRC,
+                    "-L", LIBDIR, "-ldsgd_b200", f"-Wl,-rpath,{LIBDIR}", "-o", exe], check=True)
+    return exe
+
+
+def test_cpp_header_builds_and_links(tmp_path):
+    assert os.path.exists(build(tmp_path))
+
+
+@pytest.mark.gpu
+def test_cpp_caller_runs_on_gpu(tmp_path):
+    exe = build(tmp_path)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    assert "all checks passed" in out.stdout
