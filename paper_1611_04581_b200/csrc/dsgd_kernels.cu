@@ -117,10 +117,16 @@ __device__ __forceinline__ void step_group(const StepArgs<T>& a, const NodeIO<T>
   ld(x, n.theta_in, k);
   if constexpr (MODE == kModePull || MODE == kModeStale || MODE == kModeMix || MODE == kModeAsync)
     ld(xj, n.partner, k);
-  if constexpr (MODE == kModeApply) ld(ax, n.aux, k);
+  if constexpr (MODE == kModeApply || MODE == kModeApplyDelta) ld(ax, n.aux, k);
   if constexpr (MODE == kModeStep || MODE == kModePull || MODE == kModeStale ||
-                MODE == kModeArDelta)
+                MODE == kModeArDelta) {
     ld(dp, n.delta, k);
+  } else if constexpr (MODE == kModeApplyDelta) {
+    if (n.aux != n.delta)
+      ld(dp, n.delta, k);  // per-node scope: own delta_prev
+    else
+      dp = ax;             // aggregate scope: delta_prev is the average itself
+  }
   if constexpr (MODE != kModeMix && MODE != kModeApply)
     ld_grad_inputs(gb, s, o, xi, n.grad, a.spec, a.opt, n.noise, a.quad, k);
 #pragma unroll
@@ -148,6 +154,13 @@ __device__ __forceinline__ void step_group(const StepArgs<T>& a, const NodeIO<T>
                              a.wd, a.mu_nz, a.wd_pos, a.quad, norm, nacc);
     } else if constexpr (MODE == kModeApply) {
       out_t.v[l] = radd(x.v[l], ax.v[l]);
+    } else if constexpr (MODE == kModeApplyDelta) {
+      // theta_{t+1} = theta_t + avg_t  (protocols.cpp:126), then round t+1's
+      // compute_local_delta at theta_{t+1}, in one pass
+      const T x1 = radd(x.v[l], ax.v[l]);
+      out_t.v[l] = x1;
+      out_d.v[l] = sgd_delta(x1, dp.v[l], gb.v[l], s.v[l], o.v[l], xi.v[l], n.alpha, a.mu, a.wd,
+                             a.mu_nz, a.wd_pos, a.quad, norm, nacc);
     } else {  // kModeAsync: no lookahead, no momentum; y = x + (-alpha)*g
       T g = a.quad ? rmul(s.v[l], rsub(x.v[l], o.v[l])) : gb.v[l];
       if (a.wd_pos) g = radd(g, rmul(a.wd, x.v[l]));
@@ -160,6 +173,10 @@ __device__ __forceinline__ void step_group(const StepArgs<T>& a, const NodeIO<T>
   if constexpr (MODE == kModeArDelta) {
     st(n.aux, k, out_d);
     if (n.aux != n.delta) st(n.delta, k, out_d);  // per-node scope keeps the own delta
+  } else if constexpr (MODE == kModeApplyDelta) {
+    st(n.theta_out, k, out_t);
+    st(n.aux, k, out_d);
+    if (n.aux != n.delta) st(n.delta, k, out_d);
   } else {
     st(n.theta_out, k, out_t);
     if constexpr (MODE == kModeStep || MODE == kModePull || MODE == kModeStale)
@@ -211,6 +228,7 @@ cudaError_t launch_step(int mode, const StepArgs<T>& a, int vec, uint32_t grid, 
     DSGD_STEP_CASE(kModeArDelta)
     DSGD_STEP_CASE(kModeApply)
     DSGD_STEP_CASE(kModeAsync)
+    DSGD_STEP_CASE(kModeApplyDelta)
     default:
       return cudaErrorInvalidValue;
   }

@@ -31,7 +31,8 @@ enum StepMode : int {
   kModeMix = 3,      // mix only (pull_mix / gossip_fresh_mix)
   kModeArDelta = 4,  // compute_local_delta -> aux            protocols.cpp:85-100
   kModeApply = 5,    // theta += aux (averaged delta)        protocols.cpp:125-129
-  kModeAsync = 6     // async_pull_event                      protocols.cpp:278-297
+  kModeAsync = 6,    // async_pull_event                      protocols.cpp:278-297
+  kModeApplyDelta = 7  // previous round's theta += avg fused with this round's delta
 };
 
 template <typename T>

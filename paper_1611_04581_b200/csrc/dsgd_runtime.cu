@@ -154,6 +154,8 @@ struct dsgd_ctx {
   uint64_t ea_seq = 0;           // gated EASGD rounds run (multi-GPU chain)
   void* ea_update_out[kMaxLocal] = {};   // optional ea_client_step update outputs
   std::vector<uint32_t> prev_readers;  // nodes that read this context's snapshot last round
+  bool ar_pending = false;             // multi-GPU all-reduce: theta += avg not yet applied
+  dsgd_momentum_scope ar_pending_scope = DSGD_SCOPE_AGGREGATE;
   unsigned long long timeout_ns = 30ull * 1000 * 1000 * 1000;
 
   // multi-GPU
@@ -438,6 +440,36 @@ dsgd_status do_pull(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& gs,
   return DSGD_OK;
 }
 
+// Materialises a deferred multi-GPU all-reduce apply: theta += avg.
+template <typename T>
+dsgd_status flush_pending_t(dsgd_ctx* c) {
+  if (!c->ar_pending) return DSGD_OK;
+  char* xbuf = c->ar_pending_scope == DSGD_SCOPE_PER_NODE ? c->aux[0] : c->delta[0];
+  dsgd::StepArgs<T> a{};
+  a.node[0].theta_in = as<T>(c->theta_ptr(0, c->cur));
+  a.node[0].theta_out = as<T>(c->theta_ptr(0, c->cur ^ 1));
+  a.node[0].aux = as<T>(xbuf);
+  a.d = c->d;
+  a.n_local = 1;
+  const uint64_t W = 16 / sizeof(T);
+  a.blocks_per_node = blocks_for(c, (c->d / W + 1) / 2, 1);
+  build_signal(c, &a.signal);
+  {
+    LaunchScope ls(c, DSGD_K_AR_APPLY);
+    DSGD_CUDA(dsgd::launch_step<T>(dsgd::kModeApply, a, 1, a.blocks_per_node, c->stream));
+  }
+  c->seq += 1;
+  c->cur ^= 1;
+  c->ar_pending = false;
+  return DSGD_OK;
+}
+
+dsgd_status flush_pending(dsgd_ctx* c) {
+  if (!c->ar_pending) return DSGD_OK;
+  DeviceGuard g(c->device);
+  return c->dtype == DSGD_F32 ? flush_pending_t<float>(c) : flush_pending_t<double>(c);
+}
+
 template <typename T>
 dsgd_status do_allreduce(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& gs,
                          dsgd_momentum_scope scope) {
@@ -457,12 +489,17 @@ dsgd_status do_allreduce(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& 
     return DSGD_OK;
   }
   if (!c->comm) return set_error(DSGD_ESTATE, "multi-GPU all-reduce needs dsgd_ctx_init_nccl");
-  // delta kernel -> ncclAllReduce(avg) in place on the exchange buffer ->
-  // apply kernel.  Aggregate scope exchanges delta_prev itself, so the
-  // averaged delta lands where the next round's momentum reads it.
+  // delta kernel -> ncclAllReduce(avg) in place on the exchange buffer.
+  // Aggregate scope exchanges delta_prev itself, so the averaged delta lands
+  // where the next round's momentum reads it.  The apply theta += avg
+  // (protocols.cpp:126) is deferred and fused into the next round's delta
+  // kernel (kModeApplyDelta: 20 instead of 16 + 12 B/param); any other call
+  // first materialises it (flush_pending).
   const bool per_node = scope == DSGD_SCOPE_PER_NODE;
+  if (c->ar_pending && c->ar_pending_scope != scope) DSGD_TRY(flush_pending_t<T>(c));
   if (per_node && !c->aux[0]) DSGD_CUDA(cudaMalloc(&c->aux[0], c->d * c->es));
   char* xbuf = per_node ? c->aux[0] : c->delta[0];
+  const bool fused = c->ar_pending;
   {
     dsgd::StepArgs<T> a{};
     fill_node<T>(c, 0, gs, h, &a.node[0]);
@@ -473,27 +510,17 @@ dsgd_status do_allreduce(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& 
     const uint64_t W = vec ? 16 / sizeof(T) : 1;
     a.blocks_per_node = blocks_for(c, (c->d / W + 1) / 2, 1);
     LaunchScope ls(c, DSGD_K_AR_DELTA);
-    DSGD_CUDA(dsgd::launch_step<T>(dsgd::kModeArDelta, a, vec, a.blocks_per_node, c->stream));
+    DSGD_CUDA(dsgd::launch_step<T>(fused ? dsgd::kModeApplyDelta : dsgd::kModeArDelta, a, vec,
+                                   a.blocks_per_node, c->stream));
   }
+  if (fused) c->cur ^= 1;  // theta_{t} + avg_{t-1} now materialised in the other buffer
   {
     LaunchScope ls(c, DSGD_K_NCCL);
     DSGD_NCCL(ncclAllReduce(xbuf, xbuf, c->d, sizeof(T) == 4 ? ncclFloat : ncclDouble, ncclAvg,
                             c->comm, c->stream));
   }
-  {
-    dsgd::StepArgs<T> a{};
-    fill_node<T>(c, 0, gs, nullptr, &a.node[0]);
-    a.node[0].aux = as<T>(xbuf);
-    a.node[0].norm = nullptr;
-    a.d = c->d;
-    a.n_local = 1;
-    const uint64_t W = 16 / sizeof(T);
-    a.blocks_per_node = blocks_for(c, (c->d / W + 1) / 2, 1);
-    build_signal(c, &a.signal);
-    LaunchScope ls(c, DSGD_K_AR_APPLY);
-    DSGD_CUDA(dsgd::launch_step<T>(dsgd::kModeApply, a, 1, a.blocks_per_node, c->stream));
-    c->seq += 1;
-  }
+  c->ar_pending = true;
+  c->ar_pending_scope = scope;
   c->prev_readers.clear();
   return DSGD_OK;
 }
@@ -547,8 +574,10 @@ dsgd_status do_ea(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& gs, int
   a.timeout_ns = c->timeout_ns;
   a.error = c->error;
   const bool vec = all_aligned(c, gs);
-  const uint32_t grid =
-      (uint32_t)std::min<uint64_t>(c->n_chunks, (uint64_t)c->sm_count * c->blocks_per_sm);
+  // one CTA per chunk: a CTA blocked on its flag or in its release fence
+  // leaves the SM to the other resident chunks (dispatch is in chunk order,
+  // the order the previous rank produces them)
+  const uint32_t grid = (uint32_t)std::min<uint64_t>(c->n_chunks, 0x7fffffffu);
   LaunchScope ls(c, DSGD_K_EA);
   DSGD_CUDA(dsgd::launch_ea_chain<T>(a, vec, grid, c->stream));
   c->prev_readers.clear();
@@ -800,6 +829,7 @@ dsgd_status dsgd_ctx_set_timeout(dsgd_ctx* c, double seconds) {
 
 dsgd_status dsgd_buffer_ptr(dsgd_ctx* c, uint32_t local, dsgd_buffer which, void** dev) {
   DSGD_TRY(check_ctx(c));
+  if (which == DSGD_BUF_THETA || which == DSGD_BUF_DELTA) DSGD_TRY(flush_pending(c));
   if (local >= c->n_local) return set_error(DSGD_EINVAL, "local node out of range");
   char* p = buffer_of(c, local, which);
   if (!p) return set_error(DSGD_ESTATE, "buffer not allocated for this context");
@@ -810,6 +840,7 @@ dsgd_status dsgd_buffer_ptr(dsgd_ctx* c, uint32_t local, dsgd_buffer which, void
 dsgd_status dsgd_set_state(dsgd_ctx* c, uint32_t local, const double* theta,
                            const double* delta_prev, uint64_t t) {
   DSGD_TRY(check_ctx(c));
+  DSGD_TRY(flush_pending(c));
   if (local >= c->n_local) return set_error(DSGD_EINVAL, "local node out of range");
   DeviceGuard g(c->device);
   if (theta) DSGD_TRY(upload_vec(c, c->theta_ptr(local, c->cur), theta));
@@ -821,6 +852,7 @@ dsgd_status dsgd_set_state(dsgd_ctx* c, uint32_t local, const double* theta,
 dsgd_status dsgd_get_state(dsgd_ctx* c, uint32_t local, double* theta, double* delta_prev,
                            uint64_t* t) {
   DSGD_TRY(check_ctx(c));
+  DSGD_TRY(flush_pending(c));
   if (local >= c->n_local) return set_error(DSGD_EINVAL, "local node out of range");
   DeviceGuard g(c->device);
   DSGD_TRY(dsgd_ctx_sync(c));
@@ -832,6 +864,7 @@ dsgd_status dsgd_get_state(dsgd_ctx* c, uint32_t local, double* theta, double* d
 
 dsgd_status dsgd_set_vector(dsgd_ctx* c, uint32_t local, dsgd_buffer which, const double* host) {
   DSGD_TRY(check_ctx(c));
+  if (which == DSGD_BUF_THETA || which == DSGD_BUF_DELTA) DSGD_TRY(flush_pending(c));
   if (local >= c->n_local) return set_error(DSGD_EINVAL, "local node out of range");
   char* p = buffer_of(c, local, which);
   if (!p) return set_error(DSGD_ESTATE, "buffer not allocated for this context");
@@ -841,6 +874,7 @@ dsgd_status dsgd_set_vector(dsgd_ctx* c, uint32_t local, dsgd_buffer which, cons
 
 dsgd_status dsgd_get_vector(dsgd_ctx* c, uint32_t local, dsgd_buffer which, double* host) {
   DSGD_TRY(check_ctx(c));
+  if (which == DSGD_BUF_THETA || which == DSGD_BUF_DELTA) DSGD_TRY(flush_pending(c));
   if (local >= c->n_local) return set_error(DSGD_EINVAL, "local node out of range");
   char* p = buffer_of(c, local, which);
   if (!p) return set_error(DSGD_ESTATE, "buffer not allocated for this context");
@@ -851,6 +885,7 @@ dsgd_status dsgd_get_vector(dsgd_ctx* c, uint32_t local, dsgd_buffer which, doub
 dsgd_status dsgd_upload_async(dsgd_ctx* c, uint32_t local, dsgd_buffer which, const void* host,
                               uint64_t count) {
   DSGD_TRY(check_ctx(c));
+  if (which == DSGD_BUF_THETA || which == DSGD_BUF_DELTA) DSGD_TRY(flush_pending(c));
   if (local >= c->n_local || count > c->d) return set_error(DSGD_EINVAL, "range");
   char* p = buffer_of(c, local, which);
   if (!p) return set_error(DSGD_ESTATE, "buffer not allocated for this context");
@@ -862,6 +897,7 @@ dsgd_status dsgd_upload_async(dsgd_ctx* c, uint32_t local, dsgd_buffer which, co
 dsgd_status dsgd_download_async(dsgd_ctx* c, uint32_t local, dsgd_buffer which, void* host,
                                 uint64_t count) {
   DSGD_TRY(check_ctx(c));
+  if (which == DSGD_BUF_THETA || which == DSGD_BUF_DELTA) DSGD_TRY(flush_pending(c));
   if (local >= c->n_local || count > c->d) return set_error(DSGD_EINVAL, "range");
   char* p = buffer_of(c, local, which);
   if (!p) return set_error(DSGD_ESTATE, "buffer not allocated for this context");
@@ -873,6 +909,7 @@ dsgd_status dsgd_download_async(dsgd_ctx* c, uint32_t local, dsgd_buffer which, 
 dsgd_status dsgd_copy_in_async(dsgd_ctx* c, uint32_t local, dsgd_buffer which, const void* src,
                                uint64_t count) {
   DSGD_TRY(check_ctx(c));
+  if (which == DSGD_BUF_THETA || which == DSGD_BUF_DELTA) DSGD_TRY(flush_pending(c));
   if (local >= c->n_local || count > c->d || !src) return set_error(DSGD_EINVAL, "range");
   char* p = buffer_of(c, local, which);
   if (!p) return set_error(DSGD_ESTATE, "buffer not allocated for this context");
@@ -898,6 +935,7 @@ dsgd_status dsgd_set_t(dsgd_ctx* c, uint32_t local, uint64_t t) {
 // ----------------------------------------------------------- update rules
 dsgd_status dsgd_local_sgd_step(dsgd_ctx* c, const dsgd_hyperparams* h, const dsgd_grad_spec* g) {
   DSGD_TRY(check_ctx(c));
+  DSGD_TRY(flush_pending(c));
   if (!h) return set_error(DSGD_EINVAL, "null hyperparams");
   if (!c->connected) return set_error(DSGD_ESTATE, "peers not connected");
   GradSel gs;
@@ -923,7 +961,7 @@ dsgd_status dsgd_allreduce_round(dsgd_ctx* c, const dsgd_hyperparams* h, const d
     using T = decltype(z);
     DSGD_TRY(norm_begin(c, gs));
     DSGD_TRY(do_allreduce<T>(c, h, gs, scope));
-    finish_round(c, true);
+    finish_round(c, !c->distributed());  // multi-GPU: do_allreduce tracks the buffers
     return norm_end(c, gs, g);
   });
 }
@@ -931,6 +969,7 @@ dsgd_status dsgd_allreduce_round(dsgd_ctx* c, const dsgd_hyperparams* h, const d
 dsgd_status dsgd_ea_round(dsgd_ctx* c, const dsgd_hyperparams* h, const dsgd_grad_spec* g,
                           int gated) {
   DSGD_TRY(check_ctx(c));
+  DSGD_TRY(flush_pending(c));
   if (!h) return set_error(DSGD_EINVAL, "null hyperparams");
   if (!c->connected) return set_error(DSGD_ESTATE, "peers not connected");
   GradSel gs;
@@ -947,6 +986,7 @@ dsgd_status dsgd_ea_round(dsgd_ctx* c, const dsgd_hyperparams* h, const dsgd_gra
 dsgd_status dsgd_pull_gossip_round(dsgd_ctx* c, const dsgd_hyperparams* h,
                                    const dsgd_grad_spec* g, const uint32_t* partner_of) {
   DSGD_TRY(check_ctx(c));
+  DSGD_TRY(flush_pending(c));
   if (!h) return set_error(DSGD_EINVAL, "null hyperparams");
   if (!c->connected) return set_error(DSGD_ESTATE, "peers not connected");
   DSGD_TRY(check_common_round(c));
@@ -968,6 +1008,7 @@ dsgd_status dsgd_pull_gossip_round(dsgd_ctx* c, const dsgd_hyperparams* h,
 dsgd_status dsgd_push_gossip_round(dsgd_ctx* c, const dsgd_hyperparams* h,
                                    const dsgd_grad_spec* g, const uint32_t* target_of) {
   DSGD_TRY(check_ctx(c));
+  DSGD_TRY(flush_pending(c));
   if (!h) return set_error(DSGD_EINVAL, "null hyperparams");
   if (!c->connected) return set_error(DSGD_ESTATE, "peers not connected");
   DSGD_TRY(check_common_round(c));
@@ -988,6 +1029,7 @@ dsgd_status dsgd_push_gossip_round(dsgd_ctx* c, const dsgd_hyperparams* h,
 dsgd_status dsgd_gossip_stale_round(dsgd_ctx* c, const dsgd_hyperparams* h,
                                     const dsgd_grad_spec* g, const uint32_t* partner_of) {
   DSGD_TRY(check_ctx(c));
+  DSGD_TRY(flush_pending(c));
   if (!h) return set_error(DSGD_EINVAL, "null hyperparams");
   if (!c->connected) return set_error(DSGD_ESTATE, "peers not connected");
   DSGD_TRY(check_map(c, partner_of));
@@ -1005,6 +1047,7 @@ dsgd_status dsgd_gossip_stale_round(dsgd_ctx* c, const dsgd_hyperparams* h,
 dsgd_status dsgd_gossip_fresh_round(dsgd_ctx* c, const dsgd_hyperparams* h,
                                     const dsgd_grad_spec* g, const uint32_t* partner_of) {
   DSGD_TRY(check_ctx(c));
+  DSGD_TRY(flush_pending(c));
   if (!h) return set_error(DSGD_EINVAL, "null hyperparams");
   if (!c->connected) return set_error(DSGD_ESTATE, "peers not connected");
   DSGD_TRY(check_map(c, partner_of));
@@ -1027,6 +1070,7 @@ dsgd_status dsgd_gossip_fresh_round(dsgd_ctx* c, const dsgd_hyperparams* h,
 dsgd_status dsgd_async_pull_event(dsgd_ctx* c, const dsgd_hyperparams* h,
                                   const dsgd_grad_spec* g, uint32_t i, uint32_t j) {
   DSGD_TRY(check_ctx(c));
+  DSGD_TRY(flush_pending(c));
   if (!h) return set_error(DSGD_EINVAL, "null hyperparams");
   if (c->distributed()) return set_error(DSGD_EINVAL, "async-pull runs on a single context");
   if (i >= c->p || j >= c->p)
@@ -1067,6 +1111,7 @@ dsgd_status dsgd_async_pull_event(dsgd_ctx* c, const dsgd_hyperparams* h,
 
 dsgd_status dsgd_pull_mix(dsgd_ctx* c, const uint32_t* partner_of) {
   DSGD_TRY(check_ctx(c));
+  DSGD_TRY(flush_pending(c));
   if (!c->connected) return set_error(DSGD_ESTATE, "peers not connected");
   DSGD_TRY(check_map(c, partner_of));
   GradSel gs;
@@ -1081,6 +1126,7 @@ dsgd_status dsgd_pull_mix(dsgd_ctx* c, const uint32_t* partner_of) {
 
 dsgd_status dsgd_push_mix(dsgd_ctx* c, const uint32_t* target_of) {
   DSGD_TRY(check_ctx(c));
+  DSGD_TRY(flush_pending(c));
   if (!c->connected) return set_error(DSGD_ESTATE, "peers not connected");
   DSGD_TRY(check_map(c, target_of));
   for (uint32_t k = 0; k < c->p; ++k)
@@ -1095,6 +1141,7 @@ dsgd_status dsgd_push_mix(dsgd_ctx* c, const uint32_t* target_of) {
 
 dsgd_status dsgd_gossip_fresh_mix(dsgd_ctx* c, const uint32_t* partner_of, double beta) {
   DSGD_TRY(check_ctx(c));
+  DSGD_TRY(flush_pending(c));
   if (!c->connected) return set_error(DSGD_ESTATE, "peers not connected");
   DSGD_TRY(check_map(c, partner_of));
   GradSel gs;
@@ -1115,6 +1162,7 @@ dsgd_status dsgd_ea_set_update_out(dsgd_ctx* c, void* const* update_out) {
 
 dsgd_status dsgd_ea_server_apply(dsgd_ctx* c, const void* update) {
   DSGD_TRY(check_ctx(c));
+  DSGD_TRY(flush_pending(c));
   if (!(c->flags & DSGD_CTX_CENTER) || c->first != 0)
     return set_error(DSGD_ESTATE, "the server center lives on the context hosting node 0");
   if (!update) return set_error(DSGD_EINVAL, "null update");
@@ -1138,6 +1186,7 @@ dsgd_status dsgd_ea_server_apply(dsgd_ctx* c, const void* update) {
 
 dsgd_status dsgd_ea_init_center(dsgd_ctx* c) {
   DSGD_TRY(check_ctx(c));
+  DSGD_TRY(flush_pending(c));
   if (!(c->flags & DSGD_CTX_CENTER)) return set_error(DSGD_ESTATE, "no center (DSGD_CTX_CENTER)");
   return dispatch(c, [&](auto z) -> dsgd_status {
     using T = decltype(z);
@@ -1257,7 +1306,9 @@ dsgd_status dsgd_run_rounds(dsgd_ctx* c, const dsgd_run_desc* run) {
     }
     if (st != DSGD_OK) return st;
   }
-  return DSGD_OK;
+  // leave the context in its logical state (the timed work of `rounds`
+  // rounds includes the last deferred apply)
+  return flush_pending(c);
 }
 
 // -------------------------------------------------------- multi-GPU wiring

@@ -48,12 +48,14 @@ def main():
         g.set_state(0, thetas[rank])
         if proto == "elastic-avg" and rank == 0:
             # the reference's pivot-form spatial mean of the initial thetas
-            c = thetas[0].copy()
-            dev = np.zeros(d)
+            # in the context's precision, exactly as spatial_mean_f32/f64 does
+            npd = np.float64 if dtype == "f64" else np.float32
+            th = thetas.astype(npd)
+            dev = np.zeros(d, dtype=npd)
             for i in range(1, world):
-                dev = dev + (thetas[i] - thetas[0])
-            c = thetas[0] + dev * (1.0 / world)
-            g.set_center(c)
+                dev = dev + (th[i] - th[0])
+            c = th[0] + dev * (npd(1) / npd(world))
+            g.set_center(c.astype(np.float64))
         dist.barrier()
         g.seed_streams(1, f"mg/{proto}")
         g.run_rounds(D.PROTOCOLS[proto], Hyperparams(**hk), 25, scope="aggregate",
