@@ -265,10 +265,11 @@ def main():
                 "step_hbm_gbs": step_bytes / (step_ms * 1e-3) / 1e9,
                 "share_of_step": (kms / ms) if ms else None}
     if world > 1:
-        nms, nn = prof.get("nccl_allreduce", (0.0, 0))
+        nms, nn = prof.get("allreduce_comm", (0.0, 0))
         t_nccl = nms / max(1, nn) * 1e-3
-        roofline["nccl_allreduce_us"] = t_nccl * 1e6
-        roofline["nccl_busbw_gbs"] = 2 * (world - 1) / world * es * d / t_nccl / 1e9 if nn else None
+        roofline["allreduce_comm_backend"] = os.environ.get("DSGD_ALLREDUCE", "p2p")
+        roofline["allreduce_comm_us"] = t_nccl * 1e6
+        roofline["allreduce_busbw_gbs"] = 2 * (world - 1) / world * es * d / t_nccl / 1e9 if nn else None
         roofline["nvlink_peak_gbs"] = 770.0
     per_kernel = {k: {"ms_total": v[0], "launches": v[1]} for k, v in prof.items() if v[1]}
 

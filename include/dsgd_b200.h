@@ -288,7 +288,7 @@ typedef enum {
   DSGD_K_ALLREDUCE = 1,  /* single-context fused all-reduce round */
   DSGD_K_AR_DELTA = 2,   /* multi-GPU all-reduce: delta kernel */
   DSGD_K_AR_APPLY = 3,   /* multi-GPU all-reduce: apply kernel */
-  DSGD_K_NCCL = 4,       /* ncclAllReduce */
+  DSGD_K_NCCL = 4,       /* all-reduce exchange: ncclAllReduce or the peer-memory reduce kernel */
   DSGD_K_EA = 5,         /* EASGD fused chain */
   DSGD_K_PUSH = 6,
   DSGD_K_OTHER = 7,

@@ -502,3 +502,33 @@ def ref_time_rounds(protocol: int, p: int, d: int, rounds: int, threaded: bool,
     if sec < 0:
         raise RuntimeError(ref().ref_last_error().decode())
     return sec
+
+
+def run_transport_allreduce(cfg: SimConfig, dtype=np.float64) -> "Nodes":
+    """run_transport's all-reduce worker loop (transport.cpp:350-360) restated
+    with the oracle primitives: per node compute_local_delta, ring_allreduce
+    mean (transport.cpp:183-248, fixed chunking and fold order), theta +=
+    avg, delta_prev = aggregate ? avg : own.  Offset-ones init only.
+    Pinned against the compiled reference by tests/test_oracle_golden.py."""
+    p, d = cfg.p, cfg.d
+    if cfg.init_kind != INIT_OFFSET_ONES:
+        raise ValueError("offset-ones init only")
+    opt = np.zeros(d) if cfg.opt is None else np.asarray(cfg.opt, dtype=np.float64)
+    c = np.sqrt(cfg.target_sq_err / (p * d))
+    n = Nodes(np.tile(opt + c, (p, 1)).astype(dtype), dtype=dtype)
+    streams = [Stream.make(cfg.seed, cfg.run_id, i, "gradient-noise") for i in range(p)]
+    for _ in range(cfg.rounds):
+        noise = None
+        if cfg.sigma is not None:
+            noise = np.array([[cfg.sigma * s.normal() for _ in range(d)] for s in streams]).astype(dtype)
+        deltas = np.zeros((p, d), dtype=dtype)
+        for i in range(p):
+            m = Nodes(n.theta[i:i + 1], n.dprev[i:i + 1], n.t[i:i + 1], dtype=dtype)
+            local_sgd_step(m, cfg.hyper, spec=cfg.spectrum, opt=opt,
+                           noise=None if noise is None else noise[i:i + 1])
+            deltas[i] = m.dprev[0]
+        avg = ring_allreduce(deltas)
+        n.theta = (n.theta + avg).astype(dtype)
+        n.dprev = deltas.copy() if cfg.per_node_scope else avg.copy()
+        n.t += 1
+    return n

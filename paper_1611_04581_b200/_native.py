@@ -23,7 +23,7 @@ CTX_QUADRATIC, CTX_GRAD, CTX_NOISE, CTX_CENTER = 1, 2, 4, 8
 BUF_THETA, BUF_DELTA, BUF_GRAD, BUF_NOISE, BUF_SPECTRUM, BUF_OPT, BUF_CENTER = range(7)
 GRAD_QUADRATIC, GRAD_BUFFER = 0, 1
 K_STEP, K_ALLREDUCE, K_AR_DELTA, K_AR_APPLY, K_NCCL, K_EA, K_PUSH, K_OTHER = range(8)
-KERNEL_NAMES = ["step", "allreduce_local", "ar_delta", "ar_apply", "nccl_allreduce",
+KERNEL_NAMES = ["step", "allreduce_local", "ar_delta", "ar_apply", "allreduce_comm",
                 "ea", "push", "other"]
 HANDLE_BYTES = 256
 NCCL_ID_BYTES = 128

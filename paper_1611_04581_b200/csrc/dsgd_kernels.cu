@@ -117,15 +117,16 @@ __device__ __forceinline__ void step_group(const StepArgs<T>& a, const NodeIO<T>
   ld(x, n.theta_in, k);
   if constexpr (MODE == kModePull || MODE == kModeStale || MODE == kModeMix || MODE == kModeAsync)
     ld(xj, n.partner, k);
-  if constexpr (MODE == kModeApply || MODE == kModeApplyDelta) ld(ax, n.aux, k);
+  if constexpr (MODE == kModeApply) ld(ax, n.aux, k);
+  if constexpr (MODE == kModeApplyDelta) ld(ax, n.partner ? n.partner : n.aux, k);  // avg_t
   if constexpr (MODE == kModeStep || MODE == kModePull || MODE == kModeStale ||
                 MODE == kModeArDelta) {
     ld(dp, n.delta, k);
   } else if constexpr (MODE == kModeApplyDelta) {
-    if (n.aux != n.delta)
-      ld(dp, n.delta, k);  // per-node scope: own delta_prev
-    else
+    if (a.agg)
       dp = ax;             // aggregate scope: delta_prev is the average itself
+    else
+      ld(dp, n.delta, k);  // per-node scope: own delta_prev
   }
   if constexpr (MODE != kModeMix && MODE != kModeApply)
     ld_grad_inputs(gb, s, o, xi, n.grad, a.spec, a.opt, n.noise, a.quad, k);
@@ -176,7 +177,7 @@ __device__ __forceinline__ void step_group(const StepArgs<T>& a, const NodeIO<T>
   } else if constexpr (MODE == kModeApplyDelta) {
     st(n.theta_out, k, out_t);
     st(n.aux, k, out_d);
-    if (n.aux != n.delta) st(n.delta, k, out_d);
+    if (!a.agg) st(n.delta, k, out_d);
   } else {
     st(n.theta_out, k, out_t);
     if constexpr (MODE == kModeStep || MODE == kModePull || MODE == kModeStale)
@@ -233,6 +234,49 @@ cudaError_t launch_step(int mode, const StepArgs<T>& a, int vec, uint32_t grid, 
       return cudaErrorInvalidValue;
   }
 #undef DSGD_STEP_CASE
+  return cudaGetLastError();
+}
+
+// ----------------------------------------- multi-GPU reduce + all-gather
+template <typename T, bool VEC>
+__device__ __forceinline__ void ar_reduce_group(const ArReduceArgs<T>& a, uint64_t k) {
+  using L = Lanes<T, VEC>;
+  constexpr int W = L::W;
+  L acc, v;
+  ld(acc, a.x[a.slice], k);
+  for (uint32_t s = 1; s < a.p; ++s) {
+    uint32_t node = a.slice + s;
+    if (node >= a.p) node -= a.p;
+    ld(v, a.x[node], k);
+#pragma unroll
+    for (int l = 0; l < W; ++l) acc.v[l] = radd(acc.v[l], v.v[l]);
+  }
+  const T pt = T(a.p);
+#pragma unroll
+  for (int l = 0; l < W; ++l) acc.v[l] = rdiv(acc.v[l], pt);
+  for (uint32_t r = 0; r < a.p; ++r) st(a.avg[r], k, acc);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_ar_reduce(const __grid_constant__ ArReduceArgs<T> a) {
+  if (!block_wait(a.wait)) return;
+  constexpr uint64_t W = Vec<T>::N;
+  // aligned vector body [vlo, vhi), scalar head/tail
+  uint64_t vlo = (a.lo + W - 1) / W * W;
+  uint64_t vhi = a.hi / W * W;
+  if (vlo > vhi) vlo = vhi = a.hi;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t v = vlo / W + tid; v < vhi / W; v += stride) ar_reduce_group<T, true>(a, v * W);
+  for (uint64_t k = a.lo + tid; k < vlo; k += stride) ar_reduce_group<T, false>(a, k);
+  for (uint64_t k = (vhi > vlo ? vhi : vlo) + tid; k < a.hi; k += stride)
+    if (k >= vlo) ar_reduce_group<T, false>(a, k);
+  block_signal(a.signal);
+}
+
+template <typename T>
+cudaError_t launch_ar_reduce(const ArReduceArgs<T>& a, uint32_t grid, cudaStream_t s) {
+  k_ar_reduce<T><<<grid, kBlock, 0, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -652,6 +696,7 @@ cudaError_t launch_fill_normal(T* out, uint64_t n, double sigma, uint64_t seed, 
   template cudaError_t launch_ea_local<T>(const EaArgs<T>&, int, int, uint32_t, cudaStream_t);     \
   template cudaError_t launch_push<T>(const PushArgs<T>&, int, uint32_t, cudaStream_t);            \
   template cudaError_t launch_ea_chain<T>(const EaChainArgs<T>&, int, uint32_t, cudaStream_t);     \
+  template cudaError_t launch_ar_reduce<T>(const ArReduceArgs<T>&, uint32_t, cudaStream_t);        \
   template cudaError_t launch_spatial_mean<T>(const T* const*, uint32_t, uint64_t, T*,             \
                                               cudaStream_t);                                       \
   template cudaError_t launch_fill_normal<T>(T*, uint64_t, double, uint64_t, uint64_t, cudaStream_t);

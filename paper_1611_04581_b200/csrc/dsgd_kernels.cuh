@@ -47,6 +47,24 @@ struct StepArgs {
   int quad;    // gradient = spec * (la - opt)
   uint32_t n_local;
   uint32_t blocks_per_node;
+  int agg;  // kModeApplyDelta: aggregate momentum scope (delta_prev = the average)
+  WaitSpec wait;
+  SignalSpec signal;
+};
+
+// Multi-GPU all-reduce over NVLink peer memory (replaces ring_allreduce,
+// transport.cpp:183-248): this rank owns reference ring chunk `slice`
+// [lo, hi); it reads every rank's exchange buffer x[k] for that range, folds
+// the sum left in ring order starting at node `slice` ("received + own",
+// transport.cpp:224-226), divides by p (229-235) and writes the average into
+// every rank's avg buffer (the all-gather, 238-246).
+template <typename T>
+struct ArReduceArgs {
+  const T* x[kMaxWait];
+  T* avg[kMaxWait];
+  uint32_t p;
+  uint32_t slice;
+  uint64_t lo, hi;
   WaitSpec wait;
   SignalSpec signal;
 };
@@ -134,6 +152,8 @@ template <typename T>
 cudaError_t launch_push(const PushArgs<T>& a, int vec, uint32_t grid, cudaStream_t s);
 template <typename T>
 cudaError_t launch_ea_chain(const EaChainArgs<T>& a, int vec, uint32_t grid, cudaStream_t s);
+template <typename T>
+cudaError_t launch_ar_reduce(const ArReduceArgs<T>& a, uint32_t grid, cudaStream_t s);
 template <typename T>
 cudaError_t launch_spatial_mean(const T* const* x, uint32_t p, uint64_t d, T* out, cudaStream_t s);
 template <typename T>

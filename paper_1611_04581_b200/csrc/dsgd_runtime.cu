@@ -88,6 +88,9 @@ struct HandleBlob {
   uint64_t off_c_in;
   uint64_t off_flags;
   uint64_t off_round;
+  uint64_t off_x;    // all-reduce exchange buffer (0: none)
+  uint64_t off_a;    // all-reduce average buffer
+  uint64_t off_ar;   // all-reduce counters: [0] exchange written, [1] average written
 };
 static_assert(sizeof(HandleBlob) <= DSGD_HANDLE_BYTES, "handle blob too large");
 
@@ -96,6 +99,9 @@ struct PeerNode {  // device-addressable view of one node (local or IPC-mapped)
   char* c_in = nullptr;
   unsigned long long* flags = nullptr;
   unsigned long long* round = nullptr;
+  char* x = nullptr;                  // all-reduce exchange buffer
+  char* avg = nullptr;                // all-reduce average buffer
+  unsigned long long* ar = nullptr;   // [0] exchange written, [1] average written (rounds)
 };
 
 struct Prof {
@@ -132,7 +138,9 @@ struct dsgd_ctx {
   char* arena = nullptr;
   size_t arena_bytes = 0;
   size_t off_theta[kMaxLocal][2] = {};
-  size_t off_c_in = 0, off_flags = 0, off_round = 0;
+  size_t off_c_in = 0, off_flags = 0, off_round = 0, off_x = 0, off_a = 0, off_ar = 0;
+  bool p2p_allreduce = true;       // multi-GPU all-reduce over NVLink peer memory (else NCCL)
+  uint64_t ar_rounds = 0;          // peer-memory all-reduce rounds run
   uint64_t n_chunks = 0;
 
   char* delta[kMaxLocal] = {};
@@ -441,11 +449,27 @@ dsgd_status do_pull(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& gs,
 }
 
 // Materialises a deferred multi-GPU all-reduce apply: theta += avg.
+// Waits of a peer-memory all-reduce kernel: every rank's counter `which`
+// (0: exchange written, 1: average written) has reached `need`.
+void ar_waits(dsgd_ctx* c, int which, unsigned long long need, dsgd::WaitSpec* w) {
+  w->n = 0;
+  w->timeout_ns = c->timeout_ns;
+  w->error = c->error;
+  for (uint32_t k = 0; k < c->p && w->n < kMaxWait; ++k) {
+    w->ptr[w->n] = c->peers[k].ar + which;
+    w->val[w->n] = need;
+    w->n++;
+  }
+}
+
 template <typename T>
 dsgd_status flush_pending_t(dsgd_ctx* c) {
   if (!c->ar_pending) return DSGD_OK;
-  char* xbuf = c->ar_pending_scope == DSGD_SCOPE_PER_NODE ? c->aux[0] : c->delta[0];
+  const bool p2p = c->p2p_allreduce;
+  char* xbuf = p2p ? c->peers[c->first].avg
+                   : (c->ar_pending_scope == DSGD_SCOPE_PER_NODE ? c->aux[0] : c->delta[0]);
   dsgd::StepArgs<T> a{};
+  if (p2p) ar_waits(c, 1, c->ar_rounds, &a.wait);  // every owner wrote its average slice
   a.node[0].theta_in = as<T>(c->theta_ptr(0, c->cur));
   a.node[0].theta_out = as<T>(c->theta_ptr(0, c->cur ^ 1));
   a.node[0].aux = as<T>(xbuf);
@@ -461,6 +485,9 @@ dsgd_status flush_pending_t(dsgd_ctx* c) {
   c->seq += 1;
   c->cur ^= 1;
   c->ar_pending = false;
+  if (p2p && c->ar_pending_scope == DSGD_SCOPE_AGGREGATE)  // delta_prev = the average
+    DSGD_CUDA(cudaMemcpyAsync(c->delta[0], xbuf, c->d * c->es, cudaMemcpyDeviceToDevice,
+                              c->stream));
   return DSGD_OK;
 }
 
@@ -468,6 +495,68 @@ dsgd_status flush_pending(dsgd_ctx* c) {
   if (!c->ar_pending) return DSGD_OK;
   DeviceGuard g(c->device);
   return c->dtype == DSGD_F32 ? flush_pending_t<float>(c) : flush_pending_t<double>(c);
+}
+
+// Multi-GPU all-reduce round over NVLink peer memory, two kernels:
+//  1. fused (previous apply +) delta kernel -> own exchange buffer x
+//     [waits: every rank's averages of the previous round are written]
+//  2. reduce + all-gather of this rank's reference ring chunk: sum of every
+//     rank's x in ring order / p -> every rank's avg buffer
+//     [waits: every rank's exchange buffer is written]
+// Bit-exact with the reference's ring_allreduce (transport.cpp:183-248).
+template <typename T>
+dsgd_status do_allreduce_p2p(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& gs,
+                             dsgd_momentum_scope scope) {
+  if (!c->peers[c->first].x) return set_error(DSGD_ESTATE, "no all-reduce buffers");
+  if (c->ar_pending && c->ar_pending_scope != scope) DSGD_TRY(flush_pending_t<T>(c));
+  const uint32_t me = c->first;
+  const bool fused = c->ar_pending;
+  const unsigned long long t = c->ar_rounds;
+  {
+    dsgd::StepArgs<T> a{};
+    fill_node<T>(c, 0, gs, h, &a.node[0]);
+    a.node[0].aux = as<T>(c->peers[me].x);
+    a.node[0].partner = fused ? as<T>(c->peers[me].avg) : nullptr;
+    fill_common(c, h, gs, &a);
+    a.agg = scope == DSGD_SCOPE_AGGREGATE;
+    a.n_local = 1;
+    const bool vec = all_aligned(c, gs);
+    const uint64_t W = vec ? 16 / sizeof(T) : 1;
+    a.blocks_per_node = blocks_for(c, (c->d / W + 1) / 2, 1);
+    ar_waits(c, 1, t, &a.wait);
+    a.signal.counter = c->peers[me].ar + 0;
+    a.signal.value = t + 1;
+    a.signal.arrive = c->arrive;
+    LaunchScope ls(c, DSGD_K_AR_DELTA);
+    DSGD_CUDA(dsgd::launch_step<T>(fused ? dsgd::kModeApplyDelta : dsgd::kModeArDelta, a, vec,
+                                   a.blocks_per_node, c->stream));
+  }
+  if (fused) c->cur ^= 1;
+  {
+    dsgd::ArReduceArgs<T> a{};
+    for (uint32_t k = 0; k < c->p; ++k) {
+      a.x[k] = as<T>(c->peers[k].x);
+      a.avg[k] = as<T>(c->peers[k].avg);
+    }
+    a.p = c->p;
+    a.slice = me;
+    const uint64_t base = c->d / c->p, rem = c->d % c->p;  // transport.cpp:193-198
+    a.lo = (uint64_t)me * base + std::min<uint64_t>(me, rem);
+    a.hi = a.lo + base + (me < rem ? 1 : 0);
+    ar_waits(c, 0, t + 1, &a.wait);
+    a.signal.counter = c->peers[me].ar + 1;
+    a.signal.value = t + 1;
+    a.signal.arrive = c->arrive;
+    const uint64_t n = a.hi - a.lo;
+    const uint32_t grid = blocks_for(c, n / (16 / sizeof(T)) + 1, 1);
+    LaunchScope ls(c, DSGD_K_NCCL);
+    DSGD_CUDA(dsgd::launch_ar_reduce<T>(a, grid, c->stream));
+  }
+  c->ar_rounds = t + 1;
+  c->ar_pending = true;
+  c->ar_pending_scope = scope;
+  c->prev_readers.clear();
+  return DSGD_OK;
 }
 
 template <typename T>
@@ -488,6 +577,7 @@ dsgd_status do_allreduce(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& 
     c->prev_readers.clear();
     return DSGD_OK;
   }
+  if (c->p2p_allreduce) return do_allreduce_p2p<T>(c, h, gs, scope);
   if (!c->comm) return set_error(DSGD_ESTATE, "multi-GPU all-reduce needs dsgd_ctx_init_nccl");
   // delta kernel -> ncclAllReduce(avg) in place on the exchange buffer.
   // Aggregate scope exchanges delta_prev itself, so the averaged delta lands
@@ -505,6 +595,7 @@ dsgd_status do_allreduce(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& 
     fill_node<T>(c, 0, gs, h, &a.node[0]);
     a.node[0].aux = as<T>(xbuf);
     fill_common(c, h, gs, &a);
+    a.agg = scope == DSGD_SCOPE_AGGREGATE;
     a.n_local = 1;
     const bool vec = all_aligned(c, gs);
     const uint64_t W = vec ? 16 / sizeof(T) : 1;
@@ -730,7 +821,16 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
   if (c->flags & DSGD_CTX_CENTER) off += align_up(c->n_chunks * 8);
   c->off_round = off;
   off += align_up(8 * c->n_local);
+  if (c->n_local < c->p) {  // one node per context: peer-memory all-reduce buffers
+    c->off_x = off;
+    off += vb;
+    c->off_a = off;
+    off += vb;
+    c->off_ar = off;
+    off += 256;
+  }
   c->arena_bytes = off;
+  if (const char* e = std::getenv("DSGD_ALLREDUCE")) c->p2p_allreduce = std::string(e) != "nccl";
   DSGD_CUDA(cudaMalloc(&c->arena, c->arena_bytes));
   DSGD_CUDA(cudaMemset(c->arena, 0, c->arena_bytes));
   for (uint32_t i = 0; i < c->n_local; ++i) {
@@ -763,6 +863,11 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
     pn.theta[0] = c->theta_ptr(i, 0);
     pn.theta[1] = c->theta_ptr(i, 1);
     pn.round = c->round_ptr(i);
+    if (c->off_x) {
+      pn.x = c->arena + c->off_x;
+      pn.avg = c->arena + c->off_a;
+      pn.ar = reinterpret_cast<unsigned long long*>(c->arena + c->off_ar);
+    }
     if (i == 0 && (c->flags & DSGD_CTX_CENTER)) {
       pn.c_in = c->arena + c->off_c_in;
       pn.flags = reinterpret_cast<unsigned long long*>(c->arena + c->off_flags);
@@ -1332,6 +1437,9 @@ dsgd_status dsgd_ctx_export_handle(dsgd_ctx* c, void* blob) {
   b.off_c_in = c->off_c_in;
   b.off_flags = c->off_flags;
   b.off_round = c->off_round;
+  b.off_x = c->off_x;
+  b.off_a = c->off_a;
+  b.off_ar = c->off_ar;
   std::memset(blob, 0, DSGD_HANDLE_BYTES);
   std::memcpy(blob, &b, sizeof(b));
   return DSGD_OK;
@@ -1376,6 +1484,11 @@ dsgd_status dsgd_ctx_connect_peers(dsgd_ctx* c, const void* blobs) {
     pn.theta[0] = m + b.off_theta[0];
     pn.theta[1] = m + b.off_theta[1];
     pn.round = reinterpret_cast<unsigned long long*>(m + b.off_round);
+    if (b.off_x) {
+      pn.x = m + b.off_x;
+      pn.avg = m + b.off_a;
+      pn.ar = reinterpret_cast<unsigned long long*>(m + b.off_ar);
+    }
     if (b.flags & DSGD_CTX_CENTER) {
       pn.c_in = m + b.off_c_in;
       pn.flags = reinterpret_cast<unsigned long long*>(m + b.off_flags);

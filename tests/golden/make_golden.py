@@ -42,6 +42,17 @@ RUN_CASES = {
 }
 
 
+def transport_case(p: int) -> "O.SimConfig":
+    """The multi-GPU all-reduce case of tests/mgpu_worker.py, for the
+    reference's threaded transport (run_transport, ring_allreduce)."""
+    d = 1031
+    hk = dict(alpha0=0.05, anneal_at=(20,), mu=0.9, weight_decay=1e-4, beta_gossip=0.4,
+              beta_ea=0.15, tau=1)
+    return O.SimConfig(protocol=O.ALLREDUCE, p=p, hyper=O.HyperParams(**hk), sigma=0.05,
+                       spectrum=list(np.linspace(0.5, 2.0, d)), init_kind=O.INIT_OFFSET_ONES,
+                       rounds=25, per_node_scope=False, run_id="mg/all-reduce")
+
+
 def main():
     if not O.ref_available():
         raise SystemExit("oracle/_ref not built: needs /root/reference")
@@ -60,6 +71,11 @@ def main():
         ring[f"in_{p}_{d}"] = x
         ring[f"out_{p}_{d}"] = O.ref_ring_allreduce(x, chaos_seed=1)
     np.savez(os.path.join(HERE, "ring.npz"), **ring)
+    tr = {}
+    for p in (2, 4, 8):
+        th, dp, t, _ = O.ref_run(transport_case(p), transport=True, chaos_seed=p)
+        tr.update({f"p{p}_theta": th, f"p{p}_dprev": dp, f"p{p}_t": t})
+    np.savez(os.path.join(HERE, "transport.npz"), **tr)
     print("wrote", sorted(os.listdir(HERE)))
 
 

@@ -26,6 +26,8 @@ def main():
     results = {}
     names = {"all-reduce": O.ALLREDUCE, "elastic-avg": O.ELASTIC, "pull-gossip": O.PULL,
              "push-gossip": O.PUSH, "gossip-stale": O.STALE, "gossip-fresh": O.FRESH}
+    if len(sys.argv) > 2 and sys.argv[2] == "allreduce-only":
+        names = {"all-reduce": O.ALLREDUCE}
     for proto, oid in names.items():
         d = 1031
         hk = dict(alpha0=0.05, anneal_at=(20,), mu=0.9, weight_decay=1e-4, beta_gossip=0.4,
@@ -67,7 +69,20 @@ def main():
         dist.all_gather_object(allst, (th, dp, t))
         if rank == 0:
             npd = np.float64 if dtype == "f64" else np.float32
-            oth, odp, ot, oc = O.run(cfg, dtype=npd)
+            if proto == "all-reduce":
+                # multi-GPU all-reduce = the reference's threaded transport
+                # (ring_allreduce order), not the simulator's pivot mean
+                on = O.run_transport_allreduce(cfg, dtype=npd)
+                oth, odp, ot, oc = on.theta, on.dprev, on.t, None
+                if dtype == "f64":
+                    from tests.golden.make_golden import transport_case
+                    gp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                                      "transport.npz")
+                    if world in (2, 4, 8) and os.path.exists(gp):
+                        gold = np.load(gp)[f"p{world}_theta"]
+                        assert np.array_equal(oth, gold)
+            else:
+                oth, odp, ot, oc = O.run(cfg, dtype=npd)
             dev_th = np.array([s[0] for s in allst]).astype(npd)
             exact = dev_th.tobytes() == oth.tobytes()
             rel = float(np.abs(dev_th.astype(float) - oth.astype(float)).max() /

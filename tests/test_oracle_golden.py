@@ -397,3 +397,14 @@ def test_ref_transport_allreduce_matches_ring_restatement():
         n.dprev = avg.copy()
         n.t += 1
     assert n.theta.tobytes() == th_ref.tobytes()
+
+
+def test_golden_transport_allreduce_restatement():
+    """The restated run_transport all-reduce loop equals the compiled
+    reference's threaded transport (fixture) bit for bit, p = 2, 4, 8."""
+    from tests.golden.make_golden import transport_case
+    g = _golden("transport.npz")
+    for p in (2, 4, 8):
+        n = O.run_transport_allreduce(transport_case(p))
+        assert n.theta.tobytes() == g[f"p{p}_theta"].tobytes()
+        assert n.dprev.tobytes() == g[f"p{p}_dprev"].tobytes()
