@@ -246,31 +246,45 @@ def main():
     value = world * d / (step_ms * 1e-3)
 
     # dominant kernel + roofline (algorithmic bytes per launch)
-    if world == 1:
-        kname, bpp = "allreduce_local", 20   # read theta, delta, g; write theta', delta'
-        kdesc = "k_allreduce_local (p=1): fused delta + mean + apply, 12 B read + 8 B write per param"
-    else:
-        kname, bpp = "ar_delta", 16          # read theta, delta, g; write delta'
-        kdesc = "k_step<ArDelta>: 12 B read + 4 B write per param (then NCCL avg, k_step<Apply> 12 B)"
-    kms, kn = prof.get(kname, (0.0, 0))
+    backend = os.environ.get("DSGD_ALLREDUCE", "p2p")
     peak, peak_src = peaks()
+    nv_peak = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+    nv_bytes = 2 * (world - 1) / world * es * d  # per direction per GPU (ring-equivalent)
+    if world == 1:
+        kname, bpp = "allreduce_local", 5 * es  # read theta, delta, g; write theta', delta'
+        kdesc = "k_allreduce_local (p=1): fused delta + mean + apply, 12 B read + 8 B write per param"
+    elif backend == "p2p":
+        kname, bpp = "allreduce_comm", 7 * es
+        kdesc = ("k_ar_fused: one persistent kernel per round; HBM 28 B/param (theta, avg, g read; "
+                 "theta', x write; avg slices written by every owner; x served to peers), NVLink "
+                 f"{nv_bytes / d:.1f} B/param each direction")
+    else:
+        kname, bpp = "ar_delta", 5 * es
+        kdesc = "k_step<ApplyDelta>: read theta, avg, g; write theta', delta' (then the exchange)"
+    kms, kn = prof.get(kname, (0.0, 0))
     kavg_ms = kms / max(1, kn)
     achieved = (bpp * d / (kavg_ms * 1e-3) / 1e9) if kn else None
-    step_bytes = 20 * d if world == 1 else 28 * d
-    roofline = {"bound": "hbm", "kernel": kdesc, "achieved": achieved, "peak": peak,
+    t_hbm = bpp * d / (peak * 1e9)
+    t_nv = nv_bytes / (nv_peak * 1e9) if (world > 1 and kname == "allreduce_comm") else 0.0
+    bound = "nvlink" if t_nv > t_hbm else "hbm"
+    roofline = {"bound": bound, "kernel": kdesc, "achieved": achieved, "peak": peak,
                 "peak_source": peak_src, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": None,
                 "algorithmic_bytes_per_launch": bpp * d,
                 "kernel_avg_us": kavg_ms * 1e3,
-                "step_hbm_gbs": step_bytes / (step_ms * 1e-3) / 1e9,
+                "roofline_time_us": max(t_hbm, t_nv) * 1e6,
+                "frac_of_roofline_time": (max(t_hbm, t_nv) / (kavg_ms * 1e-3)) if kn else None,
                 "share_of_step": (kms / ms) if ms else None}
+    step_bytes = 5 * es * d if world == 1 else 7 * es * d
     if world > 1:
         nms, nn = prof.get("allreduce_comm", (0.0, 0))
-        t_nccl = nms / max(1, nn) * 1e-3
-        roofline["allreduce_comm_backend"] = os.environ.get("DSGD_ALLREDUCE", "p2p")
-        roofline["allreduce_comm_us"] = t_nccl * 1e6
-        roofline["allreduce_busbw_gbs"] = 2 * (world - 1) / world * es * d / t_nccl / 1e9 if nn else None
-        roofline["nvlink_peak_gbs"] = 770.0
+        t_c = nms / max(1, nn) * 1e-3
+        roofline["allreduce_backend"] = backend
+        roofline["allreduce_comm_us"] = t_c * 1e6
+        roofline["nvlink_bytes_per_direction"] = nv_bytes
+        roofline["nvlink_achieved_gbs"] = nv_bytes / t_c / 1e9 if nn else None
+        roofline["nvlink_peak_gbs"] = nv_peak
+        roofline["nvlink_frac"] = (nv_bytes / t_c / 1e9 / nv_peak) if nn else None
     per_kernel = {k: {"ms_total": v[0], "launches": v[1]} for k, v in prof.items() if v[1]}
 
     # ---------------- end-to-end through the C ABI (host gradients, pinned)
@@ -336,6 +350,7 @@ def main():
                            "grad_source": f"pool of {POOL} synthetic N(0,1) device buffers/worker",
                            "l2": "inputs larger than L2 (~400 MB/step/worker working set)"},
                 "gbs": step_bytes / (step_ms * 1e-3) / 1e9,
+                "gbs_note": "aggregation-step algorithmic HBM GB/s per GPU",
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": (k1 - k0) + (n1 - n0),
                 "gpu_launches_detail": {"kernels": k1 - k0, "nccl_calls": n1 - n0},

@@ -280,6 +280,174 @@ cudaError_t launch_ar_reduce(const ArReduceArgs<T>& a, uint32_t grid, cudaStream
   return cudaGetLastError();
 }
 
+// ------------------------------------ one-kernel multi-GPU all-reduce round
+__device__ __forceinline__ uint32_t ring_chunk_of(uint64_t k, uint64_t base, uint64_t rem) {
+  const uint64_t big = rem * (base + 1);  // chunks 0..rem-1 have base+1 elements
+  if (k < big) return (uint32_t)(k / (base + 1));
+  return (uint32_t)(rem + (k - big) / base);
+}
+
+// A-role work on [lo, hi) of one segment (lo, hi multiples of W when VEC).
+template <typename T, bool VEC>
+__device__ __forceinline__ void arf_a_group(const ArFusedArgs<T>& a, uint64_t k, bool norm,
+                                            double& nacc) {
+  using L = Lanes<T, VEC>;
+  constexpr int W = L::W;
+  const NodeIO<T>& n = a.node;
+  L x, ax, dp, gb, s, o, xi, ot, od;
+  ld(x, n.theta_in, k);
+  if (a.pending) {
+    ld(ax, n.partner, k);
+    if (a.agg)
+      dp = ax;
+    else
+      ld(dp, n.delta, k);
+  } else {
+    ld(dp, n.delta, k);
+  }
+  ld_grad_inputs(gb, s, o, xi, n.grad, a.spec, a.opt, n.noise, a.quad, k);
+#pragma unroll
+  for (int l = 0; l < W; ++l) {
+    const T x1 = a.pending ? radd(x.v[l], ax.v[l]) : x.v[l];
+    ot.v[l] = x1;
+    od.v[l] = sgd_delta(x1, dp.v[l], gb.v[l], s.v[l], o.v[l], xi.v[l], n.alpha, a.mu, a.wd,
+                        a.mu_nz, a.wd_pos, a.quad, norm, nacc);
+  }
+  if (a.pending) st(n.theta_out, k, ot);
+  st(n.aux, k, od);
+  if (!a.agg || !a.pending) st(n.delta, k, od);
+}
+
+// B-role: reference ring fold for each lane (start node = the element's
+// ring chunk), divide by p, write the average to every rank.
+template <typename T, bool VEC, int P>
+__device__ __forceinline__ void arf_b_group(const ArFusedArgs<T>& a, uint64_t k) {
+  using L = Lanes<T, VEC>;
+  constexpr int W = L::W;
+  L v[P];
+#pragma unroll
+  for (int r = 0; r < P; ++r) ld(v[r], a.x[r], k);  // P - 1 NVLink loads in flight
+  L acc;
+  const T pt = T(P);
+#pragma unroll
+  for (int l = 0; l < W; ++l) {
+    const uint32_t c = ring_chunk_of(k + l, a.ring_base, a.ring_rem);
+    T sum = T(0);
+#pragma unroll
+    for (int r = 0; r < P; ++r) {
+      const uint32_t node = c + r >= (uint32_t)P ? c + r - P : c + r;
+      T val = v[0].v[l];  // select v[node] without dynamic register indexing
+#pragma unroll
+      for (int q = 1; q < P; ++q)
+        if (q == (int)node) val = v[q].v[l];
+      sum = r == 0 ? val : radd(sum, val);  // ((x_c + x_c+1) + x_c+2) ...
+    }
+    acc.v[l] = rdiv(sum, pt);
+  }
+#pragma unroll
+  for (int r = 0; r < P; ++r) st(a.avg[r], k, acc);
+}
+
+__device__ __forceinline__ void arf_publish(unsigned int* cnt, unsigned int total,
+                                            unsigned long long* flag, unsigned long long val) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(cnt, 1u);
+    if (prev == total - 1) {
+      atomicExch(cnt, 0u);
+      __threadfence_system();
+      st_release_sys(flag, val);
+    }
+  }
+}
+
+template <typename T, bool VEC, int P>
+__global__ void __launch_bounds__(kBlock, 4) k_ar_fused(const __grid_constant__ ArFusedArgs<T> a) {
+  __shared__ int ok;
+  constexpr uint64_t W = Lanes<T, VEC>::W;
+  const bool is_a = blockIdx.x < a.grid_a;
+  const uint32_t role_b = is_a ? blockIdx.x : blockIdx.x - a.grid_a;
+  const uint32_t role_n = is_a ? a.grid_a : gridDim.x - a.grid_a;
+  const uint64_t tid = (uint64_t)role_b * blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)role_n * blockDim.x;
+  const bool norm = a.node.norm != nullptr;
+  double nacc = 0.0;
+  for (uint32_t sg = 0; sg < a.n_seg; ++sg) {
+    const uint64_t lo = (uint64_t)sg * a.seg_len;
+    const uint64_t hi = lo + a.seg_len < a.d ? lo + a.seg_len : a.d;
+    if (is_a) {
+      // RAW on avg / WAR on x of this segment: every rank averaged round t-1
+      if (threadIdx.x == 0) {
+        int good = 1;
+        for (uint32_t r = 0; r < a.p && good; ++r)
+          good = wait_flag(&a.flags[r]->b_done[sg], a.t, a.timeout_ns, a.error);
+        ok = good;
+      }
+      __syncthreads();
+      if (!ok) return;
+      const uint64_t nv = (hi - lo) / W;
+      for (uint64_t v = tid; v < nv; v += stride) arf_a_group<T, VEC>(a, lo + v * W, norm, nacc);
+      for (uint64_t k = lo + nv * W + tid; k < hi; k += stride)
+        arf_a_group<T, false>(a, k, norm, nacc);
+      arf_publish(&a.arrive->a_cnt[sg], role_n, &a.flags[a.rank]->a_done[sg], a.t + 1);
+    } else {
+      if (threadIdx.x == 0) {
+        int good = 1;
+        for (uint32_t r = 0; r < a.p && good; ++r)
+          good = wait_flag(&a.flags[r]->a_done[sg], a.t + 1, a.timeout_ns, a.error);
+        ok = good;
+      }
+      __syncthreads();
+      if (!ok) return;
+      // this rank's share of the segment
+      const uint64_t n = hi - lo;
+      const uint64_t per = (n / a.p + W - 1) / W * W;
+      const uint64_t mlo = lo + per * a.rank < hi ? lo + per * a.rank : hi;
+      const uint64_t mhi = mlo + per < hi ? mlo + per : hi;
+      const uint64_t nv = (mhi - mlo) / W;
+      for (uint64_t v = tid; v < nv; v += stride) arf_b_group<T, VEC, P>(a, mlo + v * W);
+      for (uint64_t k = mlo + nv * W + tid; k < mhi; k += stride) arf_b_group<T, false, P>(a, k);
+      arf_publish(&a.arrive->b_cnt[sg], role_n, &a.flags[a.rank]->b_done[sg], a.t + 1);
+    }
+  }
+  if (!is_a) arf_publish(&a.arrive->b_all_cnt, role_n, &a.flags[a.rank]->b_all, a.t + 1);
+  if (is_a) block_add_double(nacc, a.node.norm);
+}
+
+template <typename T, int P>
+cudaError_t launch_ar_fused_p(const ArFusedArgs<T>& a, int vec, uint32_t grid, cudaStream_t s) {
+  if (vec)
+    k_ar_fused<T, true, P><<<grid, kBlock, 0, s>>>(a);
+  else
+    k_ar_fused<T, false, P><<<grid, kBlock, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_ar_fused(const ArFusedArgs<T>& a, int vec, uint32_t grid, cudaStream_t s) {
+  switch (a.p) {
+    case 2: return launch_ar_fused_p<T, 2>(a, vec, grid, s);
+    case 3: return launch_ar_fused_p<T, 3>(a, vec, grid, s);
+    case 4: return launch_ar_fused_p<T, 4>(a, vec, grid, s);
+    case 5: return launch_ar_fused_p<T, 5>(a, vec, grid, s);
+    case 6: return launch_ar_fused_p<T, 6>(a, vec, grid, s);
+    case 7: return launch_ar_fused_p<T, 7>(a, vec, grid, s);
+    case 8: return launch_ar_fused_p<T, 8>(a, vec, grid, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <typename T>
+int ar_fused_blocks_per_sm(int vec) {
+  int n = 0;  // the P = 8 instantiation bounds the register budget of all P
+  if (vec)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_ar_fused<T, true, 8>, kBlock, 0);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_ar_fused<T, false, 8>, kBlock, 0);
+  return n;
+}
+
 // ------------------------------------------- single-context all-reduce round
 // allreduce_round protocols.cpp:110-131 for p nodes on one GPU, one pass:
 // every node's delta, the pivot-form mean of param_vec.cpp:26-38
@@ -541,7 +709,8 @@ __global__ void __launch_bounds__(kBlock) k_ea_chain(const __grid_constant__ EaC
     if (threadIdx.x == 0) ok = wait_flag(&a.flag_in[c], a.need, a.timeout_ns, a.error) ? 1 : 0;
     __syncthreads();
     if (!ok) return;
-    const uint64_t base = c * kEaChunk + (uint64_t)threadIdx.x * 4;
+    for (uint64_t part = 0; part < a.chunk; part += kEaChunk) {
+    const uint64_t base = c * a.chunk + part + (uint64_t)threadIdx.x * 4;
     constexpr int W = Lanes<T, VEC>::W;
     for (int sub = 0; sub < 4; sub += W) {
       const uint64_t k = base + sub;
@@ -584,11 +753,11 @@ __global__ void __launch_bounds__(kBlock) k_ea_chain(const __grid_constant__ EaC
       st(n.delta, k, od);
       st(a.c_out, k, cv);
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence_system();
-      st_release_sys(&a.flag_out[c], a.seq);
     }
+    // the barrier orders every thread's center stores before thread 0's
+    // release (cumulative at system scope): no separate fence.sc
+    __syncthreads();
+    if (threadIdx.x == 0) st_release_sys(&a.flag_out[c], a.seq);
   }
   block_add_double(nacc, n.norm);
 }
@@ -697,6 +866,8 @@ cudaError_t launch_fill_normal(T* out, uint64_t n, double sigma, uint64_t seed, 
   template cudaError_t launch_push<T>(const PushArgs<T>&, int, uint32_t, cudaStream_t);            \
   template cudaError_t launch_ea_chain<T>(const EaChainArgs<T>&, int, uint32_t, cudaStream_t);     \
   template cudaError_t launch_ar_reduce<T>(const ArReduceArgs<T>&, uint32_t, cudaStream_t);        \
+  template cudaError_t launch_ar_fused<T>(const ArFusedArgs<T>&, int, uint32_t, cudaStream_t);     \
+  template int ar_fused_blocks_per_sm<T>(int);                                                     \
   template cudaError_t launch_spatial_mean<T>(const T* const*, uint32_t, uint64_t, T*,             \
                                               cudaStream_t);                                       \
   template cudaError_t launch_fill_normal<T>(T*, uint64_t, double, uint64_t, uint64_t, cudaStream_t);

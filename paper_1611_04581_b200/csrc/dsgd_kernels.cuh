@@ -69,6 +69,53 @@ struct ArReduceArgs {
   SignalSpec signal;
 };
 
+// One-kernel multi-GPU all-reduce round (p <= kMaxFusedRanks): the grid is
+// persistent (every CTA resident) and split into two roles working through
+// S segments of the vector in a pipeline:
+//   A-role CTAs: (theta += avg of the previous round) + compute_local_delta
+//     -> own exchange buffer x, segment by segment (HBM-bound); the last A
+//     CTA of a segment publishes a_done[s] = t + 1;
+//   B-role CTAs: once every rank published a_done[s], reduce this rank's
+//     share of segment s in the reference ring order and write the average
+//     into every rank's avg buffer (NVLink-bound); publish b_done[s].
+// A-role work of round t+1 on segment s waits for every rank's b_done[s].
+constexpr int kMaxFusedRanks = 8;
+constexpr int kMaxSegments = 64;
+
+struct ArFlags {  // per rank, in the IPC arena
+  unsigned long long a_done[kMaxSegments];
+  unsigned long long b_done[kMaxSegments];
+  unsigned long long b_all;   // rounds whose every segment is averaged (flush waits on it)
+  unsigned long long pad[15];
+};
+struct ArArrive {  // per rank, private
+  unsigned int a_cnt[kMaxSegments];
+  unsigned int b_cnt[kMaxSegments];
+  unsigned int b_all_cnt;
+};
+
+template <typename T>
+struct ArFusedArgs {
+  NodeIO<T> node;                     // aux = own x; partner = own avg (when pending)
+  const T* x[kMaxFusedRanks];
+  T* avg[kMaxFusedRanks];
+  ArFlags* flags[kMaxFusedRanks];
+  ArArrive* arrive;
+  const T* spec;
+  const T* opt;
+  uint64_t d;
+  uint64_t seg_len;                   // multiple of 4
+  uint32_t n_seg;
+  uint32_t p, rank;
+  uint32_t grid_a;                    // CTAs [0, grid_a) are A-role
+  uint64_t ring_base, ring_rem;       // reference ring chunking (transport.cpp:193-198)
+  unsigned long long t;               // round index (flags count rounds)
+  T mu, wd;
+  int mu_nz, wd_pos, quad, agg, pending;
+  unsigned long long timeout_ns;
+  unsigned int* error;
+};
+
 // Single-context all-reduce round (p nodes on one GPU), fused:
 // deltas -> pivot-form spatial mean -> apply.
 template <typename T>
@@ -134,6 +181,7 @@ struct EaChainArgs {
   unsigned long long seq;                // value published to flag_out[c]
   uint64_t d;
   uint64_t n_chunks;
+  uint64_t chunk;  // elements per flag (multiple of kEaChunk)
   T mu, wd, beta;
   int mu_nz, wd_pos, quad;
   unsigned long long timeout_ns;
@@ -154,6 +202,10 @@ template <typename T>
 cudaError_t launch_ea_chain(const EaChainArgs<T>& a, int vec, uint32_t grid, cudaStream_t s);
 template <typename T>
 cudaError_t launch_ar_reduce(const ArReduceArgs<T>& a, uint32_t grid, cudaStream_t s);
+template <typename T>
+cudaError_t launch_ar_fused(const ArFusedArgs<T>& a, int vec, uint32_t grid, cudaStream_t s);
+template <typename T>
+int ar_fused_blocks_per_sm(int vec);
 template <typename T>
 cudaError_t launch_spatial_mean(const T* const* x, uint32_t p, uint64_t d, T* out, cudaStream_t s);
 template <typename T>

@@ -91,6 +91,7 @@ struct HandleBlob {
   uint64_t off_x;    // all-reduce exchange buffer (0: none)
   uint64_t off_a;    // all-reduce average buffer
   uint64_t off_ar;   // all-reduce counters: [0] exchange written, [1] average written
+  uint64_t off_arf;  // one-kernel all-reduce segment flags (dsgd::ArFlags)
 };
 static_assert(sizeof(HandleBlob) <= DSGD_HANDLE_BYTES, "handle blob too large");
 
@@ -102,6 +103,7 @@ struct PeerNode {  // device-addressable view of one node (local or IPC-mapped)
   char* x = nullptr;                  // all-reduce exchange buffer
   char* avg = nullptr;                // all-reduce average buffer
   unsigned long long* ar = nullptr;   // [0] exchange written, [1] average written (rounds)
+  dsgd::ArFlags* arf = nullptr;       // one-kernel all-reduce segment flags
 };
 
 struct Prof {
@@ -140,8 +142,14 @@ struct dsgd_ctx {
   size_t off_theta[kMaxLocal][2] = {};
   size_t off_c_in = 0, off_flags = 0, off_round = 0, off_x = 0, off_a = 0, off_ar = 0;
   bool p2p_allreduce = true;       // multi-GPU all-reduce over NVLink peer memory (else NCCL)
+  bool ar_fused = true;            // ... as one persistent kernel per round (p <= 8)
+  size_t off_arf = 0;
+  dsgd::ArArrive* ar_arrive = nullptr;
+  uint32_t ar_segments = 16;
+  double ar_a_frac = 0.5;
   uint64_t ar_rounds = 0;          // peer-memory all-reduce rounds run
   uint64_t n_chunks = 0;
+  uint64_t ea_chunk = 4 * dsgd::kEaChunk;  // elements per EASGD chain flag (DSGD_EA_CHUNK)
 
   char* delta[kMaxLocal] = {};
   char* grad[kMaxLocal] = {};
@@ -470,6 +478,8 @@ dsgd_status flush_pending_t(dsgd_ctx* c) {
                    : (c->ar_pending_scope == DSGD_SCOPE_PER_NODE ? c->aux[0] : c->delta[0]);
   dsgd::StepArgs<T> a{};
   if (p2p) ar_waits(c, 1, c->ar_rounds, &a.wait);  // every owner wrote its average slice
+  if (p2p && c->ar_fused && c->p <= (uint32_t)dsgd::kMaxFusedRanks)
+    for (int k = 0; k < a.wait.n; ++k) a.wait.ptr[k] = &c->peers[k].arf->b_all;
   a.node[0].theta_in = as<T>(c->theta_ptr(0, c->cur));
   a.node[0].theta_out = as<T>(c->theta_ptr(0, c->cur ^ 1));
   a.node[0].aux = as<T>(xbuf);
@@ -512,6 +522,52 @@ dsgd_status do_allreduce_p2p(dsgd_ctx* c, const dsgd_hyperparams* h, const GradS
   const uint32_t me = c->first;
   const bool fused = c->ar_pending;
   const unsigned long long t = c->ar_rounds;
+  if (c->ar_fused && c->p <= (uint32_t)dsgd::kMaxFusedRanks) {
+    dsgd::ArFusedArgs<T> a{};
+    fill_node<T>(c, 0, gs, h, &a.node);
+    a.node.aux = as<T>(c->peers[me].x);
+    a.node.partner = fused ? as<T>(c->peers[me].avg) : nullptr;
+    if (fused) a.node.theta_out = as<T>(c->theta_ptr(0, c->cur ^ 1));
+    for (uint32_t k = 0; k < c->p; ++k) {
+      a.x[k] = as<T>(c->peers[k].x);
+      a.avg[k] = as<T>(c->peers[k].avg);
+      a.flags[k] = c->peers[k].arf;
+    }
+    a.arrive = c->ar_arrive;
+    a.spec = gs.quad ? as<T>(c->spec) : nullptr;
+    a.opt = gs.quad ? as<T>(c->opt) : nullptr;
+    a.d = c->d;
+    a.n_seg = std::max<uint32_t>(1, std::min<uint64_t>(c->ar_segments, (c->d + 1023) / 1024));
+    a.seg_len = ((c->d + a.n_seg - 1) / a.n_seg + 3) / 4 * 4;
+    a.n_seg = (uint32_t)((c->d + a.seg_len - 1) / a.seg_len);
+    a.p = c->p;
+    a.rank = me;
+    a.ring_base = c->d / c->p;
+    a.ring_rem = c->d % c->p;
+    a.t = t;
+    a.mu = (T)h->mu;
+    a.wd = (T)h->weight_decay;
+    a.mu_nz = h->mu != 0.0;
+    a.wd_pos = h->weight_decay > 0.0;
+    a.quad = gs.quad;
+    a.agg = scope == DSGD_SCOPE_AGGREGATE;
+    a.pending = fused;
+    a.timeout_ns = c->timeout_ns;
+    a.error = c->error;
+    const bool vec = all_aligned(c, gs);
+    // persistent: every CTA must be resident (B-role CTAs spin on A-role flags)
+    const int occ = std::max(1, std::min(4, dsgd::ar_fused_blocks_per_sm<T>(vec)));
+    const uint32_t grid = (uint32_t)c->sm_count * occ;
+    a.grid_a = std::max<uint32_t>(1, std::min<uint32_t>(grid - 1, (uint32_t)(grid * c->ar_a_frac)));
+    LaunchScope ls(c, DSGD_K_NCCL);
+    DSGD_CUDA(dsgd::launch_ar_fused<T>(a, vec, grid, c->stream));
+    if (fused) c->cur ^= 1;
+    c->ar_rounds = t + 1;
+    c->ar_pending = true;
+    c->ar_pending_scope = scope;
+    c->prev_readers.clear();
+    return DSGD_OK;
+  }
   {
     dsgd::StepArgs<T> a{};
     fill_node<T>(c, 0, gs, h, &a.node[0]);
@@ -655,7 +711,8 @@ dsgd_status do_ea(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& gs, int
   a.need = r == 0 ? c->ea_seq - 1 : c->ea_seq;
   a.seq = c->ea_seq;
   a.d = c->d;
-  a.n_chunks = c->n_chunks;
+  a.chunk = c->ea_chunk;
+  a.n_chunks = (c->d + a.chunk - 1) / a.chunk;
   a.mu = (T)h->mu;
   a.wd = (T)h->weight_decay;
   a.beta = (T)h->beta_ea;
@@ -668,7 +725,7 @@ dsgd_status do_ea(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& gs, int
   // one CTA per chunk: a CTA blocked on its flag or in its release fence
   // leaves the SM to the other resident chunks (dispatch is in chunk order,
   // the order the previous rank produces them)
-  const uint32_t grid = (uint32_t)std::min<uint64_t>(c->n_chunks, 0x7fffffffu);
+  const uint32_t grid = (uint32_t)std::min<uint64_t>(a.n_chunks, 0x7fffffffu);
   LaunchScope ls(c, DSGD_K_EA);
   DSGD_CUDA(dsgd::launch_ea_chain<T>(a, vec, grid, c->stream));
   c->prev_readers.clear();
@@ -801,6 +858,8 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
   DSGD_CUDA(cudaSetDevice(c->device));
   DSGD_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device));
   if (const char* e = std::getenv("DSGD_BLOCKS_PER_SM")) c->blocks_per_sm = std::max(1, atoi(e));
+  if (const char* e = std::getenv("DSGD_EA_CHUNK"))
+    c->ea_chunk = std::max<uint64_t>(1, strtoull(e, nullptr, 10) / dsgd::kEaChunk) * dsgd::kEaChunk;
   if (desc->stream) {
     c->stream = static_cast<cudaStream_t>(desc->stream);
   } else {
@@ -828,9 +887,17 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
     off += vb;
     c->off_ar = off;
     off += 256;
+    c->off_arf = off;
+    off += align_up(sizeof(dsgd::ArFlags));
   }
   c->arena_bytes = off;
-  if (const char* e = std::getenv("DSGD_ALLREDUCE")) c->p2p_allreduce = std::string(e) != "nccl";
+  if (const char* e = std::getenv("DSGD_ALLREDUCE")) {
+    c->p2p_allreduce = std::string(e) != "nccl";
+    c->ar_fused = std::string(e) != "p2p2k";  // p2p2k: the two-kernel variant
+  }
+  if (const char* e = std::getenv("DSGD_AR_SEGMENTS"))
+    c->ar_segments = (uint32_t)std::min(dsgd::kMaxSegments, std::max(1, atoi(e)));
+  if (const char* e = std::getenv("DSGD_AR_A_FRAC")) c->ar_a_frac = std::min(0.95, std::max(0.05, atof(e)));
   DSGD_CUDA(cudaMalloc(&c->arena, c->arena_bytes));
   DSGD_CUDA(cudaMemset(c->arena, 0, c->arena_bytes));
   for (uint32_t i = 0; i < c->n_local; ++i) {
@@ -855,6 +922,10 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
   DSGD_CUDA(cudaMallocHost(&c->norm_host, sizeof(double) * kMaxLocal));
   DSGD_CUDA(cudaMalloc(&c->arrive, 256));
   DSGD_CUDA(cudaMemset(c->arrive, 0, 256));
+  if (c->n_local < c->p) {
+    DSGD_CUDA(cudaMalloc(&c->ar_arrive, sizeof(dsgd::ArArrive)));
+    DSGD_CUDA(cudaMemset(c->ar_arrive, 0, sizeof(dsgd::ArArrive)));
+  }
   c->error = c->arrive + 32;
   // local nodes are addressable peers of themselves
   c->peers.resize(c->p);
@@ -867,6 +938,7 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
       pn.x = c->arena + c->off_x;
       pn.avg = c->arena + c->off_a;
       pn.ar = reinterpret_cast<unsigned long long*>(c->arena + c->off_ar);
+      pn.arf = reinterpret_cast<dsgd::ArFlags*>(c->arena + c->off_arf);
     }
     if (i == 0 && (c->flags & DSGD_CTX_CENTER)) {
       pn.c_in = c->arena + c->off_c_in;
@@ -895,6 +967,7 @@ void dsgd_ctx_destroy(dsgd_ctx* c) {
   cudaFree(c->norm);
   cudaFreeHost(c->norm_host);
   cudaFree(c->arrive);
+  cudaFree(c->ar_arrive);
   cudaFreeHost(c->staging);
   cudaFree(c->arena);
   for (auto* s : c->partner_streams) dsgd_stream_destroy(s);
@@ -1440,6 +1513,7 @@ dsgd_status dsgd_ctx_export_handle(dsgd_ctx* c, void* blob) {
   b.off_x = c->off_x;
   b.off_a = c->off_a;
   b.off_ar = c->off_ar;
+  b.off_arf = c->off_arf;
   std::memset(blob, 0, DSGD_HANDLE_BYTES);
   std::memcpy(blob, &b, sizeof(b));
   return DSGD_OK;
@@ -1488,6 +1562,7 @@ dsgd_status dsgd_ctx_connect_peers(dsgd_ctx* c, const void* blobs) {
       pn.x = m + b.off_x;
       pn.avg = m + b.off_a;
       pn.ar = reinterpret_cast<unsigned long long*>(m + b.off_ar);
+      pn.arf = reinterpret_cast<dsgd::ArFlags*>(m + b.off_arf);
     }
     if (b.flags & DSGD_CTX_CENTER) {
       pn.c_in = m + b.off_c_in;
