@@ -199,8 +199,12 @@ typedef enum { DSGD_GRAD_QUADRATIC = 0, DSGD_GRAD_BUFFER = 1 } dsgd_grad_source;
 typedef struct {
   dsgd_grad_source source;
   const void* const* grad; /* GRAD_BUFFER: n_local device pointers, or NULL for DSGD_BUF_GRAD */
-  uint32_t use_noise;      /* 1: add DSGD_BUF_NOISE (NoiseModel gaussian); 0: add +0.0 (zero kind) */
+  uint32_t use_noise;      /* 0: add +0.0 (NoiseModel::zero); 1: add DSGD_BUF_NOISE (e.g. the
+                              reference noise stream drawn on the host); 2: N(0, noise_sigma^2)
+                              drawn inside the kernel (Philox keyed by noise_seed, node, t) */
   double* grad_norm_out;   /* optional: raised to max_i ||g_i|| like protocols.cpp:34-36 (syncs) */
+  double noise_sigma;      /* use_noise == 2 */
+  uint64_t noise_seed;     /* use_noise == 2 */
 } dsgd_grad_spec;
 
 /* ----------------------------------------------------------- update rules
@@ -249,6 +253,19 @@ dsgd_status dsgd_ea_set_update_out(dsgd_ctx* ctx, void* const* update_out);
 dsgd_status dsgd_ea_server_apply(dsgd_ctx* ctx, const void* update);
 /* EASGD center = spatial_mean of the nodes' current theta (simulator.cpp:62-67) */
 dsgd_status dsgd_ea_init_center(dsgd_ctx* ctx);
+/* One client tick of asynchronous EASGD (run_async simulator.cpp:419-428):
+ * node i (global id, single context) runs ea_client_step against the center
+ * and the server applies its update (gated), or a plain local step. */
+dsgd_status dsgd_ea_client_event(dsgd_ctx* ctx, const dsgd_hyperparams* h,
+                                 const dsgd_grad_spec* g, uint32_t i, int gated);
+/* make_trace_record simulator.cpp:92-123 over all p nodes: consensus error
+ * sum_i ||theta_i - mean||^2, mean objective value (quadratic contexts) and
+ * sum_i ||theta_i - theta*||^2, fp64 accumulation.  A non-finite parameter
+ * returns DSGD_ESTATE ("non-finite parameter", the reference's
+ * runtime_error).  One context per GPU: reads every peer's current theta over
+ * NVLink; call after a host barrier so every peer finished the round. */
+dsgd_status dsgd_trace(dsgd_ctx* ctx, double* sq_err_consensus, double* loss_mean,
+                       double* sq_err_opt);
 
 /* ------------------------------------------------------ per-step worker loop
  * run_sync simulator.cpp:234-369 / the run_transport worker

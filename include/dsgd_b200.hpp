@@ -94,12 +94,15 @@ class Stream {
 struct Gradient {
   dsgd_grad_source source = DSGD_GRAD_QUADRATIC;
   std::vector<const void*> buffers;  // empty: the context's own DSGD_BUF_GRAD
-  bool noise = false;
+  bool noise = false;                // add DSGD_BUF_NOISE
   double* grad_norm_out = nullptr;
+  double device_noise_sigma = 0.0;   // > 0: N(0, sigma^2) drawn inside the kernel
+  std::uint64_t device_noise_seed = 0;
 
   dsgd_grad_spec c() const {
-    return dsgd_grad_spec{source, buffers.empty() ? nullptr : buffers.data(), noise ? 1u : 0u,
-                          grad_norm_out};
+    const uint32_t mode = noise ? 1u : (device_noise_sigma > 0.0 ? 2u : 0u);
+    return dsgd_grad_spec{source, buffers.empty() ? nullptr : buffers.data(), mode,
+                          grad_norm_out, device_noise_sigma, device_noise_seed};
   }
 };
 

@@ -58,7 +58,8 @@ class CtxDesc(C.Structure):
 
 class GradSpec(C.Structure):
     _fields_ = [("source", C.c_int), ("grad", C.POINTER(C.c_void_p)),
-                ("use_noise", C.c_uint32), ("grad_norm_out", C.POINTER(C.c_double))]
+                ("use_noise", C.c_uint32), ("grad_norm_out", C.POINTER(C.c_double)),
+                ("noise_sigma", C.c_double), ("noise_seed", C.c_uint64)]
 
 
 class RunDesc(C.Structure):
@@ -121,6 +122,9 @@ _SIGS = {
     "dsgd_gossip_fresh_mix": (C.c_int, [_P, _U32P, C.c_double]),
     "dsgd_ea_set_update_out": (C.c_int, [_P, C.POINTER(_P)]),
     "dsgd_ea_server_apply": (C.c_int, [_P, _P]),
+    "dsgd_ea_client_event": (C.c_int, [_P, C.POINTER(Hyper), C.POINTER(GradSpec), C.c_uint32,
+                                       C.c_int]),
+    "dsgd_trace": (C.c_int, [_P, _DP, _DP, _DP]),
     "dsgd_ctx_seed_streams": (C.c_int, [_P, C.c_uint64, C.c_char_p]),
     "dsgd_run_rounds": (C.c_int, [_P, C.POINTER(RunDesc)]),
     "dsgd_ctx_round": (C.c_int, [_P, _U64P]),

@@ -34,6 +34,46 @@ __device__ __forceinline__ T mix(T own, T other, T beta) {
   return radd(own, rmul(beta, rsub(other, own)));
 }
 
+// ---------------------------------------------- synthetic gradient source
+// Philox4x32-10 counter-based generator + Box-Muller: N(0, sigma^2) synthetic
+// gradients / noise on the device (bench inputs; not bit-compatible with the
+// host mt19937_64 streams, which the parity path uses instead).
+__device__ __forceinline__ uint4 philox(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// Device-side gradient noise (F1): N(0, sigma^2) per coordinate from
+// Philox(counter = (k / 4, t), key = (seed, node)), Box-Muller on pairs.
+// Deterministic in (seed, node, t, k) whatever the vector width; not the
+// host mt19937_64 stream (the parity path draws those on the host).
+template <int W>
+__device__ __forceinline__ void dev_normals(uint64_t key, uint64_t ctr, uint64_t k, float (&z)[W]) {
+  const uint64_t q = k >> 2;
+  const uint4 r = philox(make_uint4((uint32_t)q, (uint32_t)(q >> 32), (uint32_t)ctr,
+                                    (uint32_t)(ctr >> 32)),
+                         make_uint2((uint32_t)key, (uint32_t)(key >> 32)));
+  const uint32_t lane0 = (uint32_t)(k & 3);
+#pragma unroll
+  for (int l = 0; l < W; ++l) {
+    const uint32_t lane = lane0 + l;
+    const uint32_t ua = lane < 2 ? r.x : r.z, ub = lane < 2 ? r.y : r.w;
+    const float u1 = ((ua >> 8) + 0.5f) * (1.0f / 16777216.0f);
+    const float u2 = ((ub >> 8) + 0.5f) * (1.0f / 16777216.0f);
+    const float rad = sqrtf(-2.0f * __logf(u1));
+    float sn, cs;
+    __sincosf(6.2831853071795864f * u2, &sn, &cs);
+    z[l] = (lane & 1) ? rad * sn : rad * cs;
+  }
+}
+
 // ------------------------------------------------------------------ loads
 template <typename T, bool VEC>
 struct Lanes {
@@ -92,19 +132,34 @@ __device__ __forceinline__ void zero(Lanes<T, VEC>& r) {
 template <typename T, bool VEC>
 __device__ __forceinline__ void ld_grad_inputs(Lanes<T, VEC>& gb, Lanes<T, VEC>& s,
                                                Lanes<T, VEC>& o, Lanes<T, VEC>& xi,
-                                               const T* grad, const T* spec, const T* opt,
-                                               const T* noise, int quad, uint64_t k) {
+                                               const NodeIO<T>& n, const T* spec, const T* opt,
+                                               int quad, uint64_t k) {
   if (quad) {
     ld_ro(s, spec, k);
     ld_ro(o, opt, k);
   } else {
-    ld_stream(gb, grad, k);
+    ld_stream(gb, n.grad, k);
   }
-  if (noise != nullptr) {
-    ld_stream(xi, noise, k);
+  if (n.noise != nullptr) {
+    ld_stream(xi, n.noise, k);
+  } else if (n.nsigma != T(0)) {
+    constexpr int W = Lanes<T, VEC>::W;
+    float z[W];
+    dev_normals<W>(n.nkey, n.nctr, n.nbase + k, z);
+#pragma unroll
+    for (int l = 0; l < W; ++l) xi.v[l] = rmul(n.nsigma, (T)z[l]);
   } else {
     zero(xi);
   }
+}
+
+template <typename T>
+__device__ __forceinline__ T noise_at(const NodeIO<T>& n, uint64_t k) {
+  if (n.noise) return n.noise[k];
+  if (n.nsigma == T(0)) return T(0);
+  float z[1];
+  dev_normals<1>(n.nkey, n.nctr, n.nbase + k, z);
+  return rmul(n.nsigma, (T)z[0]);
 }
 
 // ------------------------------------------------- fused gossip-family step
@@ -129,7 +184,7 @@ __device__ __forceinline__ void step_group(const StepArgs<T>& a, const NodeIO<T>
       ld(dp, n.delta, k);  // per-node scope: own delta_prev
   }
   if constexpr (MODE != kModeMix && MODE != kModeApply)
-    ld_grad_inputs(gb, s, o, xi, n.grad, a.spec, a.opt, n.noise, a.quad, k);
+    ld_grad_inputs(gb, s, o, xi, n, a.spec, a.opt, a.quad, k);
 #pragma unroll
   for (int l = 0; l < W; ++l) {
     if constexpr (MODE == kModeStep) {
@@ -305,7 +360,7 @@ __device__ __forceinline__ void arf_a_group(const ArFusedArgs<T>& a, uint64_t k,
   } else {
     ld(dp, n.delta, k);
   }
-  ld_grad_inputs(gb, s, o, xi, n.grad, a.spec, a.opt, n.noise, a.quad, k);
+  ld_grad_inputs(gb, s, o, xi, n, a.spec, a.opt, a.quad, k);
 #pragma unroll
   for (int l = 0; l < W; ++l) {
     const T x1 = a.pending ? radd(x.v[l], ax.v[l]) : x.v[l];
@@ -471,7 +526,7 @@ __global__ void __launch_bounds__(kBlock) k_allreduce_local(const __grid_constan
       L x, dp, gb, s, o, xi, di;
       ld(x, n.theta_in, k);
       ld(dp, n.delta, k);
-      ld_grad_inputs(gb, s, o, xi, n.grad, a.spec, a.opt, n.noise, a.quad, k);
+      ld_grad_inputs(gb, s, o, xi, n, a.spec, a.opt, a.quad, k);
       double dummy = 0.0;
 #pragma unroll
       for (int l = 0; l < W; ++l) {
@@ -519,6 +574,7 @@ cudaError_t launch_allreduce_local(const AllreduceArgs<T>& a, int vec, int norm,
         n.delta += head;
         if (n.grad) n.grad += head;
         if (n.noise) n.noise += head;
+        n.nbase += head;
       }
       if (t.spec) t.spec += head;
       if (t.opt) t.opt += head;
@@ -560,7 +616,7 @@ __global__ void __launch_bounds__(kBlock) k_ea_local(const __grid_constant__ EaA
       L x, dp, gb, s, o, xi, ot, od, uo;
       ld(x, n.theta_in, k);
       ld(dp, n.delta, k);
-      ld_grad_inputs(gb, s, o, xi, n.grad, a.spec, a.opt, n.noise, a.quad, k);
+      ld_grad_inputs(gb, s, o, xi, n, a.spec, a.opt, a.quad, k);
       double dummy = 0.0;
 #pragma unroll
       for (int l = 0; l < W; ++l) {
@@ -605,6 +661,7 @@ cudaError_t launch_ea_local(const EaArgs<T>& a, int vec, int norm, uint32_t grid
         if (n.grad) n.grad += head;
         if (n.noise) n.noise += head;
         if (n.aux) n.aux += head;
+        n.nbase += head;
       }
       if (t.spec) t.spec += head;
       if (t.opt) t.opt += head;
@@ -652,7 +709,7 @@ __device__ __forceinline__ void push_group(const PushArgs<T>& a, uint32_t node, 
   }
   L dp, gb, s, o, xi, ot, od;
   ld(dp, n.delta, k);
-  ld_grad_inputs(gb, s, o, xi, n.grad, a.spec, a.opt, n.noise, a.quad, k);
+  ld_grad_inputs(gb, s, o, xi, n, a.spec, a.opt, a.quad, k);
 #pragma unroll
   for (int l = 0; l < W; ++l) {
     const T dl = sgd_delta(m.v[l], dp.v[l], gb.v[l], s.v[l], o.v[l], xi.v[l], n.alpha, a.mu, a.wd,
@@ -723,7 +780,7 @@ __global__ void __launch_bounds__(kBlock) k_ea_chain(const __grid_constant__ EaC
             xv = rsub(xv, u);
             const T gb = a.quad ? T(0) : n.grad[kk];
             const T sv = a.quad ? a.spec[kk] : T(0), ov = a.quad ? a.opt[kk] : T(0);
-            const T xiv = n.noise ? n.noise[kk] : T(0);
+            const T xiv = noise_at(n, kk);
             const T dl = sgd_delta(xv, n.delta[kk], gb, sv, ov, xiv, n.alpha, a.mu, a.wd, a.mu_nz,
                                    a.wd_pos, a.quad, norm, nacc);
             n.delta[kk] = dl;
@@ -738,7 +795,7 @@ __global__ void __launch_bounds__(kBlock) k_ea_chain(const __grid_constant__ EaC
       ld(cv, a.c_in, k);
       ld(x, n.theta_in, k);
       ld(dp, n.delta, k);
-      ld_grad_inputs(gb, s, o, xi, n.grad, a.spec, a.opt, n.noise, a.quad, k);
+      ld_grad_inputs(gb, s, o, xi, n, a.spec, a.opt, a.quad, k);
 #pragma unroll
       for (int l = 0; l < W; ++l) {
         const T u = rmul(a.beta, rsub(x.v[l], cv.v[l]));
@@ -768,6 +825,44 @@ cudaError_t launch_ea_chain(const EaChainArgs<T>& a, int vec, uint32_t grid, cud
     k_ea_chain<T, true><<<grid, kBlock, 0, s>>>(a);
   else
     k_ea_chain<T, false><<<grid, kBlock, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ trace metrics
+// make_trace_record simulator.cpp:92-123 over p node vectors (local or NVLink
+// peer pointers): pivot-form mean (param_vec.cpp:26-38), consensus error,
+// objective value and optimum error, accumulated in fp64.
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_trace(const __grid_constant__ TraceArgs<T> a) {
+  double cons = 0.0, loss = 0.0, err = 0.0, bad = 0.0;
+  const double inv_p = 1.0 / (double)a.p;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < a.d;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const double x0 = (double)a.x[0][k];
+    double dev = 0.0;
+    for (uint32_t i = 1; i < a.p; ++i) dev += (double)a.x[i][k] - x0;
+    const double mean = x0 + dev * inv_p;
+    const double o = a.opt ? (double)a.opt[k] : 0.0;
+    const double sp = a.spec ? (double)a.spec[k] : 0.0;
+    for (uint32_t i = 0; i < a.p; ++i) {
+      const double xi = (double)a.x[i][k];
+      if (!isfinite(xi)) bad += 1.0;
+      const double c = xi - mean;
+      cons += c * c;
+      const double b = xi - o;
+      err += b * b;
+      loss += sp * b * b;
+    }
+  }
+  block_add_double(cons, a.out + 0);
+  block_add_double(loss, a.out + 1);
+  block_add_double(err, a.out + 2);
+  block_add_double(bad, a.out + 3);
+}
+
+template <typename T>
+cudaError_t launch_trace(const TraceArgs<T>& a, uint32_t grid, cudaStream_t s) {
+  k_trace<T><<<grid, kBlock, 0, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -805,22 +900,6 @@ cudaError_t launch_spatial_mean(const T* const* x, uint32_t p, uint64_t d, T* ou
   const uint64_t blocks = (d + kBlock - 1) / kBlock;
   k_spatial_mean<T><<<(unsigned)(blocks < 4096 ? (blocks ? blocks : 1) : 4096), kBlock, 0, s>>>(a);
   return cudaGetLastError();
-}
-
-// ---------------------------------------------- synthetic gradient source
-// Philox4x32-10 counter-based generator + Box-Muller: N(0, sigma^2) synthetic
-// gradients / noise on the device (bench inputs; not bit-compatible with the
-// host mt19937_64 streams, which the parity path uses instead).
-__device__ __forceinline__ uint4 philox(uint4 c, uint2 k) {
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
-    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
-    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
-    k.x += 0x9E3779B9u;
-    k.y += 0xBB67AE85u;
-  }
-  return c;
 }
 
 template <typename T>
@@ -868,6 +947,7 @@ cudaError_t launch_fill_normal(T* out, uint64_t n, double sigma, uint64_t seed, 
   template cudaError_t launch_ar_reduce<T>(const ArReduceArgs<T>&, uint32_t, cudaStream_t);        \
   template cudaError_t launch_ar_fused<T>(const ArFusedArgs<T>&, int, uint32_t, cudaStream_t);     \
   template int ar_fused_blocks_per_sm<T>(int);                                                     \
+  template cudaError_t launch_trace<T>(const TraceArgs<T>&, uint32_t, cudaStream_t);               \
   template cudaError_t launch_spatial_mean<T>(const T* const*, uint32_t, uint64_t, T*,             \
                                               cudaStream_t);                                       \
   template cudaError_t launch_fill_normal<T>(T*, uint64_t, double, uint64_t, uint64_t, cudaStream_t);

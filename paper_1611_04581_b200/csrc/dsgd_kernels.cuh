@@ -21,6 +21,21 @@ struct NodeIO {
   T* aux;              // all-reduce exchange buffer
   double* norm;        // sum of g^2 accumulator (grad_norm_out), or null
   T alpha;             // step_size_at(h, t_i)
+  T nsigma;            // device Philox noise sigma (used when noise == null), 0: none
+  uint64_t nkey;       // device noise key (seed, node)
+  uint64_t nctr;       // device noise counter (the node's t)
+  uint64_t nbase;      // element offset of this launch's k = 0 (tail launches)
+};
+
+// Trace metrics over all p nodes (make_trace_record simulator.cpp:92-123).
+template <typename T>
+struct TraceArgs {
+  const T* x[kMaxLocal];
+  const T* spec;  // null: no loss / optimum error
+  const T* opt;
+  uint32_t p;
+  uint64_t d;
+  double* out;    // [0] sq_err_consensus, [1] sum_i 2 f(theta_i), [2] sq_err_opt, [3] non-finite count
 };
 
 // Kernel modes of the fused gossip-family kernel k_step.
@@ -206,6 +221,8 @@ template <typename T>
 cudaError_t launch_ar_fused(const ArFusedArgs<T>& a, int vec, uint32_t grid, cudaStream_t s);
 template <typename T>
 int ar_fused_blocks_per_sm(int vec);
+template <typename T>
+cudaError_t launch_trace(const TraceArgs<T>& a, uint32_t grid, cudaStream_t s);
 template <typename T>
 cudaError_t launch_spatial_mean(const T* const* x, uint32_t p, uint64_t d, T* out, cudaStream_t s);
 template <typename T>

@@ -276,6 +276,9 @@ struct GradSel {
   const void* grad[kMaxLocal] = {};
   bool noise = false;
   bool norm = false;
+  bool dev_noise = false;  // Philox noise inside the kernel
+  double sigma = 0.0;
+  uint64_t seed = 0;
 };
 
 dsgd_status resolve_grad(dsgd_ctx* c, const dsgd_grad_spec* g, GradSel* out) {
@@ -292,9 +295,16 @@ dsgd_status resolve_grad(dsgd_ctx* c, const dsgd_grad_spec* g, GradSel* out) {
   } else {
     return set_error(DSGD_EINVAL, "unknown gradient source");
   }
-  if (g->use_noise) {
+  if (g->use_noise == 1) {
     if (!c->noise[0]) return set_error(DSGD_ESTATE, "no noise buffers (DSGD_CTX_NOISE)");
     s.noise = true;
+  } else if (g->use_noise == 2) {
+    if (!(g->noise_sigma >= 0.0)) return set_error(DSGD_EINVAL, "noise sigma must be >= 0");
+    s.dev_noise = g->noise_sigma > 0.0;
+    s.sigma = g->noise_sigma;
+    s.seed = g->noise_seed;
+  } else if (g->use_noise != 0) {
+    return set_error(DSGD_EINVAL, "use_noise must be 0, 1 or 2");
   }
   s.norm = g->grad_norm_out != nullptr;
   *out = s;
@@ -314,6 +324,10 @@ void fill_node(dsgd_ctx* c, uint32_t i, const GradSel& gs, const dsgd_hyperparam
   n->norm = gs.norm ? c->norm + i : nullptr;
   const double alpha = h ? dsgd_step_size_at(h, c->t[i]) : 0.0;
   n->alpha = (T)(negate_alpha ? -alpha : alpha);
+  n->nsigma = gs.dev_noise ? (T)gs.sigma : T(0);
+  n->nkey = gs.seed * 0x9E3779B97F4A7C15ull ^ (uint64_t(c->first + i) + 1) * 0xD1B54A32D192ED03ull;
+  n->nctr = c->t[i];
+  n->nbase = 0;
 }
 
 template <typename A>
@@ -1358,6 +1372,80 @@ dsgd_status dsgd_ea_server_apply(dsgd_ctx* c, const void* update) {
     a.blocks_per_node = blocks_for(c, (c->d / W + 1) / 2, 1);
     LaunchScope ls(c, DSGD_K_OTHER);
     DSGD_CUDA(dsgd::launch_step<T>(dsgd::kModeApply, a, vec, a.blocks_per_node, c->stream));
+    return DSGD_OK;
+  });
+}
+
+dsgd_status dsgd_ea_client_event(dsgd_ctx* c, const dsgd_hyperparams* h,
+                                 const dsgd_grad_spec* g, uint32_t i, int gated) {
+  DSGD_TRY(check_ctx(c));
+  DSGD_TRY(flush_pending(c));
+  if (!h) return set_error(DSGD_EINVAL, "null hyperparams");
+  if (c->distributed()) return set_error(DSGD_EINVAL, "async EASGD runs on a single context");
+  if (i >= c->p) return set_error(DSGD_EINVAL, "client index out of range");
+  if (!(c->flags & DSGD_CTX_CENTER)) return set_error(DSGD_ESTATE, "no center (DSGD_CTX_CENTER)");
+  GradSel gs;
+  DSGD_TRY(resolve_grad(c, g, &gs));
+  return dispatch(c, [&](auto z) -> dsgd_status {
+    using T = decltype(z);
+    DSGD_TRY(norm_begin(c, gs));
+    dsgd::EaArgs<T> a{};
+    fill_node<T>(c, i, gs, h, &a.node[0]);
+    a.node[0].theta_out = as<T>(c->theta_ptr(i, c->cur));  // in place: only node i moves
+    if (!gs.quad) a.node[0].grad = static_cast<const T*>(gs.grad[i]);
+    a.node[0].noise = gs.noise ? as<T>(c->noise[i]) : nullptr;
+    a.node[0].norm = gs.norm ? c->norm : nullptr;
+    fill_common(c, h, gs, &a);
+    a.center = as<T>(c->arena + c->off_c_in);
+    a.beta = (T)h->beta_ea;
+    a.gated = gated;
+    a.p = 1;
+    const bool vec = gs.quad || aligned16(gs.grad[i]);
+    const uint64_t W = vec ? 16 / sizeof(T) : 1;
+    {
+      LaunchScope ls(c, DSGD_K_EA);
+      DSGD_CUDA(dsgd::launch_ea_local<T>(a, vec, gs.norm, blocks_for(c, c->d / W, 1), c->stream));
+    }
+    c->t[i] += 1;
+    if (gs.norm) {
+      DSGD_CUDA(cudaMemcpyAsync(c->norm_host, c->norm, sizeof(double), cudaMemcpyDeviceToHost,
+                                c->stream));
+      DSGD_CUDA(cudaStreamSynchronize(c->stream));
+      *g->grad_norm_out = std::max(*g->grad_norm_out, std::sqrt(c->norm_host[0]));
+    }
+    return DSGD_OK;
+  });
+}
+
+dsgd_status dsgd_trace(dsgd_ctx* c, double* sq_err_consensus, double* loss_mean,
+                       double* sq_err_opt) {
+  DSGD_TRY(check_ctx(c));
+  DSGD_TRY(flush_pending(c));
+  if (!c->connected) return set_error(DSGD_ESTATE, "peers not connected");
+  if (c->p > (uint32_t)kMaxLocal) return set_error(DSGD_EINVAL, "trace supports p <= 32");
+  return dispatch(c, [&](auto z) -> dsgd_status {
+    using T = decltype(z);
+    dsgd::TraceArgs<T> a{};
+    for (uint32_t k = 0; k < c->p; ++k) a.x[k] = as<T>(c->peers[k].theta[c->cur]);
+    a.spec = c->spec ? as<T>(c->spec) : nullptr;
+    a.opt = c->spec ? as<T>(c->opt) : nullptr;
+    a.p = c->p;
+    a.d = c->d;
+    a.out = c->norm;  // 4 doubles of scratch
+    DSGD_CUDA(cudaMemsetAsync(c->norm, 0, 4 * sizeof(double), c->stream));
+    {
+      LaunchScope ls(c, DSGD_K_OTHER);
+      DSGD_CUDA(dsgd::launch_trace<T>(a, blocks_for(c, c->d, 1), c->stream));
+    }
+    DSGD_CUDA(cudaMemcpyAsync(c->norm_host, c->norm, 4 * sizeof(double), cudaMemcpyDeviceToHost,
+                              c->stream));
+    DSGD_CUDA(cudaStreamSynchronize(c->stream));
+    if (c->norm_host[3] != 0.0)
+      return set_error(DSGD_ESTATE, "non-finite parameter encountered at t=" +
+                                        std::to_string(c->t[0]));
+    if (sq_err_consensus) *sq_err_consensus = c->norm_host[0];
+    if (loss_mean) *loss_mean = c->spec ? 0.5 * c->norm_host[1] / c->p : 0.0;
+    if (sq_err_opt) *sq_err_opt = c->spec ? c->norm_host[2] : 0.0;
     return DSGD_OK;
   });
 }

@@ -124,6 +124,46 @@ def run_sync(cfg: SimConfig, obj: QuadraticObjective, dtype: str = "f64",
         g.close()
 
 
+def run_async_elastic(cfg: SimConfig, obj: QuadraticObjective, dtype: str = "f64",
+                      device: int = 0) -> RunResult:
+    """run_async for elastic-avg under the Poisson clock (simulator.cpp:
+    380-449): master clock (gap, then node); the ticking client runs
+    ea_client_step + ea_server_apply when gated on its own t, else a local
+    step -- one fused event kernel per tick."""
+    if cfg.events == 0:
+        raise InvalidArgument("events must be >= 1")
+    d = obj.dim()
+    thetas = make_initial_nodes(cfg, obj)
+    use_noise = cfg.noise is not None and cfg.noise.kind != "zero"
+    g = Group(d, cfg.p, dtype=dtype, quadratic=True, noise=use_noise, center=True,
+              device=device)
+    try:
+        g.set_quadratic(obj.spectrum, obj.opt)
+        for i in range(cfg.p):
+            g.set_state(i, thetas[i])
+        g.ea_init_center()
+        clock = Stream.make(cfg.seed, cfg.run_id, 0xFFFFFFFF, "clock")
+        noise = [Stream.make(cfg.seed, cfg.run_id, i, "gradient-noise") for i in range(cfg.p)]
+        t = [0] * cfg.p
+        tau = cfg.hyper.tau
+        for _ in range(cfg.events):
+            clock.exponential(cfg.p * cfg.rate_per_node)
+            i = clock.uniform_index(cfg.p)
+            if use_noise:
+                g.set_vector(i, N.BUF_NOISE, noise[i].fill_normal(cfg.noise.sigma, d))
+            gated = t[i] > 0 and t[i] % tau == 0
+            g.ea_client_event(cfg.hyper, i, gated, grad="quadratic", noise=use_noise)
+            t[i] += 1
+        th = np.zeros((cfg.p, d))
+        dp = np.zeros((cfg.p, d))
+        tt = np.zeros(cfg.p, dtype=np.uint64)
+        for i in range(cfg.p):
+            th[i], dp[i], tt[i] = g.get_state(i)
+        return RunResult(th, dp, tt, g.get_center())
+    finally:
+        g.close()
+
+
 def run_async_pull(cfg: SimConfig, obj: QuadraticObjective, dtype: str = "f64",
                    device: int = 0) -> RunResult:
     """run_async for async-pull (simulator.cpp:380-449): master Poisson clock

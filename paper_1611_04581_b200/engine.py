@@ -244,9 +244,11 @@ class Group:
         N.check(self.lib.dsgd_download_async(self._ctx, local, which, host_ptr, count))
 
     # -------------------------------------------------------- update rules
-    def _grad(self, grad, noise: bool, grad_norm: bool):
+    def _grad(self, grad, noise, grad_norm: bool):
         """grad: None -> quadratic objective if present else the context's
-        gradient buffers; 'quadratic'; or a list of device pointers."""
+        gradient buffers; 'quadratic'; or a list of device pointers.
+        noise: False (zero noise), True (the context's noise buffers) or
+        ('device', sigma, seed) for Philox noise drawn inside the kernel."""
         keep = None
         if grad is None:
             src = N.GRAD_QUADRATIC if self.flags & N.CTX_QUADRATIC else N.GRAD_BUFFER
@@ -256,8 +258,13 @@ class Group:
         else:
             keep = (C.c_void_p * len(grad))(*grad)
             src, ptr = N.GRAD_BUFFER, C.cast(keep, C.POINTER(C.c_void_p))
-        gs = N.GradSpec(src, ptr, 1 if noise else 0,
-                        C.pointer(self._norm) if grad_norm else None)
+        mode, sigma, seed = 0, 0.0, 0
+        if isinstance(noise, tuple):
+            mode, sigma, seed = 2, float(noise[1]), int(noise[2])
+        elif noise:
+            mode = 1
+        gs = N.GradSpec(src, ptr, mode, C.pointer(self._norm) if grad_norm else None,
+                        sigma, seed)
         gs._keep = keep
         return gs
 
@@ -320,6 +327,17 @@ class Group:
 
     def ea_init_center(self) -> None:
         N.check(self.lib.dsgd_ea_init_center(self._ctx))
+
+    def ea_client_event(self, h: Hyperparams, i: int, gated: bool, **kw):
+        """One asynchronous EASGD client tick (run_async simulator.cpp:419-428)."""
+        hc = h.to_c()
+        return self._run(self.lib.dsgd_ea_client_event, C.byref(hc), i, int(gated), **kw)
+
+    def trace(self) -> dict:
+        """make_trace_record (simulator.cpp:92-123) on the device."""
+        a, b, c = C.c_double(), C.c_double(), C.c_double()
+        N.check(self.lib.dsgd_trace(self._ctx, C.byref(a), C.byref(b), C.byref(c)))
+        return {"sq_err_consensus": a.value, "loss_mean": b.value, "sq_err_opt": c.value}
 
     def ea_set_update_out(self, ptrs) -> None:
         if ptrs is None:

@@ -409,3 +409,71 @@ def test_fp32_teacher_forced_within_1e5_of_fp64():
         worst = max(worst, err)
     assert worst <= 1e-5, worst
     g.close()
+
+
+# ---------------------------------------------------------- SURVEY §8(f)
+def test_async_elastic_fp64_matches_golden_reference():
+    """F4: asynchronous EASGD under the Poisson clock (run_async
+    simulator.cpp:380-449), one fused client-event kernel per tick,
+    bit-exact with the compiled reference (golden ea8_poisson)."""
+    from tests.golden.make_golden import RUN_CASES
+    cfg = RUN_CASES["ea8_poisson"]
+    g = np.load("tests/golden/runs.npz")
+    obj = P.QuadraticObjective(cfg.spectrum, cfg.opt)
+    r = D.run_async_elastic(to_driver(cfg), obj, dtype="f64")
+    assert same(r.theta, g["ea8_poisson_theta"])
+    assert same(r.delta_prev, g["ea8_poisson_dprev"])
+    assert r.t.tolist() == g["ea8_poisson_t"].tolist()
+    assert same(r.center, g["ea8_poisson_center"])
+    r32 = D.run_async_elastic(to_driver(cfg), obj, dtype="f32")
+    th, dp, t, c = O.run(cfg, dtype=np.float32)
+    assert same(r32.theta.astype(np.float32), th) and same(r32.center.astype(np.float32), c)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_trace_metrics_match_oracle(dtype):
+    """F3: make_trace_record on the device (fp64 accumulation; the summation
+    order differs from the reference's, so relative 1e-12)."""
+    p, d = 5, 3001
+    c = make_case(p, d, dtype, seed=21)
+    g = load_group(c, dtype)
+    tr = g.trace()
+    ref = O.trace(c["theta"], c["spec"], c["opt"])
+    for k in ("sq_err_consensus", "loss_mean", "sq_err_opt"):
+        assert tr[k] == pytest.approx(ref[k], rel=1e-12), k
+    th = c["theta"].astype(np.float64).copy()
+    th[2, 17] = np.nan
+    g.set_state(2, th[2])
+    with pytest.raises(N.DsgdError, match="non-finite"):
+        g.trace()
+    g.close()
+
+
+def _device_noise(d, sigma, seed, t, grad_ptrs=None):
+    """Extract the in-kernel noise: alpha = 1, mu = wd = 0, zero gradient
+    -> delta' = -xi."""
+    g = Group(d, 1, dtype="f32", grad=True)
+    g.set_state(0, np.zeros(d), np.zeros(d), t)
+    h = Hyperparams(alpha0=1.0, anneal_at=(), mu=0.0, weight_decay=0.0)
+    g.local_sgd_step(h, grad=grad_ptrs or "buffer", noise=("device", sigma, seed))
+    xi = -g.get_state(0)[1]
+    g.close()
+    return xi
+
+
+def test_device_noise_statistics_and_determinism():
+    """F1: Philox noise inside the fused kernel: N(0, sigma^2), a function of
+    (seed, node, t, k) only -- identical on the vector and scalar paths."""
+    import torch
+    d, sigma = 1_000_003, 0.3
+    a = _device_noise(d, sigma, 7, 5)
+    b = _device_noise(d, sigma, 7, 5)
+    assert same(a, b)
+    assert abs(a.mean()) < 5 * sigma / np.sqrt(d)
+    assert a.std() == pytest.approx(sigma, rel=5e-3)
+    c = _device_noise(d, sigma, 7, 6)
+    assert abs(np.corrcoef(a, c)[0, 1]) < 0.01
+    z = torch.zeros(d + 8, device="cuda")  # misaligned zero gradient -> scalar path
+    torch.cuda.synchronize()
+    s = _device_noise(d, sigma, 7, 5, grad_ptrs=[z.data_ptr() + 4])
+    assert same(s, a)
