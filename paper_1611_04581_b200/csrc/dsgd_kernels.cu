@@ -503,6 +503,104 @@ int ar_fused_blocks_per_sm(int vec) {
   return n;
 }
 
+// ------------------------------------------------ one-shot all-reduce round
+// The ring-order average of lane l of every rank's previous exchange value.
+template <typename T, bool VEC, int P>
+__device__ __forceinline__ void ring_average(const Lanes<T, VEC> (&v)[P], uint64_t k,
+                                             uint64_t base, uint64_t rem, Lanes<T, VEC>& avg) {
+  constexpr int W = Lanes<T, VEC>::W;
+#pragma unroll
+  for (int l = 0; l < W; ++l) {
+    const uint32_t c = ring_chunk_of(k + l, base, rem);
+    T sum = T(0);
+#pragma unroll
+    for (int r = 0; r < P; ++r) {
+      const uint32_t node = c + r >= (uint32_t)P ? c + r - P : c + r;
+      T val = v[0].v[l];
+#pragma unroll
+      for (int q = 1; q < P; ++q)
+        if (q == (int)node) val = v[q].v[l];
+      sum = r == 0 ? val : radd(sum, val);  // transport.cpp:224-226 fold
+    }
+    avg.v[l] = rdiv(sum, T(P));             // transport.cpp:229-235
+  }
+}
+
+template <typename T, bool VEC, int P>
+__device__ __forceinline__ void oneshot_group(const ArOneShotArgs<T>& a, uint64_t k, bool norm,
+                                              double& nacc) {
+  using L = Lanes<T, VEC>;
+  constexpr int W = L::W;
+  const NodeIO<T>& n = a.node;
+  L v[P], x, avg, dp, gb, s, o, xi, ot, od;
+  if (a.pending) {
+#pragma unroll
+    for (int r = 0; r < P; ++r) ld(v[r], a.x_prev[r], k);  // P - 1 NVLink loads in flight
+  }
+  ld(x, n.theta_in, k);
+  if (a.apply_only) {
+    ring_average<T, VEC, P>(v, k, a.ring_base, a.ring_rem, avg);
+#pragma unroll
+    for (int l = 0; l < W; ++l) ot.v[l] = radd(x.v[l], avg.v[l]);
+    st(n.theta_out, k, ot);
+    if (a.agg) st(n.delta, k, avg);
+    return;
+  }
+  if (!a.pending || !a.agg) ld(dp, n.delta, k);
+  ld_grad_inputs(gb, s, o, xi, n, a.spec, a.opt, a.quad, k);
+  if (a.pending) {
+    ring_average<T, VEC, P>(v, k, a.ring_base, a.ring_rem, avg);
+    if (a.agg) dp = avg;  // aggregate scope: delta_prev is the average
+  }
+#pragma unroll
+  for (int l = 0; l < W; ++l) {
+    const T x1 = a.pending ? radd(x.v[l], avg.v[l]) : x.v[l];  // theta += avg (protocols.cpp:126)
+    ot.v[l] = x1;
+    od.v[l] = sgd_delta(x1, dp.v[l], gb.v[l], s.v[l], o.v[l], xi.v[l], n.alpha, a.mu, a.wd,
+                        a.mu_nz, a.wd_pos, a.quad, norm, nacc);
+  }
+  if (a.pending) st(n.theta_out, k, ot);
+  st(a.x_out, k, od);
+  if (!a.agg || !a.pending) st(n.delta, k, od);
+}
+
+template <typename T, bool VEC, int P>
+__global__ void __launch_bounds__(kBlock) k_ar_oneshot(const __grid_constant__ ArOneShotArgs<T> a) {
+  if (!block_wait(a.wait)) return;
+  constexpr int W = Lanes<T, VEC>::W;
+  const bool norm = a.node.norm != nullptr;
+  double nacc = 0.0;
+  const uint64_t nv = a.d / W;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t first = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (uint64_t v = first; v < nv; v += stride) oneshot_group<T, VEC, P>(a, v * W, norm, nacc);
+  if constexpr (VEC) {
+    for (uint64_t k = nv * W + first; k < a.d; k += stride)
+      oneshot_group<T, false, P>(a, k, norm, nacc);
+  }
+  block_add_double(nacc, a.node.norm);
+  block_signal(a.signal);
+}
+
+template <typename T, int P>
+cudaError_t launch_ar_oneshot_p(const ArOneShotArgs<T>& a, int vec, uint32_t grid, cudaStream_t s) {
+  if (vec)
+    k_ar_oneshot<T, true, P><<<grid, kBlock, 0, s>>>(a);
+  else
+    k_ar_oneshot<T, false, P><<<grid, kBlock, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_ar_oneshot(const ArOneShotArgs<T>& a, int vec, uint32_t grid, cudaStream_t s) {
+  switch (a.p) {
+    case 2: return launch_ar_oneshot_p<T, 2>(a, vec, grid, s);
+    case 3: return launch_ar_oneshot_p<T, 3>(a, vec, grid, s);
+    case 4: return launch_ar_oneshot_p<T, 4>(a, vec, grid, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
 // ------------------------------------------- single-context all-reduce round
 // allreduce_round protocols.cpp:110-131 for p nodes on one GPU, one pass:
 // every node's delta, the pivot-form mean of param_vec.cpp:26-38
@@ -948,6 +1046,7 @@ cudaError_t launch_fill_normal(T* out, uint64_t n, double sigma, uint64_t seed, 
   template cudaError_t launch_ar_fused<T>(const ArFusedArgs<T>&, int, uint32_t, cudaStream_t);     \
   template int ar_fused_blocks_per_sm<T>(int);                                                     \
   template cudaError_t launch_trace<T>(const TraceArgs<T>&, uint32_t, cudaStream_t);               \
+  template cudaError_t launch_ar_oneshot<T>(const ArOneShotArgs<T>&, int, uint32_t, cudaStream_t); \
   template cudaError_t launch_spatial_mean<T>(const T* const*, uint32_t, uint64_t, T*,             \
                                               cudaStream_t);                                       \
   template cudaError_t launch_fill_normal<T>(T*, uint64_t, double, uint64_t, uint64_t, cudaStream_t);

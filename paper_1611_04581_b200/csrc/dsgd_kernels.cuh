@@ -131,6 +131,26 @@ struct ArFusedArgs {
   unsigned int* error;
 };
 
+// One-shot multi-GPU all-reduce round (small p): every rank reads every
+// peer's exchange buffer of the previous round directly over NVLink, folds
+// the average in the reference ring order and applies it fused with this
+// round's delta; exchange buffers are double-buffered by round parity.
+template <typename T>
+struct ArOneShotArgs {
+  NodeIO<T> node;                      // theta/delta/grad/noise of this rank
+  const T* x_prev[kMaxFusedRanks];     // every rank's x[(t-1) % 2]
+  T* x_out;                            // own x[t % 2]
+  const T* spec;
+  const T* opt;
+  uint64_t d;
+  uint32_t p;
+  uint64_t ring_base, ring_rem;
+  T mu, wd;
+  int mu_nz, wd_pos, quad, agg, pending, apply_only;
+  WaitSpec wait;
+  SignalSpec signal;
+};
+
 // Single-context all-reduce round (p nodes on one GPU), fused:
 // deltas -> pivot-form spatial mean -> apply.
 template <typename T>
@@ -221,6 +241,8 @@ template <typename T>
 cudaError_t launch_ar_fused(const ArFusedArgs<T>& a, int vec, uint32_t grid, cudaStream_t s);
 template <typename T>
 int ar_fused_blocks_per_sm(int vec);
+template <typename T>
+cudaError_t launch_ar_oneshot(const ArOneShotArgs<T>& a, int vec, uint32_t grid, cudaStream_t s);
 template <typename T>
 cudaError_t launch_trace(const TraceArgs<T>& a, uint32_t grid, cudaStream_t s);
 template <typename T>

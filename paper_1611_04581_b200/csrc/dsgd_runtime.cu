@@ -92,6 +92,7 @@ struct HandleBlob {
   uint64_t off_a;    // all-reduce average buffer
   uint64_t off_ar;   // all-reduce counters: [0] exchange written, [1] average written
   uint64_t off_arf;  // one-kernel all-reduce segment flags (dsgd::ArFlags)
+  uint64_t off_x2;   // second exchange buffer (one-shot all-reduce, round parity)
 };
 static_assert(sizeof(HandleBlob) <= DSGD_HANDLE_BYTES, "handle blob too large");
 
@@ -101,6 +102,7 @@ struct PeerNode {  // device-addressable view of one node (local or IPC-mapped)
   unsigned long long* flags = nullptr;
   unsigned long long* round = nullptr;
   char* x = nullptr;                  // all-reduce exchange buffer
+  char* x2 = nullptr;                 // second exchange buffer (one-shot, odd rounds)
   char* avg = nullptr;                // all-reduce average buffer
   unsigned long long* ar = nullptr;   // [0] exchange written, [1] average written (rounds)
   dsgd::ArFlags* arf = nullptr;       // one-kernel all-reduce segment flags
@@ -142,7 +144,9 @@ struct dsgd_ctx {
   size_t off_theta[kMaxLocal][2] = {};
   size_t off_c_in = 0, off_flags = 0, off_round = 0, off_x = 0, off_a = 0, off_ar = 0;
   bool p2p_allreduce = true;       // multi-GPU all-reduce over NVLink peer memory (else NCCL)
-  bool ar_fused = true;            // ... as one persistent kernel per round (p <= 8)
+  bool ar_fused = false;           // ... as one persistent role-split kernel per round (p <= 8)
+  bool ar_oneshot = false;         // ... one-shot: read every peer's exchange buffer (p <= 4)
+  size_t off_x2 = 0;
   size_t off_arf = 0;
   dsgd::ArArrive* ar_arrive = nullptr;
   uint32_t ar_segments = 16;
@@ -470,7 +474,6 @@ dsgd_status do_pull(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& gs,
   return DSGD_OK;
 }
 
-// Materialises a deferred multi-GPU all-reduce apply: theta += avg.
 // Waits of a peer-memory all-reduce kernel: every rank's counter `which`
 // (0: exchange written, 1: average written) has reached `need`.
 void ar_waits(dsgd_ctx* c, int which, unsigned long long need, dsgd::WaitSpec* w) {
@@ -484,9 +487,47 @@ void ar_waits(dsgd_ctx* c, int which, unsigned long long need, dsgd::WaitSpec* w
   }
 }
 
+char* x_of(dsgd_ctx* c, uint32_t k, uint64_t round) {
+  return (round & 1) ? c->peers[k].x2 : c->peers[k].x;
+}
+
+template <typename T>
+dsgd::ArOneShotArgs<T> oneshot_args(dsgd_ctx* c, dsgd_momentum_scope scope) {
+  dsgd::ArOneShotArgs<T> a{};
+  const uint64_t t = c->ar_rounds;
+  for (uint32_t k = 0; k < c->p; ++k) a.x_prev[k] = t ? as<T>(x_of(c, k, t - 1)) : nullptr;
+  a.x_out = as<T>(x_of(c, c->first, t));
+  a.d = c->d;
+  a.p = c->p;
+  a.ring_base = c->d / c->p;
+  a.ring_rem = c->d % c->p;
+  a.agg = scope == DSGD_SCOPE_AGGREGATE;
+  a.pending = c->ar_pending;
+  return a;
+}
+
+// Materialises a deferred multi-GPU all-reduce apply: theta += avg.
 template <typename T>
 dsgd_status flush_pending_t(dsgd_ctx* c) {
   if (!c->ar_pending) return DSGD_OK;
+  if (c->p2p_allreduce && c->ar_oneshot) {
+    dsgd::ArOneShotArgs<T> a = oneshot_args<T>(c, c->ar_pending_scope);
+    a.node.theta_in = as<T>(c->theta_ptr(0, c->cur));
+    a.node.theta_out = as<T>(c->theta_ptr(0, c->cur ^ 1));
+    a.node.delta = as<T>(c->delta[0]);
+    a.apply_only = 1;
+    ar_waits(c, 0, c->ar_rounds, &a.wait);  // every rank's last exchange is written
+    build_signal(c, &a.signal);
+    {
+      LaunchScope ls(c, DSGD_K_AR_APPLY);
+      DSGD_CUDA(dsgd::launch_ar_oneshot<T>(a, 1, blocks_for(c, (c->d / (16 / sizeof(T)) + 1), 1),
+                                           c->stream));
+    }
+    c->seq += 1;
+    c->cur ^= 1;
+    c->ar_pending = false;
+    return DSGD_OK;
+  }
   const bool p2p = c->p2p_allreduce;
   char* xbuf = p2p ? c->peers[c->first].avg
                    : (c->ar_pending_scope == DSGD_SCOPE_PER_NODE ? c->aux[0] : c->delta[0]);
@@ -536,6 +577,35 @@ dsgd_status do_allreduce_p2p(dsgd_ctx* c, const dsgd_hyperparams* h, const GradS
   const uint32_t me = c->first;
   const bool fused = c->ar_pending;
   const unsigned long long t = c->ar_rounds;
+  if (c->ar_oneshot) {
+    dsgd::ArOneShotArgs<T> a = oneshot_args<T>(c, scope);
+    fill_node<T>(c, 0, gs, h, &a.node);
+    if (fused) a.node.theta_out = as<T>(c->theta_ptr(0, c->cur ^ 1));
+    a.spec = gs.quad ? as<T>(c->spec) : nullptr;
+    a.opt = gs.quad ? as<T>(c->opt) : nullptr;
+    a.mu = (T)h->mu;
+    a.wd = (T)h->weight_decay;
+    a.mu_nz = h->mu != 0.0;
+    a.wd_pos = h->weight_decay > 0.0;
+    a.quad = gs.quad;
+    // RAW on every rank's x[t-1], WAR on my x[t % 2] (read by peers in round t-1)
+    ar_waits(c, 0, t, &a.wait);
+    a.signal.counter = c->peers[me].ar + 0;
+    a.signal.value = t + 1;
+    a.signal.arrive = c->arrive;
+    const bool vec = all_aligned(c, gs);
+    const uint64_t W = vec ? 16 / sizeof(T) : 1;
+    {
+      LaunchScope ls(c, DSGD_K_NCCL);
+      DSGD_CUDA(dsgd::launch_ar_oneshot<T>(a, vec, blocks_for(c, c->d / W, 1), c->stream));
+    }
+    if (fused) c->cur ^= 1;
+    c->ar_rounds = t + 1;
+    c->ar_pending = true;
+    c->ar_pending_scope = scope;
+    c->prev_readers.clear();
+    return DSGD_OK;
+  }
   if (c->ar_fused && c->p <= (uint32_t)dsgd::kMaxFusedRanks) {
     dsgd::ArFusedArgs<T> a{};
     fill_node<T>(c, 0, gs, h, &a.node);
@@ -903,11 +973,19 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
     off += 256;
     c->off_arf = off;
     off += align_up(sizeof(dsgd::ArFlags));
+    c->off_x2 = off;
+    off += vb;
   }
   c->arena_bytes = off;
-  if (const char* e = std::getenv("DSGD_ALLREDUCE")) {
-    c->p2p_allreduce = std::string(e) != "nccl";
-    c->ar_fused = std::string(e) != "p2p2k";  // p2p2k: the two-kernel variant
+  // multi-GPU all-reduce backend: oneshot (default p <= 2), p2p (two-shot,
+  // default p > 2), fused (persistent role-split kernel), nccl
+  {
+    std::string mode = c->p <= 2 ? "oneshot" : "p2p";
+    if (const char* e = std::getenv("DSGD_ALLREDUCE")) mode = e;
+    if (mode == "p2p2k") mode = "p2p";
+    c->p2p_allreduce = mode != "nccl";
+    c->ar_fused = mode == "fused";
+    c->ar_oneshot = mode == "oneshot" && c->p <= 4;
   }
   if (const char* e = std::getenv("DSGD_AR_SEGMENTS"))
     c->ar_segments = (uint32_t)std::min(dsgd::kMaxSegments, std::max(1, atoi(e)));
@@ -953,6 +1031,7 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
       pn.avg = c->arena + c->off_a;
       pn.ar = reinterpret_cast<unsigned long long*>(c->arena + c->off_ar);
       pn.arf = reinterpret_cast<dsgd::ArFlags*>(c->arena + c->off_arf);
+      pn.x2 = c->arena + c->off_x2;
     }
     if (i == 0 && (c->flags & DSGD_CTX_CENTER)) {
       pn.c_in = c->arena + c->off_c_in;
@@ -1602,6 +1681,7 @@ dsgd_status dsgd_ctx_export_handle(dsgd_ctx* c, void* blob) {
   b.off_a = c->off_a;
   b.off_ar = c->off_ar;
   b.off_arf = c->off_arf;
+  b.off_x2 = c->off_x2;
   std::memset(blob, 0, DSGD_HANDLE_BYTES);
   std::memcpy(blob, &b, sizeof(b));
   return DSGD_OK;
@@ -1651,6 +1731,7 @@ dsgd_status dsgd_ctx_connect_peers(dsgd_ctx* c, const void* blobs) {
       pn.avg = m + b.off_a;
       pn.ar = reinterpret_cast<unsigned long long*>(m + b.off_ar);
       pn.arf = reinterpret_cast<dsgd::ArFlags*>(m + b.off_arf);
+      pn.x2 = m + b.off_x2;
     }
     if (b.flags & DSGD_CTX_CENTER) {
       pn.c_in = m + b.off_c_in;

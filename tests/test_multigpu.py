@@ -22,15 +22,17 @@ def n_gpus():
 
 @pytest.mark.skipif("n_gpus() < 2")
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
-@pytest.mark.parametrize("backend", ["p2p", "p2p2k", "nccl"])
+@pytest.mark.parametrize("backend", ["default", "p2p", "fused", "nccl"])
 def test_two_gpu_protocols_match_oracle(dtype, backend):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1",
-           "--master-port", str(29611 + (dtype == "f32") + 2 * ["p2p", "p2p2k", "nccl"].index(backend)),
+           "--master-port",
+           str(29611 + (dtype == "f32") + 2 * ["default", "p2p", "fused", "nccl"].index(backend)),
            os.path.join(ROOT, "tests", "mgpu_worker.py"), dtype]
-    if backend != "p2p":
+    env = dict(os.environ)
+    if backend != "default":   # default at p = 2: the one-shot peer-memory kernel
         cmd.append("allreduce-only")
-    env = dict(os.environ, DSGD_ALLREDUCE=backend)
+        env["DSGD_ALLREDUCE"] = backend
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     line = [l for l in out.stdout.splitlines() if l.startswith("RESULT ")][0]
