@@ -163,12 +163,25 @@ __device__ __forceinline__ T noise_at(const NodeIO<T>& n, uint64_t k) {
 }
 
 // ------------------------------------------------- fused gossip-family step
+// Inputs of one coordinate group, loaded before any store of the iteration
+// so two groups per thread are in flight (the compiler cannot hoist loads
+// above stores through possibly aliasing pointers).
+template <typename T, bool VEC>
+struct StepIn {
+  Lanes<T, VEC> x, dp, gb, s, o, xi, xj, ax;
+};
+
 template <typename T, int MODE, bool VEC>
-__device__ __forceinline__ void step_group(const StepArgs<T>& a, const NodeIO<T>& n, uint64_t k,
-                                           bool norm, double& nacc) {
-  using L = Lanes<T, VEC>;
-  constexpr int W = L::W;
-  L x, dp, gb, s, o, xi, xj, ax, out_t, out_d;
+__device__ __forceinline__ void step_load(const StepArgs<T>& a, const NodeIO<T>& n, uint64_t k,
+                                          StepIn<T, VEC>& in) {
+  auto& x = in.x;
+  auto& dp = in.dp;
+  auto& gb = in.gb;
+  auto& s = in.s;
+  auto& o = in.o;
+  auto& xi = in.xi;
+  auto& xj = in.xj;
+  auto& ax = in.ax;
   ld(x, n.theta_in, k);
   if constexpr (MODE == kModePull || MODE == kModeStale || MODE == kModeMix || MODE == kModeAsync)
     ld(xj, n.partner, k);
@@ -185,6 +198,22 @@ __device__ __forceinline__ void step_group(const StepArgs<T>& a, const NodeIO<T>
   }
   if constexpr (MODE != kModeMix && MODE != kModeApply)
     ld_grad_inputs(gb, s, o, xi, n, a.spec, a.opt, a.quad, k);
+}
+
+template <typename T, int MODE, bool VEC>
+__device__ __forceinline__ void step_store(const StepArgs<T>& a, const NodeIO<T>& n, uint64_t k,
+                                           const StepIn<T, VEC>& in, bool norm, double& nacc) {
+  using L = Lanes<T, VEC>;
+  constexpr int W = L::W;
+  const auto& x = in.x;
+  const auto& dp = in.dp;
+  const auto& gb = in.gb;
+  const auto& s = in.s;
+  const auto& o = in.o;
+  const auto& xi = in.xi;
+  const auto& xj = in.xj;
+  const auto& ax = in.ax;
+  L out_t, out_d;
 #pragma unroll
   for (int l = 0; l < W; ++l) {
     if constexpr (MODE == kModeStep) {
@@ -241,6 +270,14 @@ __device__ __forceinline__ void step_group(const StepArgs<T>& a, const NodeIO<T>
 }
 
 template <typename T, int MODE, bool VEC>
+__device__ __forceinline__ void step_group(const StepArgs<T>& a, const NodeIO<T>& n, uint64_t k,
+                                           bool norm, double& nacc) {
+  StepIn<T, VEC> in;
+  step_load<T, MODE, VEC>(a, n, k, in);
+  step_store<T, MODE, VEC>(a, n, k, in, norm, nacc);
+}
+
+template <typename T, int MODE, bool VEC>
 __global__ void __launch_bounds__(kBlock) k_step(const __grid_constant__ StepArgs<T> a) {
   if (!block_wait(a.wait)) return;
   const uint32_t node = blockIdx.x / a.blocks_per_node;
@@ -255,8 +292,11 @@ __global__ void __launch_bounds__(kBlock) k_step(const __grid_constant__ StepArg
   // two independent groups per iteration keep 2x the bytes in flight
   uint64_t v = first;
   for (; v + stride < nv; v += 2 * stride) {
-    step_group<T, MODE, VEC>(a, n, v * W, norm, nacc);
-    step_group<T, MODE, VEC>(a, n, (v + stride) * W, norm, nacc);
+    StepIn<T, VEC> i0, i1;
+    step_load<T, MODE, VEC>(a, n, v * W, i0);
+    step_load<T, MODE, VEC>(a, n, (v + stride) * W, i1);
+    step_store<T, MODE, VEC>(a, n, v * W, i0, norm, nacc);
+    step_store<T, MODE, VEC>(a, n, (v + stride) * W, i1, norm, nacc);
   }
   if (v < nv) step_group<T, MODE, VEC>(a, n, v * W, norm, nacc);
   if constexpr (VEC) {
@@ -527,41 +567,62 @@ __device__ __forceinline__ void ring_average(const Lanes<T, VEC> (&v)[P], uint64
 }
 
 template <typename T, bool VEC, int P>
-__device__ __forceinline__ void oneshot_group(const ArOneShotArgs<T>& a, uint64_t k, bool norm,
+struct OneshotIn {
+  Lanes<T, VEC> v[P], x, dp, gb, s, o, xi;
+};
+
+template <typename T, bool VEC, int P>
+__device__ __forceinline__ void oneshot_load(const ArOneShotArgs<T>& a, uint64_t k,
+                                             OneshotIn<T, VEC, P>& in) {
+  const NodeIO<T>& n = a.node;
+  if (a.pending) {
+#pragma unroll
+    for (int r = 0; r < P; ++r) ld(in.v[r], a.x_prev[r], k);  // P - 1 NVLink loads in flight
+  }
+  ld(in.x, n.theta_in, k);
+  if (a.apply_only) return;
+  if (!a.pending || !a.agg) ld(in.dp, n.delta, k);
+  ld_grad_inputs(in.gb, in.s, in.o, in.xi, n, a.spec, a.opt, a.quad, k);
+}
+
+template <typename T, bool VEC, int P>
+__device__ __forceinline__ void oneshot_store(const ArOneShotArgs<T>& a, uint64_t k,
+                                              const OneshotIn<T, VEC, P>& in, bool norm,
                                               double& nacc) {
   using L = Lanes<T, VEC>;
   constexpr int W = L::W;
   const NodeIO<T>& n = a.node;
-  L v[P], x, avg, dp, gb, s, o, xi, ot, od;
-  if (a.pending) {
-#pragma unroll
-    for (int r = 0; r < P; ++r) ld(v[r], a.x_prev[r], k);  // P - 1 NVLink loads in flight
-  }
-  ld(x, n.theta_in, k);
+  L avg, dp = in.dp, ot, od;
   if (a.apply_only) {
-    ring_average<T, VEC, P>(v, k, a.ring_base, a.ring_rem, avg);
+    ring_average<T, VEC, P>(in.v, k, a.ring_base, a.ring_rem, avg);
 #pragma unroll
-    for (int l = 0; l < W; ++l) ot.v[l] = radd(x.v[l], avg.v[l]);
+    for (int l = 0; l < W; ++l) ot.v[l] = radd(in.x.v[l], avg.v[l]);
     st(n.theta_out, k, ot);
     if (a.agg) st(n.delta, k, avg);
     return;
   }
-  if (!a.pending || !a.agg) ld(dp, n.delta, k);
-  ld_grad_inputs(gb, s, o, xi, n, a.spec, a.opt, a.quad, k);
   if (a.pending) {
-    ring_average<T, VEC, P>(v, k, a.ring_base, a.ring_rem, avg);
+    ring_average<T, VEC, P>(in.v, k, a.ring_base, a.ring_rem, avg);
     if (a.agg) dp = avg;  // aggregate scope: delta_prev is the average
   }
 #pragma unroll
   for (int l = 0; l < W; ++l) {
-    const T x1 = a.pending ? radd(x.v[l], avg.v[l]) : x.v[l];  // theta += avg (protocols.cpp:126)
+    const T x1 = a.pending ? radd(in.x.v[l], avg.v[l]) : in.x.v[l];  // theta += avg (protocols.cpp:126)
     ot.v[l] = x1;
-    od.v[l] = sgd_delta(x1, dp.v[l], gb.v[l], s.v[l], o.v[l], xi.v[l], n.alpha, a.mu, a.wd,
-                        a.mu_nz, a.wd_pos, a.quad, norm, nacc);
+    od.v[l] = sgd_delta(x1, dp.v[l], in.gb.v[l], in.s.v[l], in.o.v[l], in.xi.v[l], n.alpha, a.mu,
+                        a.wd, a.mu_nz, a.wd_pos, a.quad, norm, nacc);
   }
   if (a.pending) st(n.theta_out, k, ot);
   st(a.x_out, k, od);
   if (!a.agg || !a.pending) st(n.delta, k, od);
+}
+
+template <typename T, bool VEC, int P>
+__device__ __forceinline__ void oneshot_group(const ArOneShotArgs<T>& a, uint64_t k, bool norm,
+                                              double& nacc) {
+  OneshotIn<T, VEC, P> in;
+  oneshot_load<T, VEC, P>(a, k, in);
+  oneshot_store<T, VEC, P>(a, k, in, norm, nacc);
 }
 
 template <typename T, bool VEC, int P>
@@ -573,7 +634,15 @@ __global__ void __launch_bounds__(kBlock) k_ar_oneshot(const __grid_constant__ A
   const uint64_t nv = a.d / W;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t first = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (uint64_t v = first; v < nv; v += stride) oneshot_group<T, VEC, P>(a, v * W, norm, nacc);
+  uint64_t v = first;
+  for (; v + stride < nv; v += 2 * stride) {  // two groups in flight per thread
+    OneshotIn<T, VEC, P> i0, i1;
+    oneshot_load<T, VEC, P>(a, v * W, i0);
+    oneshot_load<T, VEC, P>(a, (v + stride) * W, i1);
+    oneshot_store<T, VEC, P>(a, v * W, i0, norm, nacc);
+    oneshot_store<T, VEC, P>(a, (v + stride) * W, i1, norm, nacc);
+  }
+  if (v < nv) oneshot_group<T, VEC, P>(a, v * W, norm, nacc);
   if constexpr (VEC) {
     for (uint64_t k = nv * W + first; k < a.d; k += stride)
       oneshot_group<T, false, P>(a, k, norm, nacc);
@@ -582,12 +651,130 @@ __global__ void __launch_bounds__(kBlock) k_ar_oneshot(const __grid_constant__ A
   block_signal(a.signal);
 }
 
+// One-shot round with the peer exchange buffers staged through shared memory
+// by bulk async copies (TMA engine, mbarrier completion), kStages tiles
+// ahead: the NVLink stream's bytes in flight no longer cost registers.
+constexpr int kOsStages = 4;
+constexpr int kOsVecPerThread = 2;
+
+template <typename T>
+__host__ __device__ constexpr uint64_t os_tile() {  // elements per tile
+  return (uint64_t)kBlock * Vec<T>::N * kOsVecPerThread;
+}
+
+template <typename T, int P>
+__device__ __forceinline__ void os_load_local(const ArOneShotArgs<T>& a, uint32_t me, uint64_t k,
+                                              OneshotIn<T, true, P>& in) {
+  const NodeIO<T>& n = a.node;
+  (void)me;
+  ld(in.x, n.theta_in, k);
+  if (!a.agg) ld(in.dp, n.delta, k);
+  ld_grad_inputs(in.gb, in.s, in.o, in.xi, n, a.spec, a.opt, a.quad, k);
+}
+
+// Every rank's tile (own included) sits in slot r of the stage, so the
+// register array is indexed at compile time only.
+template <typename T, int P>
+__device__ __forceinline__ void os_load_stage(uint32_t me, const T* src0, OneshotIn<T, true, P>& in) {
+  constexpr uint64_t TILE = os_tile<T>();
+  (void)me;
+#pragma unroll
+  for (int r = 0; r < P; ++r) {
+    Vec<T> t;
+    t.u = *reinterpret_cast<const uint4*>(src0 + (uint64_t)r * TILE);
+#pragma unroll
+    for (int l = 0; l < Vec<T>::N; ++l) in.v[r].v[l] = t.t[l];
+  }
+}
+
+// Thread 0: bulk-copy every remote rank's tile j (of this CTA) into stage s.
+template <typename T, int P>
+__device__ __forceinline__ void os_issue(const ArOneShotArgs<T>& a, uint32_t me, uint64_t nt,
+                                         uint64_t j, int s, uint64_t* bars, T* stage) {
+  constexpr uint64_t TILE = os_tile<T>();
+  constexpr uint32_t TB = (uint32_t)(TILE * sizeof(T));
+  const uint64_t tile = blockIdx.x + j * gridDim.x;
+  if (tile >= nt) return;
+  (void)me;
+  mbar_expect_tx(&bars[s], TB * P);
+#pragma unroll
+  for (int r = 0; r < P; ++r)  // P - 1 peers over NVLink + the own tile from local HBM
+    bulk_g2s(stage + ((uint64_t)s * P + r) * TILE, a.x_prev[r] + tile * TILE, TB, &bars[s]);
+}
+
+template <typename T, int P>
+__global__ void __launch_bounds__(kBlock) k_ar_oneshot_tma(const __grid_constant__ ArOneShotArgs<T> a,
+                                                           uint32_t me) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr uint64_t TILE = os_tile<T>();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
+  T* stage = reinterpret_cast<T*>(smem_raw + 128);
+  if (!block_wait(a.wait)) return;
+  const uint64_t nt = a.d / TILE;
+  const bool norm = a.node.norm != nullptr;
+  double nacc = 0.0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kOsStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int s = 0; s < kOsStages; ++s) os_issue<T, P>(a, me, nt, s, s, bars, stage);
+  using L = Lanes<T, true>;
+  constexpr int W = L::W;
+  for (uint64_t j = 0;; ++j) {
+    const uint64_t tile = blockIdx.x + j * gridDim.x;
+    if (tile >= nt) break;
+    const int s = (int)(j % kOsStages);
+    const uint32_t parity = (uint32_t)((j / kOsStages) & 1);
+    OneshotIn<T, true, P> in0, in1;
+    const uint64_t k0 = tile * TILE + (uint64_t)threadIdx.x * W;
+    const uint64_t k1 = k0 + (uint64_t)kBlock * W;
+    os_load_local<T, P>(a, me, k0, in0);  // local streams through registers (HBM latency)
+    os_load_local<T, P>(a, me, k1, in1);
+    mbar_wait(&bars[s], parity);
+    const T* st0 = stage + (uint64_t)s * P * TILE + (uint64_t)threadIdx.x * W;
+    os_load_stage<T, P>(me, st0, in0);
+    os_load_stage<T, P>(me, st0 + (uint64_t)kBlock * W, in1);
+    __syncthreads();  // every thread is done with stage s
+    if (threadIdx.x == 0) os_issue<T, P>(a, me, nt, j + kOsStages, s, bars, stage);
+    oneshot_store<T, true, P>(a, k0, in0, norm, nacc);
+    oneshot_store<T, true, P>(a, k1, in1, norm, nacc);
+  }
+  // ragged tail [nt * TILE, d): plain global loads
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t kk = nt * TILE + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; kk < a.d;
+       kk += stride)
+    oneshot_group<T, false, P>(a, kk, norm, nacc);
+  block_add_double(nacc, a.node.norm);
+  block_signal(a.signal);
+}
+
 template <typename T, int P>
 cudaError_t launch_ar_oneshot_p(const ArOneShotArgs<T>& a, int vec, uint32_t grid, cudaStream_t s) {
-  if (vec)
+  if (vec && a.pending && !a.apply_only && a.tma_rank >= 0) {
+    const size_t smem = 128 + (size_t)kOsStages * P * os_tile<T>() * sizeof(T);
+    static int resident = 0;  // CTAs per SM at this smem size (persistent grid)
+    if (!resident) {
+      cudaFuncSetAttribute(k_ar_oneshot_tma<T, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_ar_oneshot_tma<T, P>, kBlock,
+                                                    smem);
+      if (resident < 1) resident = 1;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t tiles = a.d / os_tile<T>();
+    uint32_t g = (uint32_t)sms * (uint32_t)resident;
+    if (tiles < g) g = (uint32_t)(tiles ? tiles : 1);
+    (void)grid;
+    k_ar_oneshot_tma<T, P><<<g, kBlock, smem, s>>>(a, (uint32_t)a.tma_rank);
+  } else if (vec) {
     k_ar_oneshot<T, true, P><<<grid, kBlock, 0, s>>>(a);
-  else
+  } else {
     k_ar_oneshot<T, false, P><<<grid, kBlock, 0, s>>>(a);
+  }
   return cudaGetLastError();
 }
 

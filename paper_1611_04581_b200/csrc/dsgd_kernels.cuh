@@ -147,6 +147,7 @@ struct ArOneShotArgs {
   uint64_t ring_base, ring_rem;
   T mu, wd;
   int mu_nz, wd_pos, quad, agg, pending, apply_only;
+  int tma_rank;                        // >= 0: stage peers through smem (this rank's id)
   WaitSpec wait;
   SignalSpec signal;
 };

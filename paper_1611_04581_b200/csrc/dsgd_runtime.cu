@@ -146,6 +146,7 @@ struct dsgd_ctx {
   bool p2p_allreduce = true;       // multi-GPU all-reduce over NVLink peer memory (else NCCL)
   bool ar_fused = false;           // ... as one persistent role-split kernel per round (p <= 8)
   bool ar_oneshot = false;         // ... one-shot: read every peer's exchange buffer (p <= 4)
+  bool ar_tma = true;              // ... staging the peer reads through smem (bulk async copies)
   size_t off_x2 = 0;
   size_t off_arf = 0;
   dsgd::ArArrive* ar_arrive = nullptr;
@@ -503,6 +504,7 @@ dsgd::ArOneShotArgs<T> oneshot_args(dsgd_ctx* c, dsgd_momentum_scope scope) {
   a.ring_rem = c->d % c->p;
   a.agg = scope == DSGD_SCOPE_AGGREGATE;
   a.pending = c->ar_pending;
+  a.tma_rank = c->ar_tma ? (int)c->first : -1;
   return a;
 }
 
@@ -987,6 +989,7 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
     c->ar_fused = mode == "fused";
     c->ar_oneshot = mode == "oneshot" && c->p <= 4;
   }
+  if (const char* e = std::getenv("DSGD_AR_TMA")) c->ar_tma = atoi(e) != 0;
   if (const char* e = std::getenv("DSGD_AR_SEGMENTS"))
     c->ar_segments = (uint32_t)std::min(dsgd::kMaxSegments, std::max(1, atoi(e)));
   if (const char* e = std::getenv("DSGD_AR_A_FRAC")) c->ar_a_frac = std::min(0.95, std::max(0.05, atof(e)));
