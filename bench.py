@@ -246,21 +246,29 @@ def main():
     value = world * d / (step_ms * 1e-3)
 
     # dominant kernel + roofline (algorithmic bytes per launch)
-    backend = os.environ.get("DSGD_ALLREDUCE", "p2p")
+    backend = os.environ.get("DSGD_ALLREDUCE", "oneshot" if world <= 2 else "p2p")
     peak, peak_src = peaks()
     nv_peak = 770.0  # measured peer copy per direction (B200_PROFILING.md)
-    nv_bytes = 2 * (world - 1) / world * es * d  # per direction per GPU (ring-equivalent)
+    if backend == "oneshot":
+        nv_bytes = (world - 1) * es * d              # each rank reads every peer's exchange
+    else:
+        nv_bytes = 2 * (world - 1) / world * es * d  # two-shot / ring, per direction per GPU
     if world == 1:
         kname, bpp = "allreduce_local", 5 * es  # read theta, delta, g; write theta', delta'
         kdesc = "k_allreduce_local (p=1): fused delta + mean + apply, 12 B read + 8 B write per param"
-    elif backend == "p2p":
-        kname, bpp = "allreduce_comm", 7 * es
-        kdesc = ("k_ar_fused: one persistent kernel per round; HBM 28 B/param (theta, avg, g read; "
-                 "theta', x write; avg slices written by every owner; x served to peers), NVLink "
-                 f"{nv_bytes / d:.1f} B/param each direction")
+    elif backend == "oneshot":
+        kname, bpp = "allreduce_comm", (5 + (world - 1)) * es
+        kdesc = ("k_ar_oneshot_tma: one kernel per round; every rank's previous exchange tile staged "
+                 "in smem by cp.async.bulk (P-1 over NVLink), ring-order average fused with theta += "
+                 "avg and the next delta; HBM: theta, g, own x read + theta', x' write + x served "
+                 f"to {world - 1} peer(s); NVLink {nv_bytes / d:.0f} B/param each direction")
+    elif backend in ("p2p", "fused"):
+        kname, bpp = "allreduce_comm", 2 * es
+        kdesc = ("k_ar_reduce: ring-order reduce of this rank's chunk from every rank + average "
+                 f"to every rank; NVLink {nv_bytes / d:.1f} B/param each direction")
     else:
         kname, bpp = "ar_delta", 5 * es
-        kdesc = "k_step<ApplyDelta>: read theta, avg, g; write theta', delta' (then the exchange)"
+        kdesc = "k_step<ApplyDelta>: read theta, avg, g; write theta', delta' (then ncclAllReduce)"
     kms, kn = prof.get(kname, (0.0, 0))
     kavg_ms = kms / max(1, kn)
     achieved = (bpp * d / (kavg_ms * 1e-3) / 1e9) if kn else None

@@ -20,14 +20,27 @@ def n_gpus():
     return torch.cuda.device_count()
 
 
+BACKENDS = ["default", "oneshot", "p2p", "fused", "nccl"]
+
+
+def worlds():
+    try:
+        n = n_gpus()
+    except Exception:
+        n = 0
+    return [w for w in (2, 4, 8) if w <= n] or [2]
+
+
 @pytest.mark.skipif("n_gpus() < 2")
+@pytest.mark.parametrize("world", worlds())
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
-@pytest.mark.parametrize("backend", ["default", "p2p", "fused", "nccl"])
-def test_two_gpu_protocols_match_oracle(dtype, backend):
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr", "127.0.0.1",
-           "--master-port",
-           str(29611 + (dtype == "f32") + 2 * ["default", "p2p", "fused", "nccl"].index(backend)),
+@pytest.mark.parametrize("backend", BACKENDS)
+def test_multi_gpu_protocols_match_oracle(world, dtype, backend):
+    if backend == "oneshot" and world > 4:
+        pytest.skip("one-shot all-reduce is for p <= 4")
+    port = 29611 + 16 * (world // 2) + (dtype == "f32") + 2 * BACKENDS.index(backend)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.join(ROOT, "tests", "mgpu_worker.py"), dtype]
     env = dict(os.environ)
     if backend != "default":   # default at p = 2: the one-shot peer-memory kernel
