@@ -246,11 +246,13 @@ def main():
     value = world * d / (step_ms * 1e-3)
 
     # dominant kernel + roofline (algorithmic bytes per launch)
-    backend = os.environ.get("DSGD_ALLREDUCE", "oneshot" if world <= 2 else "p2p")
+    backend = getattr(grp, "allreduce_backend", "local")
     peak, peak_src = peaks()
     nv_peak = 770.0  # measured peer copy per direction (B200_PROFILING.md)
     if backend == "oneshot":
         nv_bytes = (world - 1) * es * d              # each rank reads every peer's exchange
+    elif backend == "nvls":
+        nv_bytes = (1 + 1 / world) * es * d          # switch reads every x once + multicast avg
     else:
         nv_bytes = 2 * (world - 1) / world * es * d  # two-shot / ring, per direction per GPU
     if world == 1:
@@ -262,7 +264,12 @@ def main():
                  "in smem by cp.async.bulk (P-1 over NVLink), ring-order average fused with theta += "
                  "avg and the next delta; HBM: theta, g, own x read + theta', x' write + x served "
                  f"to {world - 1} peer(s); NVLink {nv_bytes / d:.0f} B/param each direction")
-    elif backend in ("p2p", "fused"):
+    elif backend == "nvls":
+        kname, bpp = "allreduce_comm", 2 * es
+        kdesc = ("k_ar_nvls: multimem.ld_reduce of this rank's slice of every GPU's exchange "
+                 "buffer (sum in the NVSwitch) + multimem.st of the average to every GPU; "
+                 f"NVLink ~{nv_bytes / d:.1f} B/param each direction")
+    elif backend == "p2p":
         kname, bpp = "allreduce_comm", 2 * es
         kdesc = ("k_ar_reduce: ring-order reduce of this rank's chunk from every rank + average "
                  f"to every rank; NVLink {nv_bytes / d:.1f} B/param each direction")
@@ -288,6 +295,8 @@ def main():
         nms, nn = prof.get("allreduce_comm", (0.0, 0))
         t_c = nms / max(1, nn) * 1e-3
         roofline["allreduce_backend"] = backend
+        if getattr(grp, "nvls_unavailable", None):
+            roofline["nvls_unavailable"] = grp.nvls_unavailable
         roofline["allreduce_comm_us"] = t_c * 1e6
         roofline["nvlink_bytes_per_direction"] = nv_bytes
         roofline["nvlink_achieved_gbs"] = nv_bytes / t_c / 1e9 if nn else None

@@ -294,6 +294,14 @@ dsgd_status dsgd_ctx_round(dsgd_ctx* ctx, uint64_t* round); /* rounds completed 
  * blobs out of band (e.g. torch.distributed all_gather) and connects. */
 dsgd_status dsgd_ctx_export_handle(dsgd_ctx* ctx, void* blob /* DSGD_HANDLE_BYTES */);
 dsgd_status dsgd_ctx_connect_peers(dsgd_ctx* ctx, const void* blobs /* p blobs */);
+/* NVLS (in-switch) all-reduce: `x` and `avg` are this context's d-element
+ * slices of a multicast-mapped (NVSwitch multicast object) allocation and
+ * `x_mc` / `avg_mc` their multicast addresses (e.g. from
+ * torch.distributed._symmetric_memory).  After this call the multi-GPU
+ * all-reduce reduces with multimem.ld_reduce and broadcasts with
+ * multimem.st (summation order: the switch's). */
+dsgd_status dsgd_ctx_attach_multicast(dsgd_ctx* ctx, void* x, void* x_mc, void* avg,
+                                      void* avg_mc);
 dsgd_status dsgd_nccl_unique_id(void* id /* DSGD_NCCL_ID_BYTES */);
 dsgd_status dsgd_ctx_init_nccl(dsgd_ctx* ctx, const void* id, int rank, int nranks);
 /* Spin-wait bound for cross-GPU flags (default 10 s). */

@@ -131,6 +131,7 @@ _SIGS = {
     "dsgd_ctx_export_handle": (C.c_int, [_P, _P]),
     "dsgd_ctx_connect_peers": (C.c_int, [_P, _P]),
     "dsgd_nccl_unique_id": (C.c_int, [_P]),
+    "dsgd_ctx_attach_multicast": (C.c_int, [_P, _P, _P, _P, _P]),
     "dsgd_ctx_init_nccl": (C.c_int, [_P, _P, C.c_int, C.c_int]),
     "dsgd_ctx_set_timeout": (C.c_int, [_P, C.c_double]),
     "dsgd_profile_enable": (C.c_int, [_P, C.c_int]),

@@ -307,8 +307,115 @@ __global__ void __launch_bounds__(kBlock) k_step(const __grid_constant__ StepArg
   block_signal(a.signal);
 }
 
+// Gossip-family step of ONE node whose partner snapshot lives in a peer GPU:
+// the partner tiles are staged through shared memory by cp.async.bulk
+// (kOsStages ahead, mbarrier completion) so the NVLink read stream keeps many
+// KB in flight per SM without registers; the local streams use LDG.
+constexpr int kStStages = 4;
+template <typename T>
+__host__ __device__ constexpr uint64_t st_tile() {
+  return (uint64_t)kBlock * Vec<T>::N * 2;
+}
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(kBlock) k_step_tma(const __grid_constant__ StepArgs<T> a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr uint64_t TILE = st_tile<T>();
+  constexpr uint32_t TB = (uint32_t)(TILE * sizeof(T));
+  constexpr int W = Vec<T>::N;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
+  T* stage = reinterpret_cast<T*>(smem_raw + 128);
+  if (!block_wait(a.wait)) return;
+  const NodeIO<T>& n = a.node[0];
+  const uint64_t nt = a.d / TILE;
+  const bool norm = n.norm != nullptr;
+  double nacc = 0.0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+    for (int s = 0; s < kStStages; ++s) {
+      const uint64_t tile = blockIdx.x + (uint64_t)s * gridDim.x;
+      if (tile < nt) {
+        mbar_expect_tx(&bars[s], TB);
+        bulk_g2s(stage + (uint64_t)s * TILE, n.partner + tile * TILE, TB, &bars[s]);
+      }
+    }
+  }
+  __syncthreads();
+  for (uint64_t j = 0;; ++j) {
+    const uint64_t tile = blockIdx.x + j * gridDim.x;
+    if (tile >= nt) break;
+    const int s = (int)(j % kStStages);
+    const uint32_t parity = (uint32_t)((j / kStStages) & 1);
+    const uint64_t k0 = tile * TILE + (uint64_t)threadIdx.x * W;
+    const uint64_t k1 = k0 + (uint64_t)kBlock * W;
+    StepIn<T, true> i0, i1;
+    // local streams (theta, delta, gradient, noise); the partner comes from smem
+    ld(i0.x, n.theta_in, k0);
+    ld(i1.x, n.theta_in, k1);
+    if constexpr (MODE != kModeMix) {
+      ld(i0.dp, n.delta, k0);
+      ld(i1.dp, n.delta, k1);
+      ld_grad_inputs(i0.gb, i0.s, i0.o, i0.xi, n, a.spec, a.opt, a.quad, k0);
+      ld_grad_inputs(i1.gb, i1.s, i1.o, i1.xi, n, a.spec, a.opt, a.quad, k1);
+    }
+    mbar_wait(&bars[s], parity);
+    const T* src = stage + (uint64_t)s * TILE + (uint64_t)threadIdx.x * W;
+    Vec<T> t0, t1;
+    t0.u = *reinterpret_cast<const uint4*>(src);
+    t1.u = *reinterpret_cast<const uint4*>(src + (uint64_t)kBlock * W);
+#pragma unroll
+    for (int l = 0; l < W; ++l) {
+      i0.xj.v[l] = t0.t[l];
+      i1.xj.v[l] = t1.t[l];
+    }
+    __syncthreads();  // stage s consumed by every thread
+    if (threadIdx.x == 0) {
+      const uint64_t nxt = blockIdx.x + (j + kStStages) * gridDim.x;
+      if (nxt < nt) {
+        mbar_expect_tx(&bars[s], TB);
+        bulk_g2s(stage + (uint64_t)s * TILE, n.partner + nxt * TILE, TB, &bars[s]);
+      }
+    }
+    step_store<T, MODE, true>(a, n, k0, i0, norm, nacc);
+    step_store<T, MODE, true>(a, n, k1, i1, norm, nacc);
+  }
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t kk = nt * TILE + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; kk < a.d;
+       kk += stride)
+    step_group<T, MODE, false>(a, n, kk, norm, nacc);
+  block_add_double(nacc, n.norm);
+  block_signal(a.signal);
+}
+
+template <typename T, int MODE>
+cudaError_t launch_step_tma(const StepArgs<T>& a, cudaStream_t s) {
+  const size_t smem = 128 + (size_t)kStStages * st_tile<T>() * sizeof(T);
+  static int resident = 0;
+  if (!resident) {
+    cudaFuncSetAttribute(k_step_tma<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_step_tma<T, MODE>, kBlock, smem);
+    if (resident < 1) resident = 1;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t tiles = a.d / st_tile<T>();
+  uint32_t g = (uint32_t)sms * (uint32_t)resident;
+  if (tiles < g) g = (uint32_t)(tiles ? tiles : 1);
+  k_step_tma<T, MODE><<<g, kBlock, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t launch_step(int mode, const StepArgs<T>& a, int vec, uint32_t grid, cudaStream_t s) {
+  // one node whose partner is a peer GPU: stage the NVLink stream in smem
+  if (a.tma_partner && vec && a.n_local == 1 && a.blocks_per_node == grid) {
+    if (mode == kModePull) return launch_step_tma<T, kModePull>(a, s);
+    if (mode == kModeStale) return launch_step_tma<T, kModeStale>(a, s);
+    if (mode == kModeMix) return launch_step_tma<T, kModeMix>(a, s);
+  }
 #define DSGD_STEP_CASE(M)                                                   \
   case M:                                                                   \
     if (vec)                                                                \
@@ -375,172 +482,68 @@ cudaError_t launch_ar_reduce(const ArReduceArgs<T>& a, uint32_t grid, cudaStream
   return cudaGetLastError();
 }
 
-// ------------------------------------ one-kernel multi-GPU all-reduce round
+// ------------------------------------------------ reference ring chunking
 __device__ __forceinline__ uint32_t ring_chunk_of(uint64_t k, uint64_t base, uint64_t rem) {
   const uint64_t big = rem * (base + 1);  // chunks 0..rem-1 have base+1 elements
   if (k < big) return (uint32_t)(k / (base + 1));
   return (uint32_t)(rem + (k - big) / base);
 }
 
-// A-role work on [lo, hi) of one segment (lo, hi multiples of W when VEC).
-template <typename T, bool VEC>
-__device__ __forceinline__ void arf_a_group(const ArFusedArgs<T>& a, uint64_t k, bool norm,
-                                            double& nacc) {
-  using L = Lanes<T, VEC>;
-  constexpr int W = L::W;
-  const NodeIO<T>& n = a.node;
-  L x, ax, dp, gb, s, o, xi, ot, od;
-  ld(x, n.theta_in, k);
-  if (a.pending) {
-    ld(ax, n.partner, k);
-    if (a.agg)
-      dp = ax;
-    else
-      ld(dp, n.delta, k);
+// ------------------------------------------------ NVLS reduce + broadcast
+__device__ __forceinline__ void fence_proxy_alias() { asm volatile("fence.proxy.alias;" ::: "memory"); }
+
+__device__ __forceinline__ void nvls_group(const float* x, float* y, float inv_div) {
+  float a, b, c, d;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(a), "=f"(b), "=f"(c), "=f"(d)
+               : "l"(x)
+               : "memory");
+  a = __fdiv_rn(a, inv_div);
+  b = __fdiv_rn(b, inv_div);
+  c = __fdiv_rn(c, inv_div);
+  d = __fdiv_rn(d, inv_div);
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(y), "f"(a), "f"(b),
+               "f"(c), "f"(d)
+               : "memory");
+}
+__device__ __forceinline__ void nvls_scalar(const float* x, float* y, float div) {
+  float a;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(a) : "l"(x) : "memory");
+  a = __fdiv_rn(a, div);
+  asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(y), "f"(a) : "memory");
+}
+__device__ __forceinline__ void nvls_scalar(const double* x, double* y, double div) {
+  double a;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f64 %0, [%1];" : "=d"(a) : "l"(x) : "memory");
+  a = __ddiv_rn(a, div);
+  asm volatile("multimem.st.relaxed.sys.global.f64 [%0], %1;" ::"l"(y), "d"(a) : "memory");
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_ar_nvls(const __grid_constant__ ArNvlsArgs<T> a) {
+  if (!block_wait(a.wait)) return;
+  fence_proxy_alias();  // peers wrote x through their unicast mappings
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const T div = T(a.p);
+  if constexpr (sizeof(T) == 4) {
+    // lo is a multiple of 4 elements (16 B): vector body, scalar tail
+    const uint64_t nv = (a.hi - a.lo) / 4;
+    for (uint64_t v = tid; v < nv; v += stride)
+      nvls_group(a.x_mc + a.lo + 4 * v, a.avg_mc + a.lo + 4 * v, div);
+    for (uint64_t k = a.lo + 4 * nv + tid; k < a.hi; k += stride)
+      nvls_scalar(a.x_mc + k, a.avg_mc + k, div);
   } else {
-    ld(dp, n.delta, k);
+    for (uint64_t k = a.lo + tid; k < a.hi; k += stride) nvls_scalar(a.x_mc + k, a.avg_mc + k, div);
   }
-  ld_grad_inputs(gb, s, o, xi, n, a.spec, a.opt, a.quad, k);
-#pragma unroll
-  for (int l = 0; l < W; ++l) {
-    const T x1 = a.pending ? radd(x.v[l], ax.v[l]) : x.v[l];
-    ot.v[l] = x1;
-    od.v[l] = sgd_delta(x1, dp.v[l], gb.v[l], s.v[l], o.v[l], xi.v[l], n.alpha, a.mu, a.wd,
-                        a.mu_nz, a.wd_pos, a.quad, norm, nacc);
-  }
-  if (a.pending) st(n.theta_out, k, ot);
-  st(n.aux, k, od);
-  if (!a.agg || !a.pending) st(n.delta, k, od);
+  fence_proxy_alias();
+  block_signal(a.signal);
 }
 
-// B-role: reference ring fold for each lane (start node = the element's
-// ring chunk), divide by p, write the average to every rank.
-template <typename T, bool VEC, int P>
-__device__ __forceinline__ void arf_b_group(const ArFusedArgs<T>& a, uint64_t k) {
-  using L = Lanes<T, VEC>;
-  constexpr int W = L::W;
-  L v[P];
-#pragma unroll
-  for (int r = 0; r < P; ++r) ld(v[r], a.x[r], k);  // P - 1 NVLink loads in flight
-  L acc;
-  const T pt = T(P);
-#pragma unroll
-  for (int l = 0; l < W; ++l) {
-    const uint32_t c = ring_chunk_of(k + l, a.ring_base, a.ring_rem);
-    T sum = T(0);
-#pragma unroll
-    for (int r = 0; r < P; ++r) {
-      const uint32_t node = c + r >= (uint32_t)P ? c + r - P : c + r;
-      T val = v[0].v[l];  // select v[node] without dynamic register indexing
-#pragma unroll
-      for (int q = 1; q < P; ++q)
-        if (q == (int)node) val = v[q].v[l];
-      sum = r == 0 ? val : radd(sum, val);  // ((x_c + x_c+1) + x_c+2) ...
-    }
-    acc.v[l] = rdiv(sum, pt);
-  }
-#pragma unroll
-  for (int r = 0; r < P; ++r) st(a.avg[r], k, acc);
-}
-
-__device__ __forceinline__ void arf_publish(unsigned int* cnt, unsigned int total,
-                                            unsigned long long* flag, unsigned long long val) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned prev = atomicAdd(cnt, 1u);
-    if (prev == total - 1) {
-      atomicExch(cnt, 0u);
-      __threadfence_system();
-      st_release_sys(flag, val);
-    }
-  }
-}
-
-template <typename T, bool VEC, int P>
-__global__ void __launch_bounds__(kBlock, 4) k_ar_fused(const __grid_constant__ ArFusedArgs<T> a) {
-  __shared__ int ok;
-  constexpr uint64_t W = Lanes<T, VEC>::W;
-  const bool is_a = blockIdx.x < a.grid_a;
-  const uint32_t role_b = is_a ? blockIdx.x : blockIdx.x - a.grid_a;
-  const uint32_t role_n = is_a ? a.grid_a : gridDim.x - a.grid_a;
-  const uint64_t tid = (uint64_t)role_b * blockDim.x + threadIdx.x;
-  const uint64_t stride = (uint64_t)role_n * blockDim.x;
-  const bool norm = a.node.norm != nullptr;
-  double nacc = 0.0;
-  for (uint32_t sg = 0; sg < a.n_seg; ++sg) {
-    const uint64_t lo = (uint64_t)sg * a.seg_len;
-    const uint64_t hi = lo + a.seg_len < a.d ? lo + a.seg_len : a.d;
-    if (is_a) {
-      // RAW on avg / WAR on x of this segment: every rank averaged round t-1
-      if (threadIdx.x == 0) {
-        int good = 1;
-        for (uint32_t r = 0; r < a.p && good; ++r)
-          good = wait_flag(&a.flags[r]->b_done[sg], a.t, a.timeout_ns, a.error);
-        ok = good;
-      }
-      __syncthreads();
-      if (!ok) return;
-      const uint64_t nv = (hi - lo) / W;
-      for (uint64_t v = tid; v < nv; v += stride) arf_a_group<T, VEC>(a, lo + v * W, norm, nacc);
-      for (uint64_t k = lo + nv * W + tid; k < hi; k += stride)
-        arf_a_group<T, false>(a, k, norm, nacc);
-      arf_publish(&a.arrive->a_cnt[sg], role_n, &a.flags[a.rank]->a_done[sg], a.t + 1);
-    } else {
-      if (threadIdx.x == 0) {
-        int good = 1;
-        for (uint32_t r = 0; r < a.p && good; ++r)
-          good = wait_flag(&a.flags[r]->a_done[sg], a.t + 1, a.timeout_ns, a.error);
-        ok = good;
-      }
-      __syncthreads();
-      if (!ok) return;
-      // this rank's share of the segment
-      const uint64_t n = hi - lo;
-      const uint64_t per = (n / a.p + W - 1) / W * W;
-      const uint64_t mlo = lo + per * a.rank < hi ? lo + per * a.rank : hi;
-      const uint64_t mhi = mlo + per < hi ? mlo + per : hi;
-      const uint64_t nv = (mhi - mlo) / W;
-      for (uint64_t v = tid; v < nv; v += stride) arf_b_group<T, VEC, P>(a, mlo + v * W);
-      for (uint64_t k = mlo + nv * W + tid; k < mhi; k += stride) arf_b_group<T, false, P>(a, k);
-      arf_publish(&a.arrive->b_cnt[sg], role_n, &a.flags[a.rank]->b_done[sg], a.t + 1);
-    }
-  }
-  if (!is_a) arf_publish(&a.arrive->b_all_cnt, role_n, &a.flags[a.rank]->b_all, a.t + 1);
-  if (is_a) block_add_double(nacc, a.node.norm);
-}
-
-template <typename T, int P>
-cudaError_t launch_ar_fused_p(const ArFusedArgs<T>& a, int vec, uint32_t grid, cudaStream_t s) {
-  if (vec)
-    k_ar_fused<T, true, P><<<grid, kBlock, 0, s>>>(a);
-  else
-    k_ar_fused<T, false, P><<<grid, kBlock, 0, s>>>(a);
+template <typename T>
+cudaError_t launch_ar_nvls(const ArNvlsArgs<T>& a, uint32_t grid, cudaStream_t s) {
+  k_ar_nvls<T><<<grid, kBlock, 0, s>>>(a);
   return cudaGetLastError();
-}
-
-template <typename T>
-cudaError_t launch_ar_fused(const ArFusedArgs<T>& a, int vec, uint32_t grid, cudaStream_t s) {
-  switch (a.p) {
-    case 2: return launch_ar_fused_p<T, 2>(a, vec, grid, s);
-    case 3: return launch_ar_fused_p<T, 3>(a, vec, grid, s);
-    case 4: return launch_ar_fused_p<T, 4>(a, vec, grid, s);
-    case 5: return launch_ar_fused_p<T, 5>(a, vec, grid, s);
-    case 6: return launch_ar_fused_p<T, 6>(a, vec, grid, s);
-    case 7: return launch_ar_fused_p<T, 7>(a, vec, grid, s);
-    case 8: return launch_ar_fused_p<T, 8>(a, vec, grid, s);
-  }
-  return cudaErrorInvalidValue;
-}
-
-template <typename T>
-int ar_fused_blocks_per_sm(int vec) {
-  int n = 0;  // the P = 8 instantiation bounds the register budget of all P
-  if (vec)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_ar_fused<T, true, 8>, kBlock, 0);
-  else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_ar_fused<T, false, 8>, kBlock, 0);
-  return n;
 }
 
 // ------------------------------------------------ one-shot all-reduce round
@@ -1230,10 +1233,9 @@ cudaError_t launch_fill_normal(T* out, uint64_t n, double sigma, uint64_t seed, 
   template cudaError_t launch_push<T>(const PushArgs<T>&, int, uint32_t, cudaStream_t);            \
   template cudaError_t launch_ea_chain<T>(const EaChainArgs<T>&, int, uint32_t, cudaStream_t);     \
   template cudaError_t launch_ar_reduce<T>(const ArReduceArgs<T>&, uint32_t, cudaStream_t);        \
-  template cudaError_t launch_ar_fused<T>(const ArFusedArgs<T>&, int, uint32_t, cudaStream_t);     \
-  template int ar_fused_blocks_per_sm<T>(int);                                                     \
   template cudaError_t launch_trace<T>(const TraceArgs<T>&, uint32_t, cudaStream_t);               \
   template cudaError_t launch_ar_oneshot<T>(const ArOneShotArgs<T>&, int, uint32_t, cudaStream_t); \
+  template cudaError_t launch_ar_nvls<T>(const ArNvlsArgs<T>&, uint32_t, cudaStream_t);            \
   template cudaError_t launch_spatial_mean<T>(const T* const*, uint32_t, uint64_t, T*,             \
                                               cudaStream_t);                                       \
   template cudaError_t launch_fill_normal<T>(T*, uint64_t, double, uint64_t, uint64_t, cudaStream_t);

@@ -63,6 +63,7 @@ struct StepArgs {
   uint32_t n_local;
   uint32_t blocks_per_node;
   int agg;  // kModeApplyDelta: aggregate momentum scope (delta_prev = the average)
+  int tma_partner;  // stage the (peer-GPU) partner snapshot via bulk async copies
   WaitSpec wait;
   SignalSpec signal;
 };
@@ -84,51 +85,22 @@ struct ArReduceArgs {
   SignalSpec signal;
 };
 
-// One-kernel multi-GPU all-reduce round (p <= kMaxFusedRanks): the grid is
-// persistent (every CTA resident) and split into two roles working through
-// S segments of the vector in a pipeline:
-//   A-role CTAs: (theta += avg of the previous round) + compute_local_delta
-//     -> own exchange buffer x, segment by segment (HBM-bound); the last A
-//     CTA of a segment publishes a_done[s] = t + 1;
-//   B-role CTAs: once every rank published a_done[s], reduce this rank's
-//     share of segment s in the reference ring order and write the average
-//     into every rank's avg buffer (NVLink-bound); publish b_done[s].
-// A-role work of round t+1 on segment s waits for every rank's b_done[s].
-constexpr int kMaxFusedRanks = 8;
-constexpr int kMaxSegments = 64;
+constexpr int kMaxFusedRanks = 8;  // peer-memory all-reduce kernels: p <= 8
 
-struct ArFlags {  // per rank, in the IPC arena
-  unsigned long long a_done[kMaxSegments];
-  unsigned long long b_done[kMaxSegments];
-  unsigned long long b_all;   // rounds whose every segment is averaged (flush waits on it)
-  unsigned long long pad[15];
-};
-struct ArArrive {  // per rank, private
-  unsigned int a_cnt[kMaxSegments];
-  unsigned int b_cnt[kMaxSegments];
-  unsigned int b_all_cnt;
-};
-
+// NVLS reduce + broadcast of this rank's slice [lo, hi) (the second kernel of
+// the two-shot all-reduce round): multimem.ld_reduce on the multicast
+// address of the exchange buffers returns the sum over every GPU, reduced in
+// the NVSwitch; the average is written to every GPU's avg buffer with one
+// multimem.st.  (Summation order is the switch's: tolerance parity, like
+// NCCL.)
 template <typename T>
-struct ArFusedArgs {
-  NodeIO<T> node;                     // aux = own x; partner = own avg (when pending)
-  const T* x[kMaxFusedRanks];
-  T* avg[kMaxFusedRanks];
-  ArFlags* flags[kMaxFusedRanks];
-  ArArrive* arrive;
-  const T* spec;
-  const T* opt;
-  uint64_t d;
-  uint64_t seg_len;                   // multiple of 4
-  uint32_t n_seg;
-  uint32_t p, rank;
-  uint32_t grid_a;                    // CTAs [0, grid_a) are A-role
-  uint64_t ring_base, ring_rem;       // reference ring chunking (transport.cpp:193-198)
-  unsigned long long t;               // round index (flags count rounds)
-  T mu, wd;
-  int mu_nz, wd_pos, quad, agg, pending;
-  unsigned long long timeout_ns;
-  unsigned int* error;
+struct ArNvlsArgs {
+  const T* x_mc;
+  T* avg_mc;
+  uint64_t lo, hi;
+  uint32_t p;
+  WaitSpec wait;
+  SignalSpec signal;
 };
 
 // One-shot multi-GPU all-reduce round (small p): every rank reads every
@@ -239,9 +211,7 @@ cudaError_t launch_ea_chain(const EaChainArgs<T>& a, int vec, uint32_t grid, cud
 template <typename T>
 cudaError_t launch_ar_reduce(const ArReduceArgs<T>& a, uint32_t grid, cudaStream_t s);
 template <typename T>
-cudaError_t launch_ar_fused(const ArFusedArgs<T>& a, int vec, uint32_t grid, cudaStream_t s);
-template <typename T>
-int ar_fused_blocks_per_sm(int vec);
+cudaError_t launch_ar_nvls(const ArNvlsArgs<T>& a, uint32_t grid, cudaStream_t s);
 template <typename T>
 cudaError_t launch_ar_oneshot(const ArOneShotArgs<T>& a, int vec, uint32_t grid, cudaStream_t s);
 template <typename T>

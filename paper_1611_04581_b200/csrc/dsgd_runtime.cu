@@ -91,7 +91,7 @@ struct HandleBlob {
   uint64_t off_x;    // all-reduce exchange buffer (0: none)
   uint64_t off_a;    // all-reduce average buffer
   uint64_t off_ar;   // all-reduce counters: [0] exchange written, [1] average written
-  uint64_t off_arf;  // one-kernel all-reduce segment flags (dsgd::ArFlags)
+  uint64_t off_arf;  // reserved
   uint64_t off_x2;   // second exchange buffer (one-shot all-reduce, round parity)
 };
 static_assert(sizeof(HandleBlob) <= DSGD_HANDLE_BYTES, "handle blob too large");
@@ -105,7 +105,6 @@ struct PeerNode {  // device-addressable view of one node (local or IPC-mapped)
   char* x2 = nullptr;                 // second exchange buffer (one-shot, odd rounds)
   char* avg = nullptr;                // all-reduce average buffer
   unsigned long long* ar = nullptr;   // [0] exchange written, [1] average written (rounds)
-  dsgd::ArFlags* arf = nullptr;       // one-kernel all-reduce segment flags
 };
 
 struct Prof {
@@ -144,14 +143,13 @@ struct dsgd_ctx {
   size_t off_theta[kMaxLocal][2] = {};
   size_t off_c_in = 0, off_flags = 0, off_round = 0, off_x = 0, off_a = 0, off_ar = 0;
   bool p2p_allreduce = true;       // multi-GPU all-reduce over NVLink peer memory (else NCCL)
-  bool ar_fused = false;           // ... as one persistent role-split kernel per round (p <= 8)
   bool ar_oneshot = false;         // ... one-shot: read every peer's exchange buffer (p <= 4)
   bool ar_tma = true;              // ... staging the peer reads through smem (bulk async copies)
+  bool ar_nvls = false;            // ... two-shot with the reduce/broadcast in the NVSwitch
+  char* nvls_x_mc = nullptr;
+  char* nvls_avg_mc = nullptr;
   size_t off_x2 = 0;
-  size_t off_arf = 0;
-  dsgd::ArArrive* ar_arrive = nullptr;
-  uint32_t ar_segments = 16;
-  double ar_a_frac = 0.5;
+
   uint64_t ar_rounds = 0;          // peer-memory all-reduce rounds run
   uint64_t n_chunks = 0;
   uint64_t ea_chunk = 4 * dsgd::kEaChunk;  // elements per EASGD chain flag (DSGD_EA_CHUNK)
@@ -445,6 +443,9 @@ dsgd_status run_step_mode(dsgd_ctx* c, int mode, int kid, const dsgd_hyperparams
   bool vec = all_aligned(c, gs);
   if (partner_of)
     for (uint32_t i = 0; i < c->n_local; ++i) vec = vec && aligned16(a.node[i].partner);
+  // a remote partner (one node per GPU): stage its snapshot through smem
+  a.tma_partner = partner_of && c->distributed() && c->ar_tma &&
+                  partner_of[c->first] != c->first;
   const uint64_t W = vec ? 16 / sizeof(T) : 1;
   a.blocks_per_node = blocks_for(c, (c->d / W + 1) / 2, c->n_local);
   build_waits(c, reads, &a.wait);
@@ -535,8 +536,6 @@ dsgd_status flush_pending_t(dsgd_ctx* c) {
                    : (c->ar_pending_scope == DSGD_SCOPE_PER_NODE ? c->aux[0] : c->delta[0]);
   dsgd::StepArgs<T> a{};
   if (p2p) ar_waits(c, 1, c->ar_rounds, &a.wait);  // every owner wrote its average slice
-  if (p2p && c->ar_fused && c->p <= (uint32_t)dsgd::kMaxFusedRanks)
-    for (int k = 0; k < a.wait.n; ++k) a.wait.ptr[k] = &c->peers[k].arf->b_all;
   a.node[0].theta_in = as<T>(c->theta_ptr(0, c->cur));
   a.node[0].theta_out = as<T>(c->theta_ptr(0, c->cur ^ 1));
   a.node[0].aux = as<T>(xbuf);
@@ -608,52 +607,6 @@ dsgd_status do_allreduce_p2p(dsgd_ctx* c, const dsgd_hyperparams* h, const GradS
     c->prev_readers.clear();
     return DSGD_OK;
   }
-  if (c->ar_fused && c->p <= (uint32_t)dsgd::kMaxFusedRanks) {
-    dsgd::ArFusedArgs<T> a{};
-    fill_node<T>(c, 0, gs, h, &a.node);
-    a.node.aux = as<T>(c->peers[me].x);
-    a.node.partner = fused ? as<T>(c->peers[me].avg) : nullptr;
-    if (fused) a.node.theta_out = as<T>(c->theta_ptr(0, c->cur ^ 1));
-    for (uint32_t k = 0; k < c->p; ++k) {
-      a.x[k] = as<T>(c->peers[k].x);
-      a.avg[k] = as<T>(c->peers[k].avg);
-      a.flags[k] = c->peers[k].arf;
-    }
-    a.arrive = c->ar_arrive;
-    a.spec = gs.quad ? as<T>(c->spec) : nullptr;
-    a.opt = gs.quad ? as<T>(c->opt) : nullptr;
-    a.d = c->d;
-    a.n_seg = std::max<uint32_t>(1, std::min<uint64_t>(c->ar_segments, (c->d + 1023) / 1024));
-    a.seg_len = ((c->d + a.n_seg - 1) / a.n_seg + 3) / 4 * 4;
-    a.n_seg = (uint32_t)((c->d + a.seg_len - 1) / a.seg_len);
-    a.p = c->p;
-    a.rank = me;
-    a.ring_base = c->d / c->p;
-    a.ring_rem = c->d % c->p;
-    a.t = t;
-    a.mu = (T)h->mu;
-    a.wd = (T)h->weight_decay;
-    a.mu_nz = h->mu != 0.0;
-    a.wd_pos = h->weight_decay > 0.0;
-    a.quad = gs.quad;
-    a.agg = scope == DSGD_SCOPE_AGGREGATE;
-    a.pending = fused;
-    a.timeout_ns = c->timeout_ns;
-    a.error = c->error;
-    const bool vec = all_aligned(c, gs);
-    // persistent: every CTA must be resident (B-role CTAs spin on A-role flags)
-    const int occ = std::max(1, std::min(4, dsgd::ar_fused_blocks_per_sm<T>(vec)));
-    const uint32_t grid = (uint32_t)c->sm_count * occ;
-    a.grid_a = std::max<uint32_t>(1, std::min<uint32_t>(grid - 1, (uint32_t)(grid * c->ar_a_frac)));
-    LaunchScope ls(c, DSGD_K_NCCL);
-    DSGD_CUDA(dsgd::launch_ar_fused<T>(a, vec, grid, c->stream));
-    if (fused) c->cur ^= 1;
-    c->ar_rounds = t + 1;
-    c->ar_pending = true;
-    c->ar_pending_scope = scope;
-    c->prev_readers.clear();
-    return DSGD_OK;
-  }
   {
     dsgd::StepArgs<T> a{};
     fill_node<T>(c, 0, gs, h, &a.node[0]);
@@ -674,7 +627,22 @@ dsgd_status do_allreduce_p2p(dsgd_ctx* c, const dsgd_hyperparams* h, const GradS
                                    a.blocks_per_node, c->stream));
   }
   if (fused) c->cur ^= 1;
-  {
+  if (c->ar_nvls) {
+    dsgd::ArNvlsArgs<T> a{};
+    a.x_mc = as<T>(c->nvls_x_mc);
+    a.avg_mc = as<T>(c->nvls_avg_mc);
+    const uint64_t per = ((c->d + c->p - 1) / c->p + 3) / 4 * 4;
+    a.lo = std::min<uint64_t>(c->d, (uint64_t)me * per);
+    a.hi = std::min<uint64_t>(c->d, a.lo + per);
+    a.p = c->p;
+    ar_waits(c, 0, t + 1, &a.wait);
+    a.signal.counter = c->peers[me].ar + 1;
+    a.signal.value = t + 1;
+    a.signal.arrive = c->arrive;
+    const uint32_t grid = blocks_for(c, (a.hi - a.lo) / 4 + 1, 1);
+    LaunchScope ls(c, DSGD_K_NCCL);
+    DSGD_CUDA(dsgd::launch_ar_nvls<T>(a, grid, c->stream));
+  } else {
     dsgd::ArReduceArgs<T> a{};
     for (uint32_t k = 0; k < c->p; ++k) {
       a.x[k] = as<T>(c->peers[k].x);
@@ -973,26 +941,21 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
     off += vb;
     c->off_ar = off;
     off += 256;
-    c->off_arf = off;
-    off += align_up(sizeof(dsgd::ArFlags));
     c->off_x2 = off;
     off += vb;
   }
   c->arena_bytes = off;
   // multi-GPU all-reduce backend: oneshot (default p <= 2), p2p (two-shot,
-  // default p > 2), fused (persistent role-split kernel), nccl
+  // default p > 2), nccl
   {
     std::string mode = c->p <= 2 ? "oneshot" : "p2p";
     if (const char* e = std::getenv("DSGD_ALLREDUCE")) mode = e;
     if (mode == "p2p2k") mode = "p2p";
     c->p2p_allreduce = mode != "nccl";
-    c->ar_fused = mode == "fused";
     c->ar_oneshot = mode == "oneshot" && c->p <= 4;
   }
   if (const char* e = std::getenv("DSGD_AR_TMA")) c->ar_tma = atoi(e) != 0;
-  if (const char* e = std::getenv("DSGD_AR_SEGMENTS"))
-    c->ar_segments = (uint32_t)std::min(dsgd::kMaxSegments, std::max(1, atoi(e)));
-  if (const char* e = std::getenv("DSGD_AR_A_FRAC")) c->ar_a_frac = std::min(0.95, std::max(0.05, atof(e)));
+
   DSGD_CUDA(cudaMalloc(&c->arena, c->arena_bytes));
   DSGD_CUDA(cudaMemset(c->arena, 0, c->arena_bytes));
   for (uint32_t i = 0; i < c->n_local; ++i) {
@@ -1017,10 +980,6 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
   DSGD_CUDA(cudaMallocHost(&c->norm_host, sizeof(double) * kMaxLocal));
   DSGD_CUDA(cudaMalloc(&c->arrive, 256));
   DSGD_CUDA(cudaMemset(c->arrive, 0, 256));
-  if (c->n_local < c->p) {
-    DSGD_CUDA(cudaMalloc(&c->ar_arrive, sizeof(dsgd::ArArrive)));
-    DSGD_CUDA(cudaMemset(c->ar_arrive, 0, sizeof(dsgd::ArArrive)));
-  }
   c->error = c->arrive + 32;
   // local nodes are addressable peers of themselves
   c->peers.resize(c->p);
@@ -1033,7 +992,6 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
       pn.x = c->arena + c->off_x;
       pn.avg = c->arena + c->off_a;
       pn.ar = reinterpret_cast<unsigned long long*>(c->arena + c->off_ar);
-      pn.arf = reinterpret_cast<dsgd::ArFlags*>(c->arena + c->off_arf);
       pn.x2 = c->arena + c->off_x2;
     }
     if (i == 0 && (c->flags & DSGD_CTX_CENTER)) {
@@ -1063,7 +1021,6 @@ void dsgd_ctx_destroy(dsgd_ctx* c) {
   cudaFree(c->norm);
   cudaFreeHost(c->norm_host);
   cudaFree(c->arrive);
-  cudaFree(c->ar_arrive);
   cudaFreeHost(c->staging);
   cudaFree(c->arena);
   for (auto* s : c->partner_streams) dsgd_stream_destroy(s);
@@ -1683,7 +1640,6 @@ dsgd_status dsgd_ctx_export_handle(dsgd_ctx* c, void* blob) {
   b.off_x = c->off_x;
   b.off_a = c->off_a;
   b.off_ar = c->off_ar;
-  b.off_arf = c->off_arf;
   b.off_x2 = c->off_x2;
   std::memset(blob, 0, DSGD_HANDLE_BYTES);
   std::memcpy(blob, &b, sizeof(b));
@@ -1733,7 +1689,6 @@ dsgd_status dsgd_ctx_connect_peers(dsgd_ctx* c, const void* blobs) {
       pn.x = m + b.off_x;
       pn.avg = m + b.off_a;
       pn.ar = reinterpret_cast<unsigned long long*>(m + b.off_ar);
-      pn.arf = reinterpret_cast<dsgd::ArFlags*>(m + b.off_arf);
       pn.x2 = m + b.off_x2;
     }
     if (b.flags & DSGD_CTX_CENTER) {
@@ -1742,6 +1697,24 @@ dsgd_status dsgd_ctx_connect_peers(dsgd_ctx* c, const void* blobs) {
     }
   }
   c->connected = true;
+  return DSGD_OK;
+}
+
+dsgd_status dsgd_ctx_attach_multicast(dsgd_ctx* c, void* x, void* x_mc, void* avg, void* avg_mc) {
+  DSGD_TRY(check_ctx(c));
+  DSGD_TRY(flush_pending(c));
+  if (!c->distributed() || !c->connected)
+    return set_error(DSGD_ESTATE, "multicast all-reduce needs a connected one-node-per-GPU group");
+  if (!x || !x_mc || !avg || !avg_mc) return set_error(DSGD_EINVAL, "null multicast buffer");
+  for (void* q : {x, x_mc, avg, avg_mc})
+    if (!aligned16(q)) return set_error(DSGD_EINVAL, "multicast buffers must be 16-byte aligned");
+  c->peers[c->first].x = static_cast<char*>(x);      // kernel 1 writes here (unicast)
+  c->peers[c->first].avg = static_cast<char*>(avg);  // next round / flush read here
+  c->nvls_x_mc = static_cast<char*>(x_mc);
+  c->nvls_avg_mc = static_cast<char*>(avg_mc);
+  c->p2p_allreduce = true;
+  c->ar_oneshot = false;
+  c->ar_nvls = true;
   return DSGD_OK;
 }
 

@@ -92,7 +92,9 @@ def main():
             if center is not None:
                 cexact = center.astype(npd).tobytes() == oc.tobytes()
             results[proto] = {"bit_exact": exact, "max_rel": rel, "ranks_identical": same_ranks,
-                              "center_exact": cexact}
+                              "center_exact": cexact,
+                              "nvls": getattr(g, "allreduce_backend", "") == "nvls",
+                              "backend": getattr(g, "allreduce_backend", "")}
         dist.barrier()
         g.close()
     if rank == 0:
