@@ -146,6 +146,11 @@ struct dsgd_ctx {
   bool ar_oneshot = false;         // ... one-shot: read every peer's exchange buffer (p <= 4)
   bool ar_tma = true;              // ... staging the peer reads through smem (bulk async copies)
   bool ar_nvls = false;            // ... two-shot with the reduce/broadcast in the NVSwitch
+  uint32_t ar_pipes = 2;           // two-shot: independent pipelines (streams) over d
+  cudaStream_t pipe_stream[4] = {};
+  cudaEvent_t pipe_event[5] = {};  // [0..3] join, [4] fork
+  bool pipes_forked = false;
+  uint32_t ar_pipes_used = 1;      // pipelines of the pending rounds (counters in use)
   char* nvls_x_mc = nullptr;
   char* nvls_avg_mc = nullptr;
   size_t off_x2 = 0;
@@ -225,11 +230,13 @@ cudaEvent_t take_event(dsgd_ctx* c) {
 struct LaunchScope {
   dsgd_ctx* c;
   int id;
+  cudaStream_t st;
   cudaEvent_t a = nullptr;
-  LaunchScope(dsgd_ctx* ctx, int kid) : c(ctx), id(kid) {
+  LaunchScope(dsgd_ctx* ctx, int kid, cudaStream_t on = nullptr)
+      : c(ctx), id(kid), st(on ? on : ctx->stream) {
     if (c->profile) {
       a = take_event(c);
-      cudaEventRecord(a, c->stream);
+      cudaEventRecord(a, st);
     }
   }
   ~LaunchScope() {
@@ -239,7 +246,7 @@ struct LaunchScope {
       c->kernels++;
     if (c->profile) {
       cudaEvent_t b = take_event(c);
-      cudaEventRecord(b, c->stream);
+      cudaEventRecord(b, st);
       c->prof_pending.push_back({id, a, b});
     }
   }
@@ -358,8 +365,11 @@ dsgd_status norm_begin(dsgd_ctx* c, const GradSel& gs) {
   return DSGD_OK;
 }
 
+dsgd_status join_pipes(dsgd_ctx* c);
+
 dsgd_status norm_end(dsgd_ctx* c, const GradSel& gs, const dsgd_grad_spec* g) {
   if (!gs.norm) return DSGD_OK;
+  DSGD_TRY(join_pipes(c));
   DSGD_CUDA(cudaMemcpyAsync(c->norm_host, c->norm, sizeof(double) * c->n_local,
                             cudaMemcpyDeviceToHost, c->stream));
   DSGD_CUDA(cudaStreamSynchronize(c->stream));
@@ -489,6 +499,26 @@ void ar_waits(dsgd_ctx* c, int which, unsigned long long need, dsgd::WaitSpec* w
   }
 }
 
+// Joins the two-shot pipeline streams back into the context stream.
+dsgd_status join_pipes(dsgd_ctx* c) {
+  if (!c->pipes_forked) return DSGD_OK;
+  for (uint32_t h = 0; h < c->ar_pipes; ++h) {
+    DSGD_CUDA(cudaEventRecord(c->pipe_event[h], c->pipe_stream[h]));
+    DSGD_CUDA(cudaStreamWaitEvent(c->stream, c->pipe_event[h], 0));
+  }
+  c->pipes_forked = false;
+  return DSGD_OK;
+}
+
+dsgd_status fork_pipes(dsgd_ctx* c) {
+  if (c->pipes_forked) return DSGD_OK;
+  DSGD_CUDA(cudaEventRecord(c->pipe_event[4], c->stream));
+  for (uint32_t h = 0; h < c->ar_pipes; ++h)
+    DSGD_CUDA(cudaStreamWaitEvent(c->pipe_stream[h], c->pipe_event[4], 0));
+  c->pipes_forked = true;
+  return DSGD_OK;
+}
+
 char* x_of(dsgd_ctx* c, uint32_t k, uint64_t round) {
   return (round & 1) ? c->peers[k].x2 : c->peers[k].x;
 }
@@ -531,11 +561,22 @@ dsgd_status flush_pending_t(dsgd_ctx* c) {
     c->ar_pending = false;
     return DSGD_OK;
   }
+  DSGD_TRY(join_pipes(c));
   const bool p2p = c->p2p_allreduce;
   char* xbuf = p2p ? c->peers[c->first].avg
                    : (c->ar_pending_scope == DSGD_SCOPE_PER_NODE ? c->aux[0] : c->delta[0]);
   dsgd::StepArgs<T> a{};
-  if (p2p) ar_waits(c, 1, c->ar_rounds, &a.wait);  // every owner wrote its average slice
+  if (p2p) {  // every owner wrote its average slice, in every pipeline
+    a.wait.n = 0;
+    a.wait.timeout_ns = c->timeout_ns;
+    a.wait.error = c->error;
+    for (uint32_t h = 0; h < c->ar_pipes_used; ++h)
+      for (uint32_t k = 0; k < c->p && a.wait.n < kMaxWait; ++k) {
+        a.wait.ptr[a.wait.n] = c->peers[k].ar + 2 * h + 1;
+        a.wait.val[a.wait.n] = c->ar_rounds;
+        a.wait.n++;
+      }
+  }
   a.node[0].theta_in = as<T>(c->theta_ptr(0, c->cur));
   a.node[0].theta_out = as<T>(c->theta_ptr(0, c->cur ^ 1));
   a.node[0].aux = as<T>(xbuf);
@@ -607,61 +648,101 @@ dsgd_status do_allreduce_p2p(dsgd_ctx* c, const dsgd_hyperparams* h, const GradS
     c->prev_readers.clear();
     return DSGD_OK;
   }
-  {
-    dsgd::StepArgs<T> a{};
-    fill_node<T>(c, 0, gs, h, &a.node[0]);
-    a.node[0].aux = as<T>(c->peers[me].x);
-    a.node[0].partner = fused ? as<T>(c->peers[me].avg) : nullptr;
-    fill_common(c, h, gs, &a);
-    a.agg = scope == DSGD_SCOPE_AGGREGATE;
-    a.n_local = 1;
-    const bool vec = all_aligned(c, gs);
-    const uint64_t W = vec ? 16 / sizeof(T) : 1;
-    a.blocks_per_node = blocks_for(c, (c->d / W + 1) / 2, 1);
-    ar_waits(c, 1, t, &a.wait);
-    a.signal.counter = c->peers[me].ar + 0;
-    a.signal.value = t + 1;
-    a.signal.arrive = c->arrive;
-    LaunchScope ls(c, DSGD_K_AR_DELTA);
-    DSGD_CUDA(dsgd::launch_step<T>(fused ? dsgd::kModeApplyDelta : dsgd::kModeArDelta, a, vec,
-                                   a.blocks_per_node, c->stream));
+  // K independent pipelines over d, one stream each: pipeline h's NVLink-bound
+  // reduce overlaps pipeline h'`s HBM-bound delta kernel.
+  if (t == 0) {  // the split is fixed for the context's lifetime (counters per pipeline)
+    uint32_t k0 = c->ar_pipes;
+    if (c->d < 65536 || k0 * c->p > (uint32_t)kMaxWait) k0 = 1;
+    c->ar_pipes_used = k0;
+  }
+  const uint32_t K = c->ar_pipes_used;
+  if (K > 1) DSGD_TRY(fork_pipes(c));
+  const bool vec = all_aligned(c, gs);
+  const uint64_t W = vec ? 16 / sizeof(T) : 1;
+  for (uint32_t pi = 0; pi < K; ++pi) {
+    cudaStream_t st = K > 1 ? c->pipe_stream[pi] : c->stream;
+    const uint64_t b0 = (c->d * pi / K) / 64 * 64;
+    const uint64_t b1 = pi + 1 == K ? c->d : (c->d * (pi + 1) / K) / 64 * 64;
+    const uint64_t len = b1 - b0;
+    unsigned int* arrive = c->arrive + 40 + pi;  // per pipeline: kernels run concurrently
+    {
+      dsgd::StepArgs<T> a{};
+      fill_node<T>(c, 0, gs, h, &a.node[0]);
+      dsgd::NodeIO<T>& n = a.node[0];
+      n.theta_in += b0;
+      n.theta_out += b0;
+      n.delta += b0;
+      if (n.grad) n.grad += b0;
+      if (n.noise) n.noise += b0;
+      n.nbase = b0;
+      n.aux = as<T>(c->peers[me].x) + b0;
+      n.partner = fused ? as<T>(c->peers[me].avg) + b0 : nullptr;
+      fill_common(c, h, gs, &a);
+      if (a.spec) a.spec += b0;
+      if (a.opt) a.opt += b0;
+      a.d = len;
+      a.agg = scope == DSGD_SCOPE_AGGREGATE;
+      a.n_local = 1;
+      a.blocks_per_node = std::max<uint32_t>(1, blocks_for(c, (len / W + 1) / 2, 1) / K);
+      a.wait.n = 0;
+      a.wait.timeout_ns = c->timeout_ns;
+      a.wait.error = c->error;
+      for (uint32_t k = 0; k < c->p; ++k) {  // every rank averaged this pipeline's round t-1
+        a.wait.ptr[a.wait.n] = c->peers[k].ar + 2 * pi + 1;
+        a.wait.val[a.wait.n] = t;
+        a.wait.n++;
+      }
+      a.signal.counter = c->peers[me].ar + 2 * pi;
+      a.signal.value = t + 1;
+      a.signal.arrive = arrive;
+      LaunchScope ls(c, DSGD_K_AR_DELTA, st);
+      DSGD_CUDA(dsgd::launch_step<T>(fused ? dsgd::kModeApplyDelta : dsgd::kModeArDelta, a, vec,
+                                     a.blocks_per_node, st));
+    }
+    dsgd::WaitSpec wx{};
+    wx.timeout_ns = c->timeout_ns;
+    wx.error = c->error;
+    for (uint32_t k = 0; k < c->p; ++k) {  // every rank's exchange of this pipeline is written
+      wx.ptr[wx.n] = c->peers[k].ar + 2 * pi;
+      wx.val[wx.n] = t + 1;
+      wx.n++;
+    }
+    dsgd::SignalSpec sx{c->peers[me].ar + 2 * pi + 1, t + 1, arrive};
+    if (c->ar_nvls) {
+      dsgd::ArNvlsArgs<T> a{};
+      a.x_mc = as<T>(c->nvls_x_mc);
+      a.avg_mc = as<T>(c->nvls_avg_mc);
+      const uint64_t per = ((len + c->p - 1) / c->p + 3) / 4 * 4;
+      a.lo = std::min<uint64_t>(b1, b0 + (uint64_t)me * per);
+      a.hi = std::min<uint64_t>(b1, a.lo + per);
+      a.p = c->p;
+      a.wait = wx;
+      a.signal = sx;
+      const uint32_t grid = std::max<uint32_t>(1, blocks_for(c, (a.hi - a.lo) / 4 + 1, 1) / K);
+      LaunchScope ls(c, DSGD_K_NCCL, st);
+      DSGD_CUDA(dsgd::launch_ar_nvls<T>(a, grid, st));
+    } else {
+      dsgd::ArReduceArgs<T> a{};
+      for (uint32_t k = 0; k < c->p; ++k) {
+        a.x[k] = as<T>(c->peers[k].x);
+        a.avg[k] = as<T>(c->peers[k].avg);
+      }
+      a.p = c->p;
+      a.slice = me;
+      const uint64_t base = c->d / c->p, rem = c->d % c->p;  // transport.cpp:193-198
+      const uint64_t clo = (uint64_t)me * base + std::min<uint64_t>(me, rem);
+      const uint64_t chi = clo + base + (me < rem ? 1 : 0);
+      a.lo = std::max(clo, b0);  // my ring chunk within this pipeline's range
+      a.hi = std::max(a.lo, std::min(chi, b1));
+      a.wait = wx;
+      a.signal = sx;
+      const uint32_t grid =
+          std::max<uint32_t>(1, blocks_for(c, (a.hi - a.lo) / (16 / sizeof(T)) + 1, 1) / K);
+      LaunchScope ls(c, DSGD_K_NCCL, st);
+      DSGD_CUDA(dsgd::launch_ar_reduce<T>(a, grid, st));
+    }
   }
   if (fused) c->cur ^= 1;
-  if (c->ar_nvls) {
-    dsgd::ArNvlsArgs<T> a{};
-    a.x_mc = as<T>(c->nvls_x_mc);
-    a.avg_mc = as<T>(c->nvls_avg_mc);
-    const uint64_t per = ((c->d + c->p - 1) / c->p + 3) / 4 * 4;
-    a.lo = std::min<uint64_t>(c->d, (uint64_t)me * per);
-    a.hi = std::min<uint64_t>(c->d, a.lo + per);
-    a.p = c->p;
-    ar_waits(c, 0, t + 1, &a.wait);
-    a.signal.counter = c->peers[me].ar + 1;
-    a.signal.value = t + 1;
-    a.signal.arrive = c->arrive;
-    const uint32_t grid = blocks_for(c, (a.hi - a.lo) / 4 + 1, 1);
-    LaunchScope ls(c, DSGD_K_NCCL);
-    DSGD_CUDA(dsgd::launch_ar_nvls<T>(a, grid, c->stream));
-  } else {
-    dsgd::ArReduceArgs<T> a{};
-    for (uint32_t k = 0; k < c->p; ++k) {
-      a.x[k] = as<T>(c->peers[k].x);
-      a.avg[k] = as<T>(c->peers[k].avg);
-    }
-    a.p = c->p;
-    a.slice = me;
-    const uint64_t base = c->d / c->p, rem = c->d % c->p;  // transport.cpp:193-198
-    a.lo = (uint64_t)me * base + std::min<uint64_t>(me, rem);
-    a.hi = a.lo + base + (me < rem ? 1 : 0);
-    ar_waits(c, 0, t + 1, &a.wait);
-    a.signal.counter = c->peers[me].ar + 1;
-    a.signal.value = t + 1;
-    a.signal.arrive = c->arrive;
-    const uint64_t n = a.hi - a.lo;
-    const uint32_t grid = blocks_for(c, n / (16 / sizeof(T)) + 1, 1);
-    LaunchScope ls(c, DSGD_K_NCCL);
-    DSGD_CUDA(dsgd::launch_ar_reduce<T>(a, grid, c->stream));
-  }
   c->ar_rounds = t + 1;
   c->ar_pending = true;
   c->ar_pending_scope = scope;
@@ -955,6 +1036,7 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
     c->ar_oneshot = mode == "oneshot" && c->p <= 4;
   }
   if (const char* e = std::getenv("DSGD_AR_TMA")) c->ar_tma = atoi(e) != 0;
+  if (const char* e = std::getenv("DSGD_AR_PIPES")) c->ar_pipes = (uint32_t)std::min(4, std::max(1, atoi(e)));
 
   DSGD_CUDA(cudaMalloc(&c->arena, c->arena_bytes));
   DSGD_CUDA(cudaMemset(c->arena, 0, c->arena_bytes));
@@ -980,6 +1062,12 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
   DSGD_CUDA(cudaMallocHost(&c->norm_host, sizeof(double) * kMaxLocal));
   DSGD_CUDA(cudaMalloc(&c->arrive, 256));
   DSGD_CUDA(cudaMemset(c->arrive, 0, 256));
+  if (c->n_local < c->p) {
+    for (int h = 0; h < 4; ++h)
+      DSGD_CUDA(cudaStreamCreateWithFlags(&c->pipe_stream[h], cudaStreamNonBlocking));
+    for (int h = 0; h < 5; ++h)
+      DSGD_CUDA(cudaEventCreateWithFlags(&c->pipe_event[h], cudaEventDisableTiming));
+  }
   c->error = c->arrive + 32;
   // local nodes are addressable peers of themselves
   c->peers.resize(c->p);
@@ -1031,6 +1119,13 @@ void dsgd_ctx_destroy(dsgd_ctx* c) {
     cudaEventDestroy(p.b);
   }
   for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
+  for (int h = 0; h < 4; ++h)
+    if (c->pipe_stream[h]) {
+      cudaStreamSynchronize(c->pipe_stream[h]);
+      cudaStreamDestroy(c->pipe_stream[h]);
+    }
+  for (int h = 0; h < 5; ++h)
+    if (c->pipe_event[h]) cudaEventDestroy(c->pipe_event[h]);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -1044,6 +1139,7 @@ dsgd_status dsgd_ctx_stream(dsgd_ctx* c, void** stream) {
 dsgd_status dsgd_ctx_sync(dsgd_ctx* c) {
   DSGD_TRY(check_ctx(c));
   DeviceGuard g(c->device);
+  DSGD_TRY(join_pipes(c));
   DSGD_CUDA(cudaStreamSynchronize(c->stream));
   unsigned int err = 0;
   DSGD_CUDA(cudaMemcpy(&err, c->error, sizeof(err), cudaMemcpyDeviceToHost));
