@@ -464,7 +464,33 @@ def run_extras_dist(args, world, rank, local, h, max_over_ranks, barrier):
             grp.sync()
             torch.cuda.synchronize()
             ms = max_over_ranks(e0.elapsed_time(e1)) / k
-            out[name] = {"ms_per_round": ms, "param_updates_per_s": world * d / (ms * 1e-3)}
+            hbm, _ = peaks()
+            nv = 770.0
+            if proto == N.PULL_GOSSIP:
+                # the rounds' partner maps (same reference streams as the run):
+                # GPU i reads 4 B/param from its partner and serves 4 B/param to
+                # each remote puller; bound per round = slowest GPU's NVLink / HBM
+                from paper_1611_04581_b200.engine import Stream, draw_pull_partners
+                st = [Stream.make(1, "run/trial0", i, "partner-choice") for i in range(world)]
+                t_bound = 0.0
+                for r in range(3 + k):
+                    pm = draw_pull_partners(st) if r > 0 else list(range(world))
+                    if r < 3:
+                        continue
+                    worst = 0.0
+                    for i in range(world):
+                        pullers = sum(1 for q in range(world) if pm[q] == i and q != i)
+                        nin = 4 * d if pm[i] != i else 0
+                        t_nv = max(nin, 4 * d * pullers) / (nv * 1e9)
+                        t_hbm = (20 + 4 * pullers) * d / (hbm * 1e9)
+                        worst = max(worst, t_nv, t_hbm)
+                    t_bound += worst
+                bound_ms = t_bound / k * 1e3
+            else:
+                # chain: every rank 24 B/param HBM + 4 B/param center over NVLink
+                bound_ms = max(24 * d / (hbm * 1e9), 4 * d / (nv * 1e9)) * 1e3
+            out[name] = {"ms_per_round": ms, "param_updates_per_s": world * d / (ms * 1e-3),
+                         "roofline_ms_per_round": bound_ms, "frac_of_roofline": bound_ms / ms}
             barrier()
             grp.close()
             del pool

@@ -324,6 +324,10 @@ typedef enum {
 dsgd_status dsgd_profile_enable(dsgd_ctx* ctx, int enable);
 dsgd_status dsgd_profile_read(dsgd_ctx* ctx, dsgd_kernel_id k, double* total_ms,
                               uint64_t* launches, int reset);
+/* DSGD_TRACE=<n> (environment) records up to n launches of the multi-GPU
+ * kernels: 5 u64 per record {kernel id (+16 * pipeline), round, %globaltimer
+ * at entry, after the cross-GPU wait, when the last CTA signalled}. */
+dsgd_status dsgd_trace_dump(dsgd_ctx* ctx, uint64_t* out, uint32_t max_records, uint32_t* n);
 /* Number of kernels (and NCCL calls) this context has launched. */
 dsgd_status dsgd_launch_count(dsgd_ctx* ctx, uint64_t* kernels, uint64_t* nccl_calls);
 

@@ -137,6 +137,7 @@ _SIGS = {
     "dsgd_profile_enable": (C.c_int, [_P, C.c_int]),
     "dsgd_profile_read": (C.c_int, [_P, C.c_int, _DP, _U64P, C.c_int]),
     "dsgd_launch_count": (C.c_int, [_P, _U64P, _U64P]),
+    "dsgd_trace_dump": (C.c_int, [_P, _U64P, C.c_uint32, C.POINTER(C.c_uint32)]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -71,12 +71,14 @@ struct WaitSpec {
   int n;
   unsigned long long timeout_ns;
   unsigned int* error;
+  unsigned long long* trace;    // DSGD_TRACE: [0] entry, [1] after the wait (CTA 0)
 };
 
 struct SignalSpec {
   unsigned long long* counter;  // own round counter (IPC-visible); null: no signal
   unsigned long long value;
   unsigned int* arrive;         // grid arrival counter (own device memory)
+  unsigned long long* trace;    // DSGD_TRACE: [2] last CTA done
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
@@ -113,12 +115,18 @@ __device__ __forceinline__ bool wait_flag(const unsigned long long* p, unsigned 
 }
 
 __device__ __forceinline__ bool block_wait(const WaitSpec& w) {
-  if (w.n == 0) return true;
+  const bool tr = w.trace && blockIdx.x == 0 && threadIdx.x == 0;
+  if (tr) w.trace[0] = globaltimer();
+  if (w.n == 0) {
+    if (tr) w.trace[1] = globaltimer();
+    return true;
+  }
   __shared__ int ok;
   if (threadIdx.x == 0) {
     int good = 1;
     for (int i = 0; i < w.n && good; ++i) good = wait_flag(w.ptr[i], w.val[i], w.timeout_ns, w.error);
     ok = good;
+    if (tr) w.trace[1] = globaltimer();
   }
   __syncthreads();
   return ok != 0;
@@ -137,6 +145,7 @@ __device__ __forceinline__ void block_signal(const SignalSpec& s) {
       atomicExch(s.arrive, 0u);
       __threadfence_system();
       st_release_sys(s.counter, s.value);
+      if (s.trace) s.trace[2] = globaltimer();
     }
   }
 }

@@ -6,6 +6,8 @@
 // grid sized to the SM count, every reference pass of a round fused into one
 // sweep over HBM.  The per-element arithmetic is written once (sgd_delta,
 // mix) in the reference's exact operation order; see dsgd_device.cuh.
+#include <cstdlib>
+
 #include "dsgd_kernels.cuh"
 
 namespace dsgd {
@@ -843,9 +845,168 @@ __global__ void __launch_bounds__(kBlock) k_allreduce_local(const __grid_constan
     for (uint32_t i = 0; i < a.p; ++i) block_add_double(nacc[i], a.node[i].norm);
 }
 
+// p = 1 round with every input stream (theta, delta, gradient or s/opt,
+// noise) staged through shared memory by cp.async.bulk, kLtStages tiles
+// ahead: the HBM read stream's bytes in flight cost no registers.
+constexpr int kLtStages = 3;
+template <typename T>
+__host__ __device__ constexpr uint64_t lt_tile() {
+  return (uint64_t)kBlock * Vec<T>::N * 2;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_local_tma(const __grid_constant__ AllreduceArgs<T> a,
+                                                      int nstreams) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr uint64_t TILE = lt_tile<T>();
+  constexpr uint32_t TB = (uint32_t)(TILE * sizeof(T));
+  constexpr int W = Vec<T>::N;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
+  T* stage = reinterpret_cast<T*>(smem_raw + 128);
+  const NodeIO<T>& n = a.node[0];
+  const T* src[5];
+  int ns = 0;
+  src[ns++] = n.theta_in;
+  src[ns++] = n.delta;
+  if (a.quad) {
+    src[ns++] = a.spec;
+    src[ns++] = a.opt;
+  } else {
+    src[ns++] = n.grad;
+  }
+  if (n.noise) src[ns++] = n.noise;
+  (void)nstreams;
+  const uint64_t nt = a.d / TILE;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kLtStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+    for (int s = 0; s < kLtStages; ++s) {
+      const uint64_t tile = blockIdx.x + (uint64_t)s * gridDim.x;
+      if (tile < nt) {
+        mbar_expect_tx(&bars[s], TB * ns);
+        for (int q = 0; q < ns; ++q)
+          bulk_g2s(stage + ((uint64_t)s * 5 + q) * TILE, src[q] + tile * TILE, TB, &bars[s]);
+      }
+    }
+  }
+  __syncthreads();
+  for (uint64_t j = 0;; ++j) {
+    const uint64_t tile = blockIdx.x + j * gridDim.x;
+    if (tile >= nt) break;
+    const int s = (int)(j % kLtStages);
+    mbar_wait(&bars[s], (uint32_t)((j / kLtStages) & 1));
+    Lanes<T, true> x[2], dp[2], gb[2], sp[2], o[2], xi[2];
+    const T* base = stage + (uint64_t)s * 5 * TILE + (uint64_t)threadIdx.x * W;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint64_t off = (uint64_t)u * kBlock * W;
+      Vec<T> v;
+      v.u = *reinterpret_cast<const uint4*>(base + off);
+#pragma unroll
+      for (int l = 0; l < W; ++l) x[u].v[l] = v.t[l];
+      v.u = *reinterpret_cast<const uint4*>(base + TILE + off);
+#pragma unroll
+      for (int l = 0; l < W; ++l) dp[u].v[l] = v.t[l];
+      int q = 2;
+      if (a.quad) {
+        v.u = *reinterpret_cast<const uint4*>(base + q * TILE + off);
+#pragma unroll
+        for (int l = 0; l < W; ++l) sp[u].v[l] = v.t[l];
+        v.u = *reinterpret_cast<const uint4*>(base + (q + 1) * TILE + off);
+#pragma unroll
+        for (int l = 0; l < W; ++l) o[u].v[l] = v.t[l];
+        q += 2;
+      } else {
+        v.u = *reinterpret_cast<const uint4*>(base + q * TILE + off);
+#pragma unroll
+        for (int l = 0; l < W; ++l) gb[u].v[l] = v.t[l];
+        q += 1;
+      }
+      if (n.noise) {
+        v.u = *reinterpret_cast<const uint4*>(base + q * TILE + off);
+#pragma unroll
+        for (int l = 0; l < W; ++l) xi[u].v[l] = v.t[l];
+      } else if (n.nsigma != T(0)) {
+        float z[W];
+        dev_normals<W>(n.nkey, n.nctr, n.nbase + tile * TILE + (uint64_t)threadIdx.x * W + off, z);
+#pragma unroll
+        for (int l = 0; l < W; ++l) xi[u].v[l] = rmul(n.nsigma, (T)z[l]);
+      } else {
+#pragma unroll
+        for (int l = 0; l < W; ++l) xi[u].v[l] = T(0);
+      }
+    }
+    __syncthreads();  // stage s consumed
+    if (threadIdx.x == 0) {
+      const uint64_t nxt = blockIdx.x + (j + kLtStages) * gridDim.x;
+      if (nxt < nt) {
+        mbar_expect_tx(&bars[s], TB * ns);
+        for (int q = 0; q < ns; ++q)
+          bulk_g2s(stage + ((uint64_t)s * 5 + q) * TILE, src[q] + nxt * TILE, TB, &bars[s]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint64_t k = tile * TILE + (uint64_t)threadIdx.x * W + (uint64_t)u * kBlock * W;
+      Lanes<T, true> ot, od;
+      double dummy = 0.0;
+#pragma unroll
+      for (int l = 0; l < W; ++l) {
+        const T d0 = sgd_delta(x[u].v[l], dp[u].v[l], gb[u].v[l], sp[u].v[l], o[u].v[l],
+                               xi[u].v[l], n.alpha, a.mu, a.wd, a.mu_nz, a.wd_pos, a.quad, false,
+                               dummy);
+        const T avg = radd(d0, rmul(T(0), a.inv_p));  // spatial_mean of one node (param_vec.cpp:37)
+        ot.v[l] = radd(x[u].v[l], avg);
+        od.v[l] = a.per_node ? d0 : avg;
+      }
+      st(n.theta_out, k, ot);
+      st(n.delta, k, od);
+    }
+  }
+  // ragged tail: the plain kernel's scalar path
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = nt * TILE + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < a.d;
+       k += stride) {
+    Lanes<T, false> x, dp, gb, sp, o, xi;
+    ld(x, n.theta_in, k);
+    ld(dp, n.delta, k);
+    ld_grad_inputs(gb, sp, o, xi, n, a.spec, a.opt, a.quad, k);
+    double dummy = 0.0;
+    const T d0 = sgd_delta(x.v[0], dp.v[0], gb.v[0], sp.v[0], o.v[0], xi.v[0], n.alpha, a.mu,
+                           a.wd, a.mu_nz, a.wd_pos, a.quad, false, dummy);
+    const T avg = radd(d0, rmul(T(0), a.inv_p));
+    n.theta_out[k] = radd(x.v[0], avg);
+    n.delta[k] = a.per_node ? d0 : avg;
+  }
+}
+
+template <typename T>
+cudaError_t launch_local_tma(const AllreduceArgs<T>& a, cudaStream_t s) {
+  const size_t smem = 128 + (size_t)kLtStages * 5 * lt_tile<T>() * sizeof(T);
+  static int resident = 0;
+  if (!resident) {
+    cudaFuncSetAttribute(k_local_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_local_tma<T>, kBlock, smem);
+    if (resident < 1) resident = 1;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t tiles = a.d / lt_tile<T>();
+  uint32_t g = (uint32_t)sms * (uint32_t)resident;
+  if (tiles < g) g = (uint32_t)(tiles ? tiles : 1);
+  k_local_tma<T><<<g, kBlock, smem, s>>>(a, 0);
+  return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t launch_allreduce_local(const AllreduceArgs<T>& a, int vec, int norm, uint32_t grid,
                                    cudaStream_t s) {
+  static const bool tma = [] {
+    const char* e = getenv("DSGD_LOCAL_TMA");
+    return e && e[0] == '1';
+  }();
+  if (tma && a.p == 1 && vec && !norm) return launch_local_tma<T>(a, s);
   // the vector kernel covers d - d % W; a scalar launch finishes the tail
   if (vec) {
     if (norm)

@@ -150,6 +150,11 @@ struct dsgd_ctx {
   cudaStream_t pipe_stream[4] = {};
   cudaEvent_t pipe_event[5] = {};  // [0..3] join, [4] fork
   bool pipes_forked = false;
+  // DSGD_TRACE: per launch {kind, round, %globaltimer entry / after wait / done}
+  unsigned long long* trace_dev = nullptr;
+  uint32_t trace_cap = 0, trace_n = 0;
+  std::vector<uint32_t> trace_kind;
+  std::vector<uint64_t> trace_round;
   uint32_t ar_pipes_used = 1;      // pipelines of the pending rounds (counters in use)
   char* nvls_x_mc = nullptr;
   char* nvls_avg_mc = nullptr;
@@ -399,6 +404,17 @@ dsgd_status check_map(dsgd_ctx* c, const uint32_t* m) {
   return DSGD_OK;
 }
 
+// DSGD_TRACE: give this launch a trace slot (kind = dsgd_kernel_id).
+void trace_slot(dsgd_ctx* c, int kind, dsgd::WaitSpec* w, dsgd::SignalSpec* s) {
+  if (!c->trace_dev || c->trace_n >= c->trace_cap) return;
+  unsigned long long* slot = c->trace_dev + 3ull * c->trace_n;
+  c->trace_kind.push_back((uint32_t)kind);
+  c->trace_round.push_back(c->rounds_done);
+  c->trace_n++;
+  if (w) w->trace = slot;
+  if (s) s->trace = slot;
+}
+
 // Wait list of a multi-GPU round that reads `reads` (the partner, or none)
 // and overwrites the snapshot the previous round's pullers read.
 void build_waits(dsgd_ctx* c, const std::vector<uint32_t>& reads, dsgd::WaitSpec* w) {
@@ -460,6 +476,7 @@ dsgd_status run_step_mode(dsgd_ctx* c, int mode, int kid, const dsgd_hyperparams
   a.blocks_per_node = blocks_for(c, (c->d / W + 1) / 2, c->n_local);
   build_waits(c, reads, &a.wait);
   build_signal(c, &a.signal);
+  trace_slot(c, kid, &a.wait, &a.signal);
   const uint32_t grid = a.blocks_per_node * c->n_local;
   LaunchScope ls(c, kid);
   DSGD_CUDA(dsgd::launch_step<T>(mode, a, vec ? 1 : 0, grid, c->stream));
@@ -635,6 +652,7 @@ dsgd_status do_allreduce_p2p(dsgd_ctx* c, const dsgd_hyperparams* h, const GradS
     a.signal.counter = c->peers[me].ar + 0;
     a.signal.value = t + 1;
     a.signal.arrive = c->arrive;
+    trace_slot(c, DSGD_K_NCCL, &a.wait, &a.signal);
     const bool vec = all_aligned(c, gs);
     const uint64_t W = vec ? 16 / sizeof(T) : 1;
     {
@@ -695,6 +713,7 @@ dsgd_status do_allreduce_p2p(dsgd_ctx* c, const dsgd_hyperparams* h, const GradS
       a.signal.counter = c->peers[me].ar + 2 * pi;
       a.signal.value = t + 1;
       a.signal.arrive = arrive;
+      trace_slot(c, DSGD_K_AR_DELTA + 16 * pi, &a.wait, &a.signal);
       LaunchScope ls(c, DSGD_K_AR_DELTA, st);
       DSGD_CUDA(dsgd::launch_step<T>(fused ? dsgd::kModeApplyDelta : dsgd::kModeArDelta, a, vec,
                                      a.blocks_per_node, st));
@@ -707,7 +726,8 @@ dsgd_status do_allreduce_p2p(dsgd_ctx* c, const dsgd_hyperparams* h, const GradS
       wx.val[wx.n] = t + 1;
       wx.n++;
     }
-    dsgd::SignalSpec sx{c->peers[me].ar + 2 * pi + 1, t + 1, arrive};
+    dsgd::SignalSpec sx{c->peers[me].ar + 2 * pi + 1, t + 1, arrive, nullptr};
+    trace_slot(c, DSGD_K_NCCL + 16 * pi, &wx, &sx);
     if (c->ar_nvls) {
       dsgd::ArNvlsArgs<T> a{};
       a.x_mc = as<T>(c->nvls_x_mc);
@@ -1036,6 +1056,10 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
     c->ar_oneshot = mode == "oneshot" && c->p <= 4;
   }
   if (const char* e = std::getenv("DSGD_AR_TMA")) c->ar_tma = atoi(e) != 0;
+  if (const char* e = std::getenv("DSGD_TRACE")) {
+    c->trace_cap = (uint32_t)std::max(1, atoi(e));
+    if (c->trace_cap < 64) c->trace_cap = 65536;
+  }
   if (const char* e = std::getenv("DSGD_AR_PIPES")) c->ar_pipes = (uint32_t)std::min(4, std::max(1, atoi(e)));
 
   DSGD_CUDA(cudaMalloc(&c->arena, c->arena_bytes));
@@ -1062,6 +1086,10 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
   DSGD_CUDA(cudaMallocHost(&c->norm_host, sizeof(double) * kMaxLocal));
   DSGD_CUDA(cudaMalloc(&c->arrive, 256));
   DSGD_CUDA(cudaMemset(c->arrive, 0, 256));
+  if (c->trace_cap) {
+    DSGD_CUDA(cudaMalloc(&c->trace_dev, sizeof(unsigned long long) * 3 * c->trace_cap));
+    DSGD_CUDA(cudaMemset(c->trace_dev, 0, sizeof(unsigned long long) * 3 * c->trace_cap));
+  }
   if (c->n_local < c->p) {
     for (int h = 0; h < 4; ++h)
       DSGD_CUDA(cudaStreamCreateWithFlags(&c->pipe_stream[h], cudaStreamNonBlocking));
@@ -1109,6 +1137,7 @@ void dsgd_ctx_destroy(dsgd_ctx* c) {
   cudaFree(c->norm);
   cudaFreeHost(c->norm_host);
   cudaFree(c->arrive);
+  cudaFree(c->trace_dev);
   cudaFreeHost(c->staging);
   cudaFree(c->arena);
   for (auto* s : c->partner_streams) dsgd_stream_destroy(s);
@@ -1857,6 +1886,25 @@ dsgd_status dsgd_profile_read(dsgd_ctx* c, dsgd_kernel_id k, double* total_ms, u
     c->prof_ms[k] = 0;
     c->prof_launches[k] = 0;
   }
+  return DSGD_OK;
+}
+
+dsgd_status dsgd_trace_dump(dsgd_ctx* c, uint64_t* out, uint32_t max_records, uint32_t* n) {
+  DSGD_TRY(check_ctx(c));
+  DeviceGuard g(c->device);
+  DSGD_TRY(join_pipes(c));
+  DSGD_CUDA(cudaStreamSynchronize(c->stream));
+  const uint32_t m = std::min(max_records, c->trace_n);
+  std::vector<unsigned long long> buf(3ull * std::max<uint32_t>(1, m));
+  if (m) DSGD_CUDA(cudaMemcpy(buf.data(), c->trace_dev, 24ull * m, cudaMemcpyDeviceToHost));
+  for (uint32_t i = 0; i < m; ++i) {
+    out[5ull * i + 0] = c->trace_kind[i];
+    out[5ull * i + 1] = c->trace_round[i];
+    out[5ull * i + 2] = buf[3ull * i + 0];
+    out[5ull * i + 3] = buf[3ull * i + 1];
+    out[5ull * i + 4] = buf[3ull * i + 2];
+  }
+  *n = m;
   return DSGD_OK;
 }
 

@@ -456,6 +456,14 @@ class Group:
         N.check(self.lib.dsgd_profile_read(self._ctx, kernel, C.byref(ms), C.byref(n), int(reset)))
         return ms.value, n.value
 
+    def trace_dump(self, max_records: int = 65536) -> np.ndarray:
+        """DSGD_TRACE records: [kind, round, t_entry, t_after_wait, t_done] (ns)."""
+        out = np.zeros((max_records, 5), dtype=np.uint64)
+        n = C.c_uint32()
+        N.check(self.lib.dsgd_trace_dump(self._ctx, out.ctypes.data_as(N._U64P), max_records,
+                                         C.byref(n)))
+        return out[:n.value]
+
     def launch_count(self):
         k = C.c_uint64()
         n = C.c_uint64()
