@@ -294,11 +294,8 @@ __global__ void __launch_bounds__(kBlock) k_step(const __grid_constant__ StepArg
   // two independent groups per iteration keep 2x the bytes in flight
   uint64_t v = first;
   for (; v + stride < nv; v += 2 * stride) {
-    StepIn<T, VEC> i0, i1;
-    step_load<T, MODE, VEC>(a, n, v * W, i0);
-    step_load<T, MODE, VEC>(a, n, (v + stride) * W, i1);
-    step_store<T, MODE, VEC>(a, n, v * W, i0, norm, nacc);
-    step_store<T, MODE, VEC>(a, n, (v + stride) * W, i1, norm, nacc);
+    step_group<T, MODE, VEC>(a, n, v * W, norm, nacc);
+    step_group<T, MODE, VEC>(a, n, (v + stride) * W, norm, nacc);
   }
   if (v < nv) step_group<T, MODE, VEC>(a, n, v * W, norm, nacc);
   if constexpr (VEC) {
@@ -508,6 +505,22 @@ __device__ __forceinline__ void nvls_group(const float* x, float* y, float inv_d
                "f"(c), "f"(d)
                : "memory");
 }
+__device__ __forceinline__ void nvls_group4(const float* x, float* y, uint64_t step, float div) {
+  float r[16];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r[4 * u]), "=f"(r[4 * u + 1]), "=f"(r[4 * u + 2]), "=f"(r[4 * u + 3])
+                 : "l"(x + u * step)
+                 : "memory");
+#pragma unroll
+  for (int q = 0; q < 16; ++q) r[q] = __fdiv_rn(r[q], div);
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(y + u * step),
+                 "f"(r[4 * u]), "f"(r[4 * u + 1]), "f"(r[4 * u + 2]), "f"(r[4 * u + 3])
+                 : "memory");
+}
 __device__ __forceinline__ void nvls_scalar(const float* x, float* y, float div) {
   float a;
   asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(a) : "l"(x) : "memory");
@@ -531,7 +544,10 @@ __global__ void __launch_bounds__(kBlock) k_ar_nvls(const __grid_constant__ ArNv
   if constexpr (sizeof(T) == 4) {
     // lo is a multiple of 4 elements (16 B): vector body, scalar tail
     const uint64_t nv = (a.hi - a.lo) / 4;
-    for (uint64_t v = tid; v < nv; v += stride)
+    uint64_t v = tid;
+    for (; v + 3 * stride < nv; v += 4 * stride)  // four switch reductions in flight
+      nvls_group4(a.x_mc + a.lo + 4 * v, a.avg_mc + a.lo + 4 * v, 4 * stride, div);
+    for (; v < nv; v += stride)
       nvls_group(a.x_mc + a.lo + 4 * v, a.avg_mc + a.lo + 4 * v, div);
     for (uint64_t k = a.lo + 4 * nv + tid; k < a.hi; k += stride)
       nvls_scalar(a.x_mc + k, a.avg_mc + k, div);
@@ -999,12 +1015,150 @@ cudaError_t launch_local_tma(const AllreduceArgs<T>& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// Two-shot all-reduce delta kernel (kModeArDelta / kModeApplyDelta) of one
+// node with its input streams staged through shared memory by cp.async.bulk
+// (kLtStages tiles ahead).  Saturates HBM from a fraction of the SMs, so the
+// NVLink-bound reduce of the other pipeline can run on the rest.
+template <typename T, int MODE>
+__global__ void __launch_bounds__(kBlock) k_ard_tma(const __grid_constant__ StepArgs<T> a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr uint64_t TILE = lt_tile<T>();
+  constexpr uint32_t TB = (uint32_t)(TILE * sizeof(T));
+  constexpr int W = Vec<T>::N;
+  constexpr bool PEND = MODE == kModeApplyDelta;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
+  T* stage = reinterpret_cast<T*>(smem_raw + 128);
+  if (!block_wait(a.wait)) return;
+  const NodeIO<T>& n = a.node[0];
+  const bool need_dp = !(PEND && a.agg);
+  const T* src[6];
+  int ns = 0;
+  src[ns++] = n.theta_in;                              // slot 0
+  if (PEND) src[ns++] = n.partner;                     // slot 1: avg of round t-1
+  const int s_dp = ns;
+  if (need_dp) src[ns++] = n.delta;
+  const int s_g = ns;
+  if (a.quad) {
+    src[ns++] = a.spec;
+    src[ns++] = a.opt;
+  } else {
+    src[ns++] = n.grad;
+  }
+  const int s_nz = ns;
+  if (n.noise) src[ns++] = n.noise;
+  const uint64_t nt = a.d / TILE;
+  if (threadIdx.x == 0) {
+    for (int sg = 0; sg < kLtStages; ++sg) mbar_init(&bars[sg], 1);
+    fence_mbar_init();
+    for (int sg = 0; sg < kLtStages; ++sg) {
+      const uint64_t tile = blockIdx.x + (uint64_t)sg * gridDim.x;
+      if (tile < nt) {
+        mbar_expect_tx(&bars[sg], TB * ns);
+        for (int q = 0; q < ns; ++q)
+          bulk_g2s(stage + ((uint64_t)sg * 6 + q) * TILE, src[q] + tile * TILE, TB, &bars[sg]);
+      }
+    }
+  }
+  __syncthreads();
+  const bool norm = n.norm != nullptr;
+  double nacc = 0.0;
+  for (uint64_t j = 0;; ++j) {
+    const uint64_t tile = blockIdx.x + j * gridDim.x;
+    if (tile >= nt) break;
+    const int sg = (int)(j % kLtStages);
+    mbar_wait(&bars[sg], (uint32_t)((j / kLtStages) & 1));
+    const T* base = stage + (uint64_t)sg * 6 * TILE + (uint64_t)threadIdx.x * W;
+    Lanes<T, true> x[2], ax[2], dp[2], gb[2], sp[2], o[2], xi[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint64_t off = (uint64_t)u * kBlock * W;
+      auto rd = [&](int slot, Lanes<T, true>& dst) {
+        Vec<T> v;
+        v.u = *reinterpret_cast<const uint4*>(base + (uint64_t)slot * TILE + off);
+#pragma unroll
+        for (int l = 0; l < W; ++l) dst.v[l] = v.t[l];
+      };
+      rd(0, x[u]);
+      if (PEND) rd(1, ax[u]);
+      if (need_dp) rd(s_dp, dp[u]);
+      if (PEND && a.agg) dp[u] = ax[u];
+      if (a.quad) {
+        rd(s_g, sp[u]);
+        rd(s_g + 1, o[u]);
+      } else {
+        rd(s_g, gb[u]);
+      }
+      if (n.noise) {
+        rd(s_nz, xi[u]);
+      } else if (n.nsigma != T(0)) {
+        float z[W];
+        dev_normals<W>(n.nkey, n.nctr, n.nbase + tile * TILE + (uint64_t)threadIdx.x * W + off, z);
+#pragma unroll
+        for (int l = 0; l < W; ++l) xi[u].v[l] = rmul(n.nsigma, (T)z[l]);
+      } else {
+#pragma unroll
+        for (int l = 0; l < W; ++l) xi[u].v[l] = T(0);
+      }
+    }
+    __syncthreads();  // stage consumed
+    if (threadIdx.x == 0) {
+      const uint64_t nxt = blockIdx.x + (j + kLtStages) * gridDim.x;
+      if (nxt < nt) {
+        mbar_expect_tx(&bars[sg], TB * ns);
+        for (int q = 0; q < ns; ++q)
+          bulk_g2s(stage + ((uint64_t)sg * 6 + q) * TILE, src[q] + nxt * TILE, TB, &bars[sg]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint64_t k = tile * TILE + (uint64_t)threadIdx.x * W + (uint64_t)u * kBlock * W;
+      Lanes<T, true> ot, od;
+#pragma unroll
+      for (int l = 0; l < W; ++l) {
+        const T x1 = PEND ? radd(x[u].v[l], ax[u].v[l]) : x[u].v[l];  // theta += avg
+        ot.v[l] = x1;
+        od.v[l] = sgd_delta(x1, dp[u].v[l], gb[u].v[l], sp[u].v[l], o[u].v[l], xi[u].v[l],
+                            n.alpha, a.mu, a.wd, a.mu_nz, a.wd_pos, a.quad, norm, nacc);
+      }
+      if (PEND) st(n.theta_out, k, ot);
+      st(n.aux, k, od);
+      if (!(PEND && a.agg) && n.aux != n.delta) st(n.delta, k, od);
+    }
+  }
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = nt * TILE + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < a.d;
+       k += stride)
+    step_group<T, MODE, false>(a, n, k, norm, nacc);
+  block_add_double(nacc, n.norm);
+  block_signal(a.signal);
+}
+
+template <typename T>
+cudaError_t launch_ard_tma(int mode, const StepArgs<T>& a, uint32_t grid, cudaStream_t s) {
+  const size_t smem = 128 + (size_t)kLtStages * 6 * lt_tile<T>() * sizeof(T);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_ard_tma<T, kModeArDelta>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    cudaFuncSetAttribute(k_ard_tma<T, kModeApplyDelta>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  const uint64_t tiles = a.d / lt_tile<T>();
+  if (tiles < grid) grid = (uint32_t)(tiles ? tiles : 1);
+  if (mode == kModeApplyDelta)
+    k_ard_tma<T, kModeApplyDelta><<<grid, kBlock, smem, s>>>(a);
+  else
+    k_ard_tma<T, kModeArDelta><<<grid, kBlock, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t launch_allreduce_local(const AllreduceArgs<T>& a, int vec, int norm, uint32_t grid,
                                    cudaStream_t s) {
-  static const bool tma = [] {
+  static const bool tma = [] {  // DSGD_LOCAL_TMA=0 selects the LDG kernel
     const char* e = getenv("DSGD_LOCAL_TMA");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   if (tma && a.p == 1 && vec && !norm) return launch_local_tma<T>(a, s);
   // the vector kernel covers d - d % W; a scalar launch finishes the tail
@@ -1397,6 +1551,7 @@ cudaError_t launch_fill_normal(T* out, uint64_t n, double sigma, uint64_t seed, 
   template cudaError_t launch_trace<T>(const TraceArgs<T>&, uint32_t, cudaStream_t);               \
   template cudaError_t launch_ar_oneshot<T>(const ArOneShotArgs<T>&, int, uint32_t, cudaStream_t); \
   template cudaError_t launch_ar_nvls<T>(const ArNvlsArgs<T>&, uint32_t, cudaStream_t);            \
+  template cudaError_t launch_ard_tma<T>(int, const StepArgs<T>&, uint32_t, cudaStream_t);         \
   template cudaError_t launch_spatial_mean<T>(const T* const*, uint32_t, uint64_t, T*,             \
                                               cudaStream_t);                                       \
   template cudaError_t launch_fill_normal<T>(T*, uint64_t, double, uint64_t, uint64_t, cudaStream_t);

@@ -213,6 +213,8 @@ cudaError_t launch_ar_reduce(const ArReduceArgs<T>& a, uint32_t grid, cudaStream
 template <typename T>
 cudaError_t launch_ar_nvls(const ArNvlsArgs<T>& a, uint32_t grid, cudaStream_t s);
 template <typename T>
+cudaError_t launch_ard_tma(int mode, const StepArgs<T>& a, uint32_t grid, cudaStream_t s);
+template <typename T>
 cudaError_t launch_ar_oneshot(const ArOneShotArgs<T>& a, int vec, uint32_t grid, cudaStream_t s);
 template <typename T>
 cudaError_t launch_trace(const TraceArgs<T>& a, uint32_t grid, cudaStream_t s);

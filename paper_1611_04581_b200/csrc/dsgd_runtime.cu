@@ -147,6 +147,7 @@ struct dsgd_ctx {
   bool ar_tma = true;              // ... staging the peer reads through smem (bulk async copies)
   bool ar_nvls = false;            // ... two-shot with the reduce/broadcast in the NVSwitch
   uint32_t ar_pipes = 2;           // two-shot: independent pipelines (streams) over d
+  double ar_delta_frac = 1.0;      // SMs (x CTA per SM) given to the staged delta kernel
   cudaStream_t pipe_stream[4] = {};
   cudaEvent_t pipe_event[5] = {};  // [0..3] join, [4] fork
   bool pipes_forked = false;
@@ -715,8 +716,15 @@ dsgd_status do_allreduce_p2p(dsgd_ctx* c, const dsgd_hyperparams* h, const GradS
       a.signal.arrive = arrive;
       trace_slot(c, DSGD_K_AR_DELTA + 16 * pi, &a.wait, &a.signal);
       LaunchScope ls(c, DSGD_K_AR_DELTA, st);
-      DSGD_CUDA(dsgd::launch_step<T>(fused ? dsgd::kModeApplyDelta : dsgd::kModeArDelta, a, vec,
-                                     a.blocks_per_node, st));
+      const int mode = fused ? dsgd::kModeApplyDelta : dsgd::kModeArDelta;
+      if (vec && c->ar_tma) {
+        // smem-staged streams: a fraction of the SMs saturates HBM and leaves
+        // the rest to the other pipeline's NVLink reduce
+        const uint32_t g = std::max<uint32_t>(1, (uint32_t)(c->sm_count * c->ar_delta_frac / K));
+        DSGD_CUDA(dsgd::launch_ard_tma<T>(mode, a, g, st));
+      } else {
+        DSGD_CUDA(dsgd::launch_step<T>(mode, a, vec, a.blocks_per_node, st));
+      }
     }
     dsgd::WaitSpec wx{};
     wx.timeout_ns = c->timeout_ns;
@@ -1061,6 +1069,7 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
     if (c->trace_cap < 64) c->trace_cap = 65536;
   }
   if (const char* e = std::getenv("DSGD_AR_PIPES")) c->ar_pipes = (uint32_t)std::min(4, std::max(1, atoi(e)));
+  if (const char* e = std::getenv("DSGD_AR_DELTA_FRAC")) c->ar_delta_frac = std::max(0.05, atof(e));
 
   DSGD_CUDA(cudaMalloc(&c->arena, c->arena_bytes));
   DSGD_CUDA(cudaMemset(c->arena, 0, c->arena_bytes));
