@@ -771,8 +771,144 @@ __global__ void __launch_bounds__(kBlock) k_ar_oneshot_tma(const __grid_constant
   block_signal(a.signal);
 }
 
+// One-shot round with EVERY stream staged through shared memory (every
+// rank's exchange tile + this rank's theta, delta, gradient / s+opt, noise):
+// 3 stages of up to P + 5 8-KB tiles per CTA, registers hold no loads.
+constexpr int kOs2Stages = 3;
+
+template <typename T, int P>
+__global__ void __launch_bounds__(kBlock) k_ar_oneshot_tma2(const __grid_constant__ ArOneShotArgs<T> a,
+                                                            int ns) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr uint64_t TILE = os_tile<T>();
+  constexpr uint32_t TB = (uint32_t)(TILE * sizeof(T));
+  constexpr int W = Vec<T>::N;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
+  T* stage = reinterpret_cast<T*>(smem_raw + 128);
+  if (!block_wait(a.wait)) return;
+  const NodeIO<T>& n = a.node;
+  // slots: [0, P) exchange tiles, then theta, delta (per-node), g | s, opt, noise
+  const T* src[kMaxFusedRanks + 5];
+  int q = 0;
+#pragma unroll
+  for (int r = 0; r < P; ++r) src[q++] = a.x_prev[r];
+  const int s_x = q;
+  src[q++] = n.theta_in;
+  const int s_dp = q;
+  if (!a.agg) src[q++] = n.delta;
+  const int s_g = q;
+  if (a.quad) {
+    src[q++] = a.spec;
+    src[q++] = a.opt;
+  } else {
+    src[q++] = n.grad;
+  }
+  const int s_nz = q;
+  if (n.noise) src[q++] = n.noise;
+  (void)ns;
+  const int nsl = q;
+  const uint64_t nt = a.d / TILE;
+  if (threadIdx.x == 0) {
+    for (int sg = 0; sg < kOs2Stages; ++sg) mbar_init(&bars[sg], 1);
+    fence_mbar_init();
+    for (int sg = 0; sg < kOs2Stages; ++sg) {
+      const uint64_t tile = blockIdx.x + (uint64_t)sg * gridDim.x;
+      if (tile < nt) {
+        mbar_expect_tx(&bars[sg], TB * nsl);
+        for (int i = 0; i < nsl; ++i)
+          bulk_g2s(stage + ((uint64_t)sg * nsl + i) * TILE, src[i] + tile * TILE, TB, &bars[sg]);
+      }
+    }
+  }
+  __syncthreads();
+  const bool norm = n.norm != nullptr;
+  double nacc = 0.0;
+  for (uint64_t j = 0;; ++j) {
+    const uint64_t tile = blockIdx.x + j * gridDim.x;
+    if (tile >= nt) break;
+    const int sg = (int)(j % kOs2Stages);
+    mbar_wait(&bars[sg], (uint32_t)((j / kOs2Stages) & 1));
+    const T* base = stage + (uint64_t)sg * nsl * TILE + (uint64_t)threadIdx.x * W;
+    OneshotIn<T, true, P> in[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint64_t off = (uint64_t)u * kBlock * W;
+      auto rd = [&](int slot, Lanes<T, true>& dst) {
+        Vec<T> v;
+        v.u = *reinterpret_cast<const uint4*>(base + (uint64_t)slot * TILE + off);
+#pragma unroll
+        for (int l = 0; l < W; ++l) dst.v[l] = v.t[l];
+      };
+#pragma unroll
+      for (int r = 0; r < P; ++r) rd(r, in[u].v[r]);
+      rd(s_x, in[u].x);
+      if (!a.agg) rd(s_dp, in[u].dp);
+      if (a.quad) {
+        rd(s_g, in[u].s);
+        rd(s_g + 1, in[u].o);
+      } else {
+        rd(s_g, in[u].gb);
+      }
+      if (n.noise) {
+        rd(s_nz, in[u].xi);
+      } else if (n.nsigma != T(0)) {
+        float z[W];
+        dev_normals<W>(n.nkey, n.nctr, n.nbase + tile * TILE + (uint64_t)threadIdx.x * W + off, z);
+#pragma unroll
+        for (int l = 0; l < W; ++l) in[u].xi.v[l] = rmul(n.nsigma, (T)z[l]);
+      } else {
+#pragma unroll
+        for (int l = 0; l < W; ++l) in[u].xi.v[l] = T(0);
+      }
+    }
+    __syncthreads();  // stage consumed
+    if (threadIdx.x == 0) {
+      const uint64_t nxt = blockIdx.x + (j + kOs2Stages) * gridDim.x;
+      if (nxt < nt) {
+        mbar_expect_tx(&bars[sg], TB * nsl);
+        for (int i = 0; i < nsl; ++i)
+          bulk_g2s(stage + ((uint64_t)sg * nsl + i) * TILE, src[i] + nxt * TILE, TB, &bars[sg]);
+      }
+    }
+    const uint64_t k0 = tile * TILE + (uint64_t)threadIdx.x * W;
+    oneshot_store<T, true, P>(a, k0, in[0], norm, nacc);
+    oneshot_store<T, true, P>(a, k0 + (uint64_t)kBlock * W, in[1], norm, nacc);
+  }
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t kk = nt * TILE + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; kk < a.d;
+       kk += stride)
+    oneshot_group<T, false, P>(a, kk, norm, nacc);
+  block_add_double(nacc, a.node.norm);
+  block_signal(a.signal);
+}
+
 template <typename T, int P>
 cudaError_t launch_ar_oneshot_p(const ArOneShotArgs<T>& a, int vec, uint32_t grid, cudaStream_t s) {
+  static const bool all_staged = [] {  // DSGD_OS_STAGE_ALL=0: stage only the exchange tiles
+    const char* e = getenv("DSGD_OS_STAGE_ALL");
+    return !(e && e[0] == '0');
+  }();
+  if (vec && a.pending && !a.apply_only && a.tma_rank >= 0 && all_staged) {
+    const int nsl = P + 1 + (a.agg ? 0 : 1) + (a.quad ? 2 : 1) + (a.node.noise ? 1 : 0);
+    const size_t smem = 128 + (size_t)kOs2Stages * nsl * os_tile<T>() * sizeof(T);
+    static size_t attr = 0;
+    if (attr < smem) {
+      cudaFuncSetAttribute(k_ar_oneshot_tma2<T, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      attr = smem;
+    }
+    int resident = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_ar_oneshot_tma2<T, P>, kBlock, smem);
+    if (resident < 1) resident = 1;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t tiles = a.d / os_tile<T>();
+    uint32_t g = (uint32_t)sms * (uint32_t)resident;
+    if (tiles < g) g = (uint32_t)(tiles ? tiles : 1);
+    k_ar_oneshot_tma2<T, P><<<g, kBlock, smem, s>>>(a, nsl);
+    return cudaGetLastError();
+  }
   if (vec && a.pending && !a.apply_only && a.tma_rank >= 0) {
     const size_t smem = 128 + (size_t)kOsStages * P * os_tile<T>() * sizeof(T);
     static int resident = 0;  // CTAs per SM at this smem size (persistent grid)
