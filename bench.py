@@ -438,8 +438,9 @@ def run_extras_dist(args, world, rank, local, h, max_over_ranks, barrier):
     for name, proto, d in (("pull-gossip 10M/worker", N.PULL_GOSSIP, 10_000_000),
                            ("elastic-avg 25M/worker", N.ELASTIC_AVG, 25_000_000)):
         try:
-            grp = Group.distributed(d, rank, world, local, dtype="f32", nccl=True,
-                                    center=(proto == N.ELASTIC_AVG))
+            grp = Group.distributed(d, rank, world, local, dtype="f32",
+                                    nccl=(proto == N.ELASTIC_AVG),  # center init = mean
+                                    allreduce=False, center=(proto == N.ELASTIC_AVG))
             gen = torch.Generator(device=f"cuda:{local}")
             gen.manual_seed(7 + rank)
             pool = [torch.randn(d, generator=gen, device=f"cuda:{local}") for _ in range(2)]

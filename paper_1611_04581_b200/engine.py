@@ -400,7 +400,7 @@ class Group:
 
     @classmethod
     def distributed(cls, d: int, rank: int, world: int, device: int, dtype="f32",
-                    nccl: bool = True, **kw) -> "Group":
+                    nccl: bool = True, allreduce: bool = True, **kw) -> "Group":
         """One node per process/GPU; wires IPC peers and NCCL through the
         already-initialised torch.distributed process group (any backend)."""
         import os
@@ -410,7 +410,7 @@ class Group:
             g.init_nccl(broadcast_nccl_id(rank, world), rank, world)
         g.allreduce_backend = "local" if world == 1 else os.environ.get(
             "DSGD_ALLREDUCE", "oneshot" if world <= 2 else "nvls")
-        if g.allreduce_backend == "nvls":
+        if g.allreduce_backend == "nvls" and allreduce:
             why = g._attach_nvls(device)
             if why:  # no multicast (NVLS) on this system: two-shot over peer memory
                 g.allreduce_backend = "p2p"
