@@ -387,8 +387,141 @@ __global__ void __launch_bounds__(kBlock) k_step_tma(const __grid_constant__ Ste
   block_signal(a.signal);
 }
 
+// Gossip-family step of one node with EVERY stream (NVLink partner, theta,
+// delta, gradient / s+opt, noise) staged through smem, 3 stages ahead.
+template <typename T, int MODE>
+__global__ void __launch_bounds__(kBlock) k_step_tma2(const __grid_constant__ StepArgs<T> a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr uint64_t TILE = st_tile<T>();
+  constexpr uint32_t TB = (uint32_t)(TILE * sizeof(T));
+  constexpr int W = Vec<T>::N;
+  constexpr int kStages = 3;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
+  T* stage = reinterpret_cast<T*>(smem_raw + 128);
+  if (!block_wait(a.wait)) return;
+  const NodeIO<T>& n = a.node[0];
+  const T* src[6];
+  int q = 0;
+  src[q++] = n.partner;   // slot 0: the peer snapshot (NVLink)
+  src[q++] = n.theta_in;  // slot 1
+  const bool mix_only = MODE == kModeMix;
+  const int s_dp = q;
+  if (!mix_only) src[q++] = n.delta;
+  const int s_g = q;
+  if (!mix_only) {
+    if (a.quad) {
+      src[q++] = a.spec;
+      src[q++] = a.opt;
+    } else {
+      src[q++] = n.grad;
+    }
+  }
+  const int s_nz = q;
+  if (!mix_only && n.noise) src[q++] = n.noise;
+  const int nsl = q;
+  const uint64_t nt = a.d / TILE;
+  if (threadIdx.x == 0) {
+    for (int sg = 0; sg < kStages; ++sg) mbar_init(&bars[sg], 1);
+    fence_mbar_init();
+    for (int sg = 0; sg < kStages; ++sg) {
+      const uint64_t tile = blockIdx.x + (uint64_t)sg * gridDim.x;
+      if (tile < nt) {
+        mbar_expect_tx(&bars[sg], TB * nsl);
+        for (int i = 0; i < nsl; ++i)
+          bulk_g2s(stage + ((uint64_t)sg * nsl + i) * TILE, src[i] + tile * TILE, TB, &bars[sg]);
+      }
+    }
+  }
+  __syncthreads();
+  const bool norm = n.norm != nullptr;
+  double nacc = 0.0;
+  for (uint64_t j = 0;; ++j) {
+    const uint64_t tile = blockIdx.x + j * gridDim.x;
+    if (tile >= nt) break;
+    const int sg = (int)(j % kStages);
+    mbar_wait(&bars[sg], (uint32_t)((j / kStages) & 1));
+    const T* base = stage + (uint64_t)sg * nsl * TILE + (uint64_t)threadIdx.x * W;
+    StepIn<T, true> in[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint64_t off = (uint64_t)u * kBlock * W;
+      auto rd = [&](int slot, Lanes<T, true>& dst) {
+        Vec<T> v;
+        v.u = *reinterpret_cast<const uint4*>(base + (uint64_t)slot * TILE + off);
+#pragma unroll
+        for (int l = 0; l < W; ++l) dst.v[l] = v.t[l];
+      };
+      rd(0, in[u].xj);
+      rd(1, in[u].x);
+      if (!mix_only) {
+        rd(s_dp, in[u].dp);
+        if (a.quad) {
+          rd(s_g, in[u].s);
+          rd(s_g + 1, in[u].o);
+        } else {
+          rd(s_g, in[u].gb);
+        }
+        if (n.noise) {
+          rd(s_nz, in[u].xi);
+        } else if (n.nsigma != T(0)) {
+          float z[W];
+          dev_normals<W>(n.nkey, n.nctr, n.nbase + tile * TILE + (uint64_t)threadIdx.x * W + off, z);
+#pragma unroll
+          for (int l = 0; l < W; ++l) in[u].xi.v[l] = rmul(n.nsigma, (T)z[l]);
+        } else {
+#pragma unroll
+          for (int l = 0; l < W; ++l) in[u].xi.v[l] = T(0);
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint64_t nxt = blockIdx.x + (j + kStages) * gridDim.x;
+      if (nxt < nt) {
+        mbar_expect_tx(&bars[sg], TB * nsl);
+        for (int i = 0; i < nsl; ++i)
+          bulk_g2s(stage + ((uint64_t)sg * nsl + i) * TILE, src[i] + nxt * TILE, TB, &bars[sg]);
+      }
+    }
+    const uint64_t k0 = tile * TILE + (uint64_t)threadIdx.x * W;
+    step_store<T, MODE, true>(a, n, k0, in[0], norm, nacc);
+    step_store<T, MODE, true>(a, n, k0 + (uint64_t)kBlock * W, in[1], norm, nacc);
+  }
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t kk = nt * TILE + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; kk < a.d;
+       kk += stride)
+    step_group<T, MODE, false>(a, n, kk, norm, nacc);
+  block_add_double(nacc, n.norm);
+  block_signal(a.signal);
+}
+
 template <typename T, int MODE>
 cudaError_t launch_step_tma(const StepArgs<T>& a, cudaStream_t s) {
+  static const bool all_staged = [] {  // DSGD_GOSSIP_STAGE_ALL=0: stage the partner only
+    const char* e = getenv("DSGD_GOSSIP_STAGE_ALL");
+    return !(e && e[0] == '0');
+  }();
+  if (all_staged) {
+    const int nsl = 2 + (MODE == kModeMix ? 0 : 1 + (a.quad ? 2 : 1) + (a.node[0].noise ? 1 : 0));
+    const size_t smem = 128 + (size_t)3 * nsl * st_tile<T>() * sizeof(T);
+    static size_t attr = 0;
+    if (attr < smem) {
+      cudaFuncSetAttribute(k_step_tma2<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      attr = smem;
+    }
+    int resident = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_step_tma2<T, MODE>, kBlock, smem);
+    if (resident < 1) resident = 1;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t tiles = a.d / st_tile<T>();
+    uint32_t g = (uint32_t)sms * (uint32_t)resident;
+    if (tiles < g) g = (uint32_t)(tiles ? tiles : 1);
+    k_step_tma2<T, MODE><<<g, kBlock, smem, s>>>(a);
+    return cudaGetLastError();
+  }
   const size_t smem = 128 + (size_t)kStStages * st_tile<T>() * sizeof(T);
   static int resident = 0;
   if (!resident) {
@@ -1558,8 +1691,123 @@ __global__ void __launch_bounds__(kBlock) k_ea_chain(const __grid_constant__ EaC
   block_add_double(nacc, n.norm);
 }
 
+// The chain with the chunk's local streams (theta, delta, gradient / s+opt,
+// noise) bulk-copied into shared memory BEFORE waiting for the previous
+// rank's center -- the HBM latency hides behind the chain wait -- and the
+// center chunk bulk-copied right after the flag; one chunk per CTA.
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_ea_chain_tma(const __grid_constant__ EaChainArgs<T> a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ int ok;
+  constexpr int W = Vec<T>::N;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);  // [0] local, [1] center
+  T* buf = reinterpret_cast<T*>(smem_raw + 128);
+  const NodeIO<T>& n = a.node;
+  const bool norm = n.norm != nullptr;
+  double nacc = 0.0;
+  const uint64_t c = blockIdx.x;
+  const uint64_t lo = c * a.chunk;
+  const uint64_t len = lo + a.chunk <= a.d ? a.chunk : a.d - lo;
+  const uint64_t lv = len / 4 * 4;  // staged part (16-byte multiple)
+  const uint32_t bytes = (uint32_t)(lv * sizeof(T));
+  const T* src[5];
+  int ns = 0;
+  src[ns++] = n.theta_in;
+  src[ns++] = n.delta;
+  if (a.quad) {
+    src[ns++] = a.spec;
+    src[ns++] = a.opt;
+  } else {
+    src[ns++] = n.grad;
+  }
+  const int s_nz = ns;
+  if (n.noise) src[ns++] = n.noise;
+  T* cbuf = buf + (uint64_t)ns * a.chunk;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+    if (bytes) {
+      mbar_expect_tx(&bars[0], bytes * ns);
+      for (int q = 0; q < ns; ++q) bulk_g2s(buf + (uint64_t)q * a.chunk, src[q] + lo, bytes, &bars[0]);
+    }
+    ok = wait_flag(&a.flag_in[c], a.need, a.timeout_ns, a.error) ? 1 : 0;
+    if (ok && bytes) {
+      mbar_expect_tx(&bars[1], bytes);
+      bulk_g2s(cbuf, a.c_in + lo, bytes, &bars[1]);
+    }
+  }
+  __syncthreads();
+  if (bytes) mbar_wait(&bars[0], 0);  // never leave with copies in flight
+  if (!ok) return;
+  if (bytes) mbar_wait(&bars[1], 0);
+  for (uint64_t e = (uint64_t)threadIdx.x * W; e < lv; e += (uint64_t)kBlock * W) {
+    Vec<T> vx, vd, vg, vs, vo, vn, vc;
+    vx.u = *reinterpret_cast<const uint4*>(buf + e);
+    vd.u = *reinterpret_cast<const uint4*>(buf + a.chunk + e);
+    if (a.quad) {
+      vs.u = *reinterpret_cast<const uint4*>(buf + 2 * a.chunk + e);
+      vo.u = *reinterpret_cast<const uint4*>(buf + 3 * a.chunk + e);
+    } else {
+      vg.u = *reinterpret_cast<const uint4*>(buf + 2 * a.chunk + e);
+    }
+    if (n.noise) vn.u = *reinterpret_cast<const uint4*>(buf + (uint64_t)s_nz * a.chunk + e);
+    vc.u = *reinterpret_cast<const uint4*>(cbuf + e);
+    float z[W];
+    if (!n.noise && n.nsigma != T(0)) dev_normals<W>(n.nkey, n.nctr, n.nbase + lo + e, z);
+    Lanes<T, true> ot, od, cv;
+#pragma unroll
+    for (int l = 0; l < W; ++l) {
+      const T xi = n.noise ? vn.t[l] : (n.nsigma != T(0) ? rmul(n.nsigma, (T)z[l]) : T(0));
+      const T u = rmul(a.beta, rsub(vx.t[l], vc.t[l]));
+      const T xv = rsub(vx.t[l], u);
+      const T dl = sgd_delta(xv, vd.t[l], a.quad ? T(0) : vg.t[l], a.quad ? vs.t[l] : T(0),
+                             a.quad ? vo.t[l] : T(0), xi, n.alpha, a.mu, a.wd, a.mu_nz, a.wd_pos,
+                             a.quad, norm, nacc);
+      od.v[l] = dl;
+      ot.v[l] = radd(xv, dl);
+      cv.v[l] = radd(vc.t[l], u);
+    }
+    st(n.theta_out, lo + e, ot);
+    st(n.delta, lo + e, od);
+    st(a.c_out, lo + e, cv);
+  }
+  for (uint64_t kk = lo + lv + threadIdx.x; kk < lo + len; kk += kBlock) {  // ragged tail
+    const T cv0 = a.c_in[kk];
+    T xv = n.theta_in[kk];
+    const T u = rmul(a.beta, rsub(xv, cv0));
+    xv = rsub(xv, u);
+    const T gb = a.quad ? T(0) : n.grad[kk];
+    const T sv = a.quad ? a.spec[kk] : T(0), ov = a.quad ? a.opt[kk] : T(0);
+    const T dl = sgd_delta(xv, n.delta[kk], gb, sv, ov, noise_at(n, kk), n.alpha, a.mu, a.wd,
+                           a.mu_nz, a.wd_pos, a.quad, norm, nacc);
+    n.delta[kk] = dl;
+    n.theta_out[kk] = radd(xv, dl);
+    a.c_out[kk] = radd(cv0, u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) st_release_sys(&a.flag_out[c], a.seq);
+  block_add_double(nacc, n.norm);
+}
+
 template <typename T>
 cudaError_t launch_ea_chain(const EaChainArgs<T>& a, int vec, uint32_t grid, cudaStream_t s) {
+  static const bool tma = [] {  // DSGD_EA_TMA=0: the register kernel
+    const char* e = getenv("DSGD_EA_TMA");
+    return !(e && e[0] == '0');
+  }();
+  const int nslot = 2 + (a.quad ? 2 : 1) + (a.node.noise ? 1 : 0) + 1;
+  const size_t smem = 128 + (size_t)nslot * a.chunk * sizeof(T);
+  if (vec && tma && smem <= 200 * 1024 && a.n_chunks == grid) {
+    static size_t attr = 0;
+    if (attr < smem) {
+      cudaFuncSetAttribute(k_ea_chain_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      attr = smem;
+    }
+    k_ea_chain_tma<T><<<grid, kBlock, smem, s>>>(a);
+    return cudaGetLastError();
+  }
   if (vec)
     k_ea_chain<T, true><<<grid, kBlock, 0, s>>>(a);
   else
