@@ -1792,9 +1792,9 @@ __global__ void __launch_bounds__(kBlock) k_ea_chain_tma(const __grid_constant__
 
 template <typename T>
 cudaError_t launch_ea_chain(const EaChainArgs<T>& a, int vec, uint32_t grid, cudaStream_t s) {
-  static const bool tma = [] {  // DSGD_EA_TMA=0: the register kernel
+  static const bool tma = [] {  // DSGD_EA_TMA=1: smem-staged chain (slower at chunk 4096)
     const char* e = getenv("DSGD_EA_TMA");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   const int nslot = 2 + (a.quad ? 2 : 1) + (a.node.noise ? 1 : 0) + 1;
   const size_t smem = 128 + (size_t)nslot * a.chunk * sizeof(T);
