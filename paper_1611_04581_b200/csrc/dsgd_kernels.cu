@@ -910,8 +910,7 @@ __global__ void __launch_bounds__(kBlock) k_ar_oneshot_tma(const __grid_constant
 constexpr int kOs2Stages = 3;
 
 template <typename T, int P>
-__global__ void __launch_bounds__(kBlock) k_ar_oneshot_tma2(const __grid_constant__ ArOneShotArgs<T> a,
-                                                            int ns) {
+__global__ void __launch_bounds__(kBlock) k_ar_oneshot_tma2(const __grid_constant__ ArOneShotArgs<T> a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr uint64_t TILE = os_tile<T>();
   constexpr uint32_t TB = (uint32_t)(TILE * sizeof(T));
@@ -938,7 +937,6 @@ __global__ void __launch_bounds__(kBlock) k_ar_oneshot_tma2(const __grid_constan
   }
   const int s_nz = q;
   if (n.noise) src[q++] = n.noise;
-  (void)ns;
   const int nsl = q;
   const uint64_t nt = a.d / TILE;
   if (threadIdx.x == 0) {
@@ -1039,7 +1037,7 @@ cudaError_t launch_ar_oneshot_p(const ArOneShotArgs<T>& a, int vec, uint32_t gri
     const uint64_t tiles = a.d / os_tile<T>();
     uint32_t g = (uint32_t)sms * (uint32_t)resident;
     if (tiles < g) g = (uint32_t)(tiles ? tiles : 1);
-    k_ar_oneshot_tma2<T, P><<<g, kBlock, smem, s>>>(a, nsl);
+    k_ar_oneshot_tma2<T, P><<<g, kBlock, smem, s>>>(a);
     return cudaGetLastError();
   }
   if (vec && a.pending && !a.apply_only && a.tma_rank >= 0) {
@@ -1140,8 +1138,7 @@ __host__ __device__ constexpr uint64_t lt_tile() {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kBlock) k_local_tma(const __grid_constant__ AllreduceArgs<T> a,
-                                                      int nstreams) {
+__global__ void __launch_bounds__(kBlock) k_local_tma(const __grid_constant__ AllreduceArgs<T> a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr uint64_t TILE = lt_tile<T>();
   constexpr uint32_t TB = (uint32_t)(TILE * sizeof(T));
@@ -1160,7 +1157,6 @@ __global__ void __launch_bounds__(kBlock) k_local_tma(const __grid_constant__ Al
     src[ns++] = n.grad;
   }
   if (n.noise) src[ns++] = n.noise;
-  (void)nstreams;
   const uint64_t nt = a.d / TILE;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kLtStages; ++s) mbar_init(&bars[s], 1);
@@ -1280,7 +1276,7 @@ cudaError_t launch_local_tma(const AllreduceArgs<T>& a, cudaStream_t s) {
   const uint64_t tiles = a.d / lt_tile<T>();
   uint32_t g = (uint32_t)sms * (uint32_t)resident;
   if (tiles < g) g = (uint32_t)(tiles ? tiles : 1);
-  k_local_tma<T><<<g, kBlock, smem, s>>>(a, 0);
+  k_local_tma<T><<<g, kBlock, smem, s>>>(a);
   return cudaGetLastError();
 }
 

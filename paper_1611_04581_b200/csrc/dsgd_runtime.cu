@@ -671,7 +671,8 @@ dsgd_status do_allreduce_p2p(dsgd_ctx* c, const dsgd_hyperparams* h, const GradS
   // reduce overlaps pipeline h'`s HBM-bound delta kernel.
   if (t == 0) {  // the split is fixed for the context's lifetime (counters per pipeline)
     uint32_t k0 = c->ar_pipes;
-    if (c->d < 65536 || k0 * c->p > (uint32_t)kMaxWait) k0 = 1;
+    // small d is latency-bound: one pipeline (fewer launches / cross-GPU waits)
+    if (c->d < (8u << 20) || k0 * c->p > (uint32_t)kMaxWait) k0 = 1;
     c->ar_pipes_used = k0;
   }
   const uint32_t K = c->ar_pipes_used;
@@ -1057,7 +1058,8 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
   // multi-GPU all-reduce backend: oneshot (default p <= 2), p2p (two-shot,
   // default p > 2), nccl
   {
-    std::string mode = c->p <= 2 ? "oneshot" : "p2p";
+    // one kernel per round wins at p <= 2, and at p <= 4 while d is latency-bound
+    std::string mode = (c->p <= 2 || (c->p <= 4 && c->d < (4u << 20))) ? "oneshot" : "p2p";
     if (const char* e = std::getenv("DSGD_ALLREDUCE")) mode = e;
     if (mode == "p2p2k") mode = "p2p";
     c->p2p_allreduce = mode != "nccl";

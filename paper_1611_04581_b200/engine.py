@@ -408,8 +408,9 @@ class Group:
         g.connect_peers(exchange_blobs(g.export_handle(), rank, world))
         if nccl and world > 1:
             g.init_nccl(broadcast_nccl_id(rank, world), rank, world)
+        small = world <= 2 or (world <= 4 and d < (4 << 20))  # one kernel per round
         g.allreduce_backend = "local" if world == 1 else os.environ.get(
-            "DSGD_ALLREDUCE", "oneshot" if world <= 2 else "nvls")
+            "DSGD_ALLREDUCE", "oneshot" if small else "nvls")
         if g.allreduce_backend == "nvls" and allreduce:
             why = g._attach_nvls(device)
             if why:  # no multicast (NVLS) on this system: two-shot over peer memory
