@@ -477,3 +477,65 @@ def test_device_noise_statistics_and_determinism():
     torch.cuda.synchronize()
     s = _device_noise(d, sigma, 7, 5, grad_ptrs=[z.data_ptr() + 4])
     assert same(s, a)
+
+
+# ------------------------------------------- the headline kernel (N = 1)
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("d,fixed,noise,mu,wd,scope", [
+    (5000, True, False, 0.9, 1e-4, "aggregate"),    # 2 full fp32 tiles + ragged tail
+    (2048 * 7 + 3, False, True, 0.9, 1e-3, "per-node"),
+    (4096, True, True, 0.0, 0.0, "aggregate"),       # exact tiles, no tail
+    (1_000_003, True, True, 0.9, 1e-4, "aggregate"),
+])
+def test_single_node_allreduce_staged_kernel_bit_exact(dtype, d, fixed, noise, mu, wd, scope):
+    """p = 1 all-reduce rounds run k_local_tma (every input stream staged
+    through smem by cp.async.bulk); bit-exact with the oracle over 3 rounds."""
+    c = make_case(1, d, dtype, seed=d, fixed=fixed, noise=noise)
+    g = load_group(c, dtype)
+    n = oracle_nodes(c)
+    hk = H(mu=mu, weight_decay=wd)
+    h, hc = Hyperparams(**hk), O.HyperParams(**hk)
+    for _ in range(3):
+        g.allreduce_round(h, scope=scope, grad="buffer" if fixed else "quadratic", noise=noise)
+        O.allreduce_round(n, hc, per_node=scope == "per-node", **okw(c))
+    th, dp, t = read_group(g, 1, dtype)
+    assert same(th, n.theta) and same(dp, n.dprev) and t.tolist() == n.t.tolist()
+    g.close()
+
+
+def test_device_noise_same_on_ldg_and_staged_kernels():
+    """In-kernel Philox noise depends only on (seed, node, t, k): the LDG
+    local-step kernel and the staged p = 1 all-reduce kernel draw the same."""
+    d = 300_001
+    rng = np.random.default_rng(4)
+    theta = rng.normal(size=d)
+    hk = dict(alpha0=0.1, anneal_at=(), mu=0.5, weight_decay=0.0)
+    out = []
+    for kind in ("local", "allreduce"):
+        g = Group(d, 1, dtype="f32", quadratic=True)
+        g.set_quadratic(np.ones(d), np.zeros(d))
+        g.set_state(0, theta, np.zeros(d), 4)
+        fn = g.local_sgd_step if kind == "local" else g.allreduce_round
+        fn(Hyperparams(**hk), grad="quadratic", noise=("device", 0.2, 99))
+        out.append(g.get_state(0)[0])
+        g.close()
+    assert same(out[0], out[1])
+
+
+@pytest.mark.parametrize("p", [16, 32])
+@pytest.mark.parametrize("rule", ["allreduce", "ea", "pull", "push"])
+def test_many_nodes_one_gpu_bit_exact(p, rule):
+    """Up to DSGD_MAX_LOCAL_NODES = 32 workers in one context."""
+    d = 777
+    c = make_case(p, d, "f64", seed=p, fixed=True, noise=True)
+    rng = np.random.default_rng(p)
+    partner = rng.integers(0, p, size=p).astype(np.uint32)
+    target = np.array([(i + 1 + int(rng.integers(0, p - 1))) % p for i in range(p)], dtype=np.uint32)
+    g = load_group(c, "f64")
+    n = oracle_nodes(c)
+    center = run_rule(rule, g, n, c, H(), partner, target)
+    th, dp, t = read_group(g, p, "f64")
+    assert same(th, n.theta) and same(dp, n.dprev)
+    if rule == "ea":
+        assert same(g.get_center(), center)
+    g.close()
