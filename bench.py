@@ -67,25 +67,31 @@ class ClockSampler:
         self.index = index
         self.rows = []
         self.proc = None
+        self.path = f"/tmp/dsgd_clocks_{os.getpid()}.csv"
+
+    def _load(self):
+        try:
+            with open(self.path) as f:
+                self.rows = [[x.strip() for x in line.split(",")] for line in f if line.strip()]
+        except OSError:
+            self.rows = []
 
     def __enter__(self):
+        # written to a file (a pipe would sit in nvidia-smi's stdio buffer)
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
+                 "--format=csv,noheader,nounits", "-lms", "50", "-f", self.path],
+                stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
             t0 = time.time()
-            while not self.rows and time.time() - t0 < 10:   # sampler is live
-                time.sleep(0.01)
+            while time.time() - t0 < 10:   # wait until the sampler is live
+                self._load()
+                if self.rows:
+                    break
+                time.sleep(0.05)
         except Exception:
             self.proc = None
         return self
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
 
     def __exit__(self, *exc):
         if self.proc:
@@ -94,6 +100,11 @@ class ClockSampler:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+        self._load()
+        try:
+            os.remove(self.path)
+        except OSError:
+            pass
 
     def summary(self):
         if not self.rows:
@@ -257,7 +268,8 @@ def main():
         nv_bytes = 2 * (world - 1) / world * es * d  # two-shot / ring, per direction per GPU
     if world == 1:
         kname, bpp = "allreduce_local", 5 * es  # read theta, delta, g; write theta', delta'
-        kdesc = "k_allreduce_local (p=1): fused delta + mean + apply, 12 B read + 8 B write per param"
+        kdesc = ("k_local_tma (p=1 round: fused delta + mean + apply; theta, delta, g staged "
+                 "through smem by cp.async.bulk), 12 B read + 8 B write per param")
     elif backend == "oneshot":
         kname, bpp = "allreduce_comm", (5 + (world - 1)) * es
         kdesc = ("k_ar_oneshot_tma: one kernel per round; every rank's previous exchange tile staged "

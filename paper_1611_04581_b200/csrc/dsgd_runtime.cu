@@ -68,6 +68,7 @@ using dsgd::set_error;
 namespace {
 
 constexpr uint32_t kMagic = 0xD56DB200u;
+constexpr uint64_t kBlockU = dsgd::kBlock;
 
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
@@ -148,6 +149,7 @@ struct dsgd_ctx {
   bool ar_nvls = false;            // ... two-shot with the reduce/broadcast in the NVSwitch
   uint32_t ar_pipes = 2;           // two-shot: independent pipelines (streams) over d
   double ar_delta_frac = 2.0;      // delta-kernel CTAs per SM, split over the pipelines
+  double ar_comm_frac = 4.0;       // reduce-kernel CTAs per SM, split over the pipelines
   cudaStream_t pipe_stream[4] = {};
   cudaEvent_t pipe_event[5] = {};  // [0..3] join, [4] fork
   bool pipes_forked = false;
@@ -747,7 +749,8 @@ dsgd_status do_allreduce_p2p(dsgd_ctx* c, const dsgd_hyperparams* h, const GradS
       a.p = c->p;
       a.wait = wx;
       a.signal = sx;
-      const uint32_t grid = std::max<uint32_t>(1, blocks_for(c, (a.hi - a.lo) / 4 + 1, 1) / K);
+      const uint32_t cap = std::max<uint32_t>(1, (uint32_t)(c->sm_count * c->ar_comm_frac / K));
+      const uint32_t grid = std::min<uint32_t>(cap, std::max<uint32_t>(1, (uint32_t)((a.hi - a.lo) / 4 / kBlockU + 1)));
       LaunchScope ls(c, DSGD_K_NCCL, st);
       DSGD_CUDA(dsgd::launch_ar_nvls<T>(a, grid, st));
     } else {
@@ -1072,6 +1075,7 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
   }
   if (const char* e = std::getenv("DSGD_AR_PIPES")) c->ar_pipes = (uint32_t)std::min(4, std::max(1, atoi(e)));
   if (const char* e = std::getenv("DSGD_AR_DELTA_FRAC")) c->ar_delta_frac = std::max(0.05, atof(e));
+  if (const char* e = std::getenv("DSGD_AR_COMM_FRAC")) c->ar_comm_frac = std::max(0.05, atof(e));
 
   DSGD_CUDA(cudaMalloc(&c->arena, c->arena_bytes));
   DSGD_CUDA(cudaMemset(c->arena, 0, c->arena_bytes));
