@@ -1786,8 +1786,90 @@ __global__ void __launch_bounds__(kBlock) k_ea_chain_tma(const __grid_constant__
   block_add_double(nacc, n.norm);
 }
 
+// The chain for chunk = 4096 elements (16 per thread), registers only: the
+// chunk's local streams are loaded BEFORE waiting for the previous rank's
+// center, so their HBM latency hides behind the chain wait.
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_ea_chain_pre(const __grid_constant__ EaChainArgs<T> a) {
+  __shared__ int ok;
+  constexpr int W = Vec<T>::N;
+  constexpr int NV = 16 / W;  // vectors per thread per stream
+  using L = Lanes<T, true>;
+  const NodeIO<T>& n = a.node;
+  const bool norm = n.norm != nullptr;
+  double nacc = 0.0;
+  for (uint64_t c = blockIdx.x; c < a.n_chunks; c += gridDim.x) {
+    const uint64_t lo = c * 4096;
+    const bool full = lo + 4096 <= a.d;
+    L x[NV], dp[NV], gb[NV], sp[NV], o[NV], xi[NV];
+    if (full) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const uint64_t k = lo + ((uint64_t)v * kBlock + threadIdx.x) * W;
+        ld(x[v], n.theta_in, k);
+        ld(dp[v], n.delta, k);
+        ld_grad_inputs(gb[v], sp[v], o[v], xi[v], n, a.spec, a.opt, a.quad, k);
+      }
+    }
+    if (threadIdx.x == 0) ok = wait_flag(&a.flag_in[c], a.need, a.timeout_ns, a.error) ? 1 : 0;
+    __syncthreads();
+    if (!ok) return;
+    if (full) {
+      L cv[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+        ld(cv[v], a.c_in, lo + ((uint64_t)v * kBlock + threadIdx.x) * W);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const uint64_t k = lo + ((uint64_t)v * kBlock + threadIdx.x) * W;
+        L ot, od;
+#pragma unroll
+        for (int l = 0; l < W; ++l) {
+          const T u = rmul(a.beta, rsub(x[v].v[l], cv[v].v[l]));
+          const T xv = rsub(x[v].v[l], u);
+          const T dl = sgd_delta(xv, dp[v].v[l], gb[v].v[l], sp[v].v[l], o[v].v[l], xi[v].v[l],
+                                 n.alpha, a.mu, a.wd, a.mu_nz, a.wd_pos, a.quad, norm, nacc);
+          od.v[l] = dl;
+          ot.v[l] = radd(xv, dl);
+          cv[v].v[l] = radd(cv[v].v[l], u);
+        }
+        st(n.theta_out, k, ot);
+        st(n.delta, k, od);
+        st(a.c_out, k, cv[v]);
+      }
+    } else {  // ragged last chunk: scalar
+      for (uint64_t kk = lo + threadIdx.x; kk < a.d; kk += kBlock) {
+        const T cv0 = a.c_in[kk];
+        T xv = n.theta_in[kk];
+        const T u = rmul(a.beta, rsub(xv, cv0));
+        xv = rsub(xv, u);
+        const T g0 = a.quad ? T(0) : n.grad[kk];
+        const T sv = a.quad ? a.spec[kk] : T(0), ov = a.quad ? a.opt[kk] : T(0);
+        const T dl = sgd_delta(xv, n.delta[kk], g0, sv, ov, noise_at(n, kk), n.alpha, a.mu,
+                               a.wd, a.mu_nz, a.wd_pos, a.quad, norm, nacc);
+        n.delta[kk] = dl;
+        n.theta_out[kk] = radd(xv, dl);
+        a.c_out[kk] = radd(cv0, u);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) st_release_sys(&a.flag_out[c], a.seq);
+  }
+  block_add_double(nacc, n.norm);
+}
+
 template <typename T>
 cudaError_t launch_ea_chain(const EaChainArgs<T>& a, int vec, uint32_t grid, cudaStream_t s) {
+  static const bool pre = [] {  // DSGD_EA_PRELOAD=0: the plain register kernel
+    const char* e = getenv("DSGD_EA_PRELOAD");
+    return !(e && e[0] == '0');
+  }();
+  if constexpr (sizeof(T) == 4) {  // fp64 would need 2x the registers
+    if (vec && pre && a.chunk == 4096) {
+      k_ea_chain_pre<T><<<grid, kBlock, 0, s>>>(a);
+      return cudaGetLastError();
+    }
+  }
   static const bool tma = [] {  // DSGD_EA_TMA=1: smem-staged chain (slower at chunk 4096)
     const char* e = getenv("DSGD_EA_TMA");
     return e && e[0] == '1';

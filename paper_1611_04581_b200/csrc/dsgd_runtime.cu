@@ -149,7 +149,7 @@ struct dsgd_ctx {
   bool ar_nvls = false;            // ... two-shot with the reduce/broadcast in the NVSwitch
   uint32_t ar_pipes = 2;           // two-shot: independent pipelines (streams) over d
   double ar_delta_frac = 2.0;      // delta-kernel CTAs per SM, split over the pipelines
-  double ar_comm_frac = 4.0;       // reduce-kernel CTAs per SM, split over the pipelines
+  double ar_comm_frac = 2.0;       // reduce-kernel CTAs per SM, split over the pipelines
   cudaStream_t pipe_stream[4] = {};
   cudaEvent_t pipe_event[5] = {};  // [0..3] join, [4] fork
   bool pipes_forked = false;
