@@ -135,7 +135,14 @@ __device__ __forceinline__ bool block_wait(const WaitSpec& w) {
 // Every CTA fences its writes at system scope and arrives; the last one to
 // arrive publishes the round counter with a release store.
 __device__ __forceinline__ void block_signal(const SignalSpec& s) {
-  if (s.counter == nullptr) return;
+  if (s.counter == nullptr) {
+    // nothing to publish (single context); the tracer stamps CTA 0's end
+    if (s.trace && blockIdx.x == 0) {
+      __syncthreads();
+      if (threadIdx.x == 0) s.trace[2] = globaltimer();
+    }
+    return;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();

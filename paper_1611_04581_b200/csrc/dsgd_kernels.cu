@@ -1687,205 +1687,8 @@ __global__ void __launch_bounds__(kBlock) k_ea_chain(const __grid_constant__ EaC
   block_add_double(nacc, n.norm);
 }
 
-// The chain with the chunk's local streams (theta, delta, gradient / s+opt,
-// noise) bulk-copied into shared memory BEFORE waiting for the previous
-// rank's center -- the HBM latency hides behind the chain wait -- and the
-// center chunk bulk-copied right after the flag; one chunk per CTA.
-template <typename T>
-__global__ void __launch_bounds__(kBlock) k_ea_chain_tma(const __grid_constant__ EaChainArgs<T> a) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ int ok;
-  constexpr int W = Vec<T>::N;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);  // [0] local, [1] center
-  T* buf = reinterpret_cast<T*>(smem_raw + 128);
-  const NodeIO<T>& n = a.node;
-  const bool norm = n.norm != nullptr;
-  double nacc = 0.0;
-  const uint64_t c = blockIdx.x;
-  const uint64_t lo = c * a.chunk;
-  const uint64_t len = lo + a.chunk <= a.d ? a.chunk : a.d - lo;
-  const uint64_t lv = len / 4 * 4;  // staged part (16-byte multiple)
-  const uint32_t bytes = (uint32_t)(lv * sizeof(T));
-  const T* src[5];
-  int ns = 0;
-  src[ns++] = n.theta_in;
-  src[ns++] = n.delta;
-  if (a.quad) {
-    src[ns++] = a.spec;
-    src[ns++] = a.opt;
-  } else {
-    src[ns++] = n.grad;
-  }
-  const int s_nz = ns;
-  if (n.noise) src[ns++] = n.noise;
-  T* cbuf = buf + (uint64_t)ns * a.chunk;
-  if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    fence_mbar_init();
-    if (bytes) {
-      mbar_expect_tx(&bars[0], bytes * ns);
-      for (int q = 0; q < ns; ++q) bulk_g2s(buf + (uint64_t)q * a.chunk, src[q] + lo, bytes, &bars[0]);
-    }
-    ok = wait_flag(&a.flag_in[c], a.need, a.timeout_ns, a.error) ? 1 : 0;
-    if (ok && bytes) {
-      mbar_expect_tx(&bars[1], bytes);
-      bulk_g2s(cbuf, a.c_in + lo, bytes, &bars[1]);
-    }
-  }
-  __syncthreads();
-  if (bytes) mbar_wait(&bars[0], 0);  // never leave with copies in flight
-  if (!ok) return;
-  if (bytes) mbar_wait(&bars[1], 0);
-  for (uint64_t e = (uint64_t)threadIdx.x * W; e < lv; e += (uint64_t)kBlock * W) {
-    Vec<T> vx, vd, vg, vs, vo, vn, vc;
-    vx.u = *reinterpret_cast<const uint4*>(buf + e);
-    vd.u = *reinterpret_cast<const uint4*>(buf + a.chunk + e);
-    if (a.quad) {
-      vs.u = *reinterpret_cast<const uint4*>(buf + 2 * a.chunk + e);
-      vo.u = *reinterpret_cast<const uint4*>(buf + 3 * a.chunk + e);
-    } else {
-      vg.u = *reinterpret_cast<const uint4*>(buf + 2 * a.chunk + e);
-    }
-    if (n.noise) vn.u = *reinterpret_cast<const uint4*>(buf + (uint64_t)s_nz * a.chunk + e);
-    vc.u = *reinterpret_cast<const uint4*>(cbuf + e);
-    float z[W];
-    if (!n.noise && n.nsigma != T(0)) dev_normals<W>(n.nkey, n.nctr, n.nbase + lo + e, z);
-    Lanes<T, true> ot, od, cv;
-#pragma unroll
-    for (int l = 0; l < W; ++l) {
-      const T xi = n.noise ? vn.t[l] : (n.nsigma != T(0) ? rmul(n.nsigma, (T)z[l]) : T(0));
-      const T u = rmul(a.beta, rsub(vx.t[l], vc.t[l]));
-      const T xv = rsub(vx.t[l], u);
-      const T dl = sgd_delta(xv, vd.t[l], a.quad ? T(0) : vg.t[l], a.quad ? vs.t[l] : T(0),
-                             a.quad ? vo.t[l] : T(0), xi, n.alpha, a.mu, a.wd, a.mu_nz, a.wd_pos,
-                             a.quad, norm, nacc);
-      od.v[l] = dl;
-      ot.v[l] = radd(xv, dl);
-      cv.v[l] = radd(vc.t[l], u);
-    }
-    st(n.theta_out, lo + e, ot);
-    st(n.delta, lo + e, od);
-    st(a.c_out, lo + e, cv);
-  }
-  for (uint64_t kk = lo + lv + threadIdx.x; kk < lo + len; kk += kBlock) {  // ragged tail
-    const T cv0 = a.c_in[kk];
-    T xv = n.theta_in[kk];
-    const T u = rmul(a.beta, rsub(xv, cv0));
-    xv = rsub(xv, u);
-    const T gb = a.quad ? T(0) : n.grad[kk];
-    const T sv = a.quad ? a.spec[kk] : T(0), ov = a.quad ? a.opt[kk] : T(0);
-    const T dl = sgd_delta(xv, n.delta[kk], gb, sv, ov, noise_at(n, kk), n.alpha, a.mu, a.wd,
-                           a.mu_nz, a.wd_pos, a.quad, norm, nacc);
-    n.delta[kk] = dl;
-    n.theta_out[kk] = radd(xv, dl);
-    a.c_out[kk] = radd(cv0, u);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) st_release_sys(&a.flag_out[c], a.seq);
-  block_add_double(nacc, n.norm);
-}
-
-// The chain for chunk = 4096 elements (16 per thread), registers only: the
-// chunk's local streams are loaded BEFORE waiting for the previous rank's
-// center, so their HBM latency hides behind the chain wait.
-template <typename T>
-__global__ void __launch_bounds__(kBlock) k_ea_chain_pre(const __grid_constant__ EaChainArgs<T> a) {
-  __shared__ int ok;
-  constexpr int W = Vec<T>::N;
-  constexpr int NV = 16 / W;  // vectors per thread per stream
-  using L = Lanes<T, true>;
-  const NodeIO<T>& n = a.node;
-  const bool norm = n.norm != nullptr;
-  double nacc = 0.0;
-  for (uint64_t c = blockIdx.x; c < a.n_chunks; c += gridDim.x) {
-    const uint64_t lo = c * 4096;
-    const bool full = lo + 4096 <= a.d;
-    L x[NV], dp[NV], gb[NV], sp[NV], o[NV], xi[NV];
-    if (full) {
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const uint64_t k = lo + ((uint64_t)v * kBlock + threadIdx.x) * W;
-        ld(x[v], n.theta_in, k);
-        ld(dp[v], n.delta, k);
-        ld_grad_inputs(gb[v], sp[v], o[v], xi[v], n, a.spec, a.opt, a.quad, k);
-      }
-    }
-    if (threadIdx.x == 0) ok = wait_flag(&a.flag_in[c], a.need, a.timeout_ns, a.error) ? 1 : 0;
-    __syncthreads();
-    if (!ok) return;
-    if (full) {
-      L cv[NV];
-#pragma unroll
-      for (int v = 0; v < NV; ++v)
-        ld(cv[v], a.c_in, lo + ((uint64_t)v * kBlock + threadIdx.x) * W);
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const uint64_t k = lo + ((uint64_t)v * kBlock + threadIdx.x) * W;
-        L ot, od;
-#pragma unroll
-        for (int l = 0; l < W; ++l) {
-          const T u = rmul(a.beta, rsub(x[v].v[l], cv[v].v[l]));
-          const T xv = rsub(x[v].v[l], u);
-          const T dl = sgd_delta(xv, dp[v].v[l], gb[v].v[l], sp[v].v[l], o[v].v[l], xi[v].v[l],
-                                 n.alpha, a.mu, a.wd, a.mu_nz, a.wd_pos, a.quad, norm, nacc);
-          od.v[l] = dl;
-          ot.v[l] = radd(xv, dl);
-          cv[v].v[l] = radd(cv[v].v[l], u);
-        }
-        st(n.theta_out, k, ot);
-        st(n.delta, k, od);
-        st(a.c_out, k, cv[v]);
-      }
-    } else {  // ragged last chunk: scalar
-      for (uint64_t kk = lo + threadIdx.x; kk < a.d; kk += kBlock) {
-        const T cv0 = a.c_in[kk];
-        T xv = n.theta_in[kk];
-        const T u = rmul(a.beta, rsub(xv, cv0));
-        xv = rsub(xv, u);
-        const T g0 = a.quad ? T(0) : n.grad[kk];
-        const T sv = a.quad ? a.spec[kk] : T(0), ov = a.quad ? a.opt[kk] : T(0);
-        const T dl = sgd_delta(xv, n.delta[kk], g0, sv, ov, noise_at(n, kk), n.alpha, a.mu,
-                               a.wd, a.mu_nz, a.wd_pos, a.quad, norm, nacc);
-        n.delta[kk] = dl;
-        n.theta_out[kk] = radd(xv, dl);
-        a.c_out[kk] = radd(cv0, u);
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) st_release_sys(&a.flag_out[c], a.seq);
-  }
-  block_add_double(nacc, n.norm);
-}
-
 template <typename T>
 cudaError_t launch_ea_chain(const EaChainArgs<T>& a, int vec, uint32_t grid, cudaStream_t s) {
-  static const bool pre = [] {  // DSGD_EA_PRELOAD=0: the plain register kernel
-    const char* e = getenv("DSGD_EA_PRELOAD");
-    return !(e && e[0] == '0');
-  }();
-  if constexpr (sizeof(T) == 4) {  // fp64 would need 2x the registers
-    if (vec && pre && a.chunk == 4096) {
-      k_ea_chain_pre<T><<<grid, kBlock, 0, s>>>(a);
-      return cudaGetLastError();
-    }
-  }
-  static const bool tma = [] {  // DSGD_EA_TMA=1: smem-staged chain (slower at chunk 4096)
-    const char* e = getenv("DSGD_EA_TMA");
-    return e && e[0] == '1';
-  }();
-  const int nslot = 2 + (a.quad ? 2 : 1) + (a.node.noise ? 1 : 0) + 1;
-  const size_t smem = 128 + (size_t)nslot * a.chunk * sizeof(T);
-  if (vec && tma && smem <= 200 * 1024 && a.n_chunks == grid) {
-    static size_t attr = 0;
-    if (attr < smem) {
-      cudaFuncSetAttribute(k_ea_chain_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
-      attr = smem;
-    }
-    k_ea_chain_tma<T><<<grid, kBlock, smem, s>>>(a);
-    return cudaGetLastError();
-  }
   if (vec)
     k_ea_chain<T, true><<<grid, kBlock, 0, s>>>(a);
   else

@@ -539,3 +539,25 @@ def test_many_nodes_one_gpu_bit_exact(p, rule):
     if rule == "ea":
         assert same(g.get_center(), center)
     g.close()
+
+
+def test_device_tracer_records_launches():
+    """DSGD_TRACE: every traced launch stamps entry <= after-wait <= done."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np\n"
+        "from paper_1611_04581_b200.engine import Group, Hyperparams\n"
+        "g = Group(100_000, 2, quadratic=True)\n"
+        "g.set_quadratic(np.ones(100_000))\n"
+        "h = Hyperparams(alpha0=0.1, anneal_at=())\n"
+        "for _ in range(3): g.pull_gossip_round(h, [1, 0], grad='quadratic')\n"
+        "tr = g.trace_dump()\n"
+        "assert tr.shape == (3, 5), tr.shape\n"
+        "assert (tr[:, 2] <= tr[:, 3]).all() and (tr[:, 3] <= tr[:, 4]).all() and (tr[:, 4] > 0).all()\n"
+        "assert tr[:, 1].tolist() == [0, 1, 2]\n"
+        "print('ok')\n")
+    env = dict(__import__("os").environ, DSGD_TRACE="64")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         timeout=120, cwd=__import__("os").path.dirname(__import__("os").path.dirname(__file__)))
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr
