@@ -24,23 +24,26 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dtype = sys.argv[1] if len(sys.argv) > 1 else "f64"
     results = {}
-    names = {"all-reduce": O.ALLREDUCE, "elastic-avg": O.ELASTIC, "pull-gossip": O.PULL,
-             "push-gossip": O.PUSH, "gossip-stale": O.STALE, "gossip-fresh": O.FRESH}
+    names = {"all-reduce": O.ALLREDUCE, "all-reduce-pn": O.ALLREDUCE, "elastic-avg": O.ELASTIC,
+             "pull-gossip": O.PULL, "push-gossip": O.PUSH, "gossip-stale": O.STALE,
+             "gossip-fresh": O.FRESH}
     if len(sys.argv) > 2 and sys.argv[2] == "allreduce-only":
-        names = {"all-reduce": O.ALLREDUCE}
+        names = {"all-reduce": O.ALLREDUCE, "all-reduce-pn": O.ALLREDUCE}
     for proto, oid in names.items():
         d = 1031
         hk = dict(alpha0=0.05, anneal_at=(20,), mu=0.9, weight_decay=1e-4, beta_gossip=0.4,
                   beta_ea=0.15, tau=1)
+        ar = proto.startswith("all-reduce")
+        pn = proto == "all-reduce-pn"
         cfg = O.SimConfig(protocol=oid, p=world, hyper=O.HyperParams(**hk), sigma=0.05,
                           spectrum=list(np.linspace(0.5, 2.0, d)),
-                          init_kind=O.INIT_OFFSET_ONES if proto == "all-reduce" else O.INIT_GAUSSIAN,
-                          rounds=25, per_node_scope=False, run_id=f"mg/{proto}")
+                          init_kind=O.INIT_OFFSET_ONES if ar else O.INIT_GAUSSIAN,
+                          rounds=25, per_node_scope=pn, run_id=f"mg/{proto}")
         obj = P.QuadraticObjective(cfg.spectrum)
-        dcfg = D.SimConfig(protocol=proto, p=world, hyper=Hyperparams(**hk),
+        dcfg = D.SimConfig(protocol="all-reduce" if ar else proto, p=world, hyper=Hyperparams(**hk),
                            noise=P.NoiseModel.gaussian_per_coord(0.05, d),
-                           init=D.InitSpec("offset-ones" if proto == "all-reduce" else "gaussian-spread"),
-                           momentum_scope="aggregate",
+                           init=D.InitSpec("offset-ones" if ar else "gaussian-spread"),
+                           momentum_scope="per-node" if pn else "aggregate",
                            rounds=25, run_id=f"mg/{proto}")
         thetas = D.make_initial_nodes(dcfg, obj)
         g = Group.distributed(d, rank, world, local, dtype=dtype, quadratic=True, noise=True,
@@ -60,7 +63,8 @@ def main():
             g.set_center(c.astype(np.float64))
         dist.barrier()
         g.seed_streams(1, f"mg/{proto}")
-        g.run_rounds(D.PROTOCOLS[proto], Hyperparams(**hk), 25, scope="aggregate",
+        g.run_rounds(D.PROTOCOLS[dcfg.protocol], Hyperparams(**hk), 25,
+                     scope="per-node" if pn else "aggregate",
                      grad="quadratic", host_noise_sigma=0.05)
         g.sync()
         th, dp, t = g.get_state(0)
@@ -69,12 +73,12 @@ def main():
         dist.all_gather_object(allst, (th, dp, t))
         if rank == 0:
             npd = np.float64 if dtype == "f64" else np.float32
-            if proto == "all-reduce":
+            if ar:
                 # multi-GPU all-reduce = the reference's threaded transport
                 # (ring_allreduce order), not the simulator's pivot mean
                 on = O.run_transport_allreduce(cfg, dtype=npd)
                 oth, odp, ot, oc = on.theta, on.dprev, on.t, None
-                if dtype == "f64":
+                if dtype == "f64" and not pn:
                     from tests.golden.make_golden import transport_case
                     gp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
                                       "transport.npz")
@@ -85,6 +89,9 @@ def main():
                 oth, odp, ot, oc = O.run(cfg, dtype=npd)
             dev_th = np.array([s[0] for s in allst]).astype(npd)
             exact = dev_th.tobytes() == oth.tobytes()
+            if ar:  # delta_prev too (aggregate: the average; per-node: own delta)
+                dev_dp = np.array([s_[1] for s_ in allst]).astype(npd)
+                exact = exact and dev_dp.tobytes() == odp.tobytes()
             rel = float(np.abs(dev_th.astype(float) - oth.astype(float)).max() /
                         np.abs(oth).max())
             same_ranks = all(np.array_equal(allst[0][0], s[0]) for s in allst)

@@ -52,7 +52,7 @@ def test_multi_gpu_protocols_match_oracle(world, dtype, backend):
     res = json.loads(line[7:])
     for proto, r in res.items():
         assert r["ranks_identical"] or proto != "all-reduce", proto
-        if proto == "all-reduce" and (backend == "nccl" or r["nvls"]):
+        if proto.startswith("all-reduce") and (backend == "nccl" or r["nvls"]):
             assert r["max_rel"] <= (1e-12 if dtype == "f64" else 1e-5), (proto, r)
         else:
             assert r["bit_exact"], (proto, r)
