@@ -5,9 +5,11 @@ Nesterov momentum, d = 25M fp32 parameters per worker, one worker per GPU
 (p = N), synthetic N(0,1) gradients (a pool of 4 distinct device buffers per
 worker, cycled; every step's working set -- theta, delta, gradient, ~400 MB
 -- exceeds the 126 MB L2, so no flush is needed).  A step is one
-allreduce_round (protocols.cpp:110-131): fused delta kernel ->
-ncclAllReduce over NVLink -> fused apply kernel (N > 1), or the single fused
-round kernel (N = 1).
+allreduce_round (protocols.cpp:110-131): at N = 1 the single fused round
+kernel (k_local_tma, streams staged through smem by cp.async.bulk); at N > 1
+the library's multi-GPU all-reduce over NVLink (one-shot peer-memory kernel
+at N <= 2, NVLS multimem two-shot with two pipelines at N > 2; see
+DESIGN.md §5), with the apply fused into the next round's delta.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
