@@ -194,7 +194,17 @@ dsgd_status dsgd_set_t(dsgd_ctx* ctx, uint32_t local, uint64_t t);
  * minibatch gradient (the caller's model fills it).  Weight decay and the
  * additive noise draw are always applied inside the kernel, in the
  * reference order (protocols.cpp:27-38, 98). */
-typedef enum { DSGD_GRAD_QUADRATIC = 0, DSGD_GRAD_BUFFER = 1 } dsgd_grad_source;
+typedef enum {
+  DSGD_GRAD_QUADRATIC = 0,
+  DSGD_GRAD_BUFFER = 1,
+  /* LogisticObjective::stochastic_gradient (objectives.cpp:147-162) on the
+   * device-resident dataset of dsgd_set_logistic, evaluated at the point the
+   * rule evaluates its gradient (after the pull/push/EASGD mix, at the
+   * lookahead theta + mu*delta_prev, or at theta for async-pull), h->batch
+   * rows per node.  Written into each node's DSGD_BUF_GRAD, then consumed as
+   * DSGD_GRAD_BUFFER. */
+  DSGD_GRAD_LOGISTIC = 2
+} dsgd_grad_source;
 
 typedef struct {
   dsgd_grad_source source;
@@ -205,7 +215,22 @@ typedef struct {
   double* grad_norm_out;   /* optional: raised to max_i ||g_i|| like protocols.cpp:34-36 (syncs) */
   double noise_sigma;      /* use_noise == 2 */
   uint64_t noise_seed;     /* use_noise == 2 */
+  const uint64_t* rows;    /* GRAD_LOGISTIC: n_local * batch global row indices (host), node
+                              i's at [i * batch]; NULL: drawn from each node's sample stream
+                              (dsgd_ctx_seed_streams), row = begin + uniform_index(end - begin)
+                              objectives.cpp:154-157 */
 } dsgd_grad_spec;
+
+/* LogisticObjective (objectives.cpp:80-106): features n_samples x d row-major
+ * (host, fp64; stored in the context dtype), labels 0/1, l2 > 0.  Replicated
+ * per context; every local node samples all rows until
+ * dsgd_logistic_set_sample_range.  Errors (DSGD_EINVAL) carry the
+ * constructor's messages. */
+dsgd_status dsgd_set_logistic(dsgd_ctx* ctx, const double* features, const int32_t* labels,
+                              uint64_t n_samples, double l2);
+/* LogisticObjective::set_sample_range objectives.cpp:108-114 for one local node */
+dsgd_status dsgd_logistic_set_sample_range(dsgd_ctx* ctx, uint32_t local, uint64_t begin,
+                                           uint64_t end);
 
 /* ----------------------------------------------------------- update rules
  * All are lock-step over every node of the group and advance each node's t. */

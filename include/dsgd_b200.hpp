@@ -98,11 +98,14 @@ struct Gradient {
   double* grad_norm_out = nullptr;
   double device_noise_sigma = 0.0;   // > 0: N(0, sigma^2) drawn inside the kernel
   std::uint64_t device_noise_seed = 0;
+  std::vector<std::uint64_t> rows;   // DSGD_GRAD_LOGISTIC: n_local * batch rows (empty: streams)
 
   dsgd_grad_spec c() const {
     const uint32_t mode = noise ? 1u : (device_noise_sigma > 0.0 ? 2u : 0u);
-    return dsgd_grad_spec{source, buffers.empty() ? nullptr : buffers.data(), mode,
-                          grad_norm_out, device_noise_sigma, device_noise_seed};
+    return dsgd_grad_spec{source,        buffers.empty() ? nullptr : buffers.data(),
+                          mode,          grad_norm_out,
+                          device_noise_sigma, device_noise_seed,
+                          rows.empty() ? nullptr : rows.data()};
   }
 };
 
@@ -136,6 +139,24 @@ class Context {
     std::vector<double> v(dim);
     check(dsgd_get_vector(ctx_, local, which, v.data()));
     return v;
+  }
+  // LogisticObjective(features, labels, l2) objectives.cpp:80-106 (features row-major)
+  void set_logistic(const std::vector<std::vector<double>>& features,
+                    const std::vector<int>& labels, double l2) {
+    std::vector<double> flat;
+    for (const auto& r : features) {
+      if (r.size() != features[0].size())
+        throw std::invalid_argument("logistic feature rows have inconsistent width");
+      flat.insert(flat.end(), r.begin(), r.end());
+    }
+    if (features.size() != labels.size())
+      throw std::invalid_argument("logistic features/labels size mismatch");
+    std::vector<int32_t> y(labels.begin(), labels.end());
+    check(dsgd_set_logistic(ctx_, flat.empty() ? nullptr : flat.data(),
+                            y.empty() ? nullptr : y.data(), features.size(), l2));
+  }
+  void set_sample_range(std::uint32_t local, std::uint64_t begin, std::uint64_t end) {
+    check(dsgd_logistic_set_sample_range(ctx_, local, begin, end));
   }
   void sync() { check(dsgd_ctx_sync(ctx_)); }
 

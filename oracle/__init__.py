@@ -45,7 +45,7 @@ class Hyper(C.Structure):
                 ("anneal_at", C.POINTER(C.c_uint64)), ("n_anneal", C.c_uint32),
                 ("mu", C.c_double), ("weight_decay", C.c_double),
                 ("beta_gossip", C.c_double), ("beta_ea", C.c_double),
-                ("tau", C.c_uint32)]
+                ("tau", C.c_uint32), ("batch", C.c_uint32)]
 
 
 class Sim(C.Structure):
@@ -71,11 +71,12 @@ class HyperParams:
     beta_gossip: float = 0.5
     beta_ea: float = 0.1
     tau: int = 1
+    batch: int = 1
 
     def to_c(self) -> Hyper:
         arr = (C.c_uint64 * max(1, len(self.anneal_at)))(*self.anneal_at)
         h = Hyper(self.alpha0, self.anneal_factor, arr, len(self.anneal_at), self.mu,
-                  self.weight_decay, self.beta_gossip, self.beta_ea, self.tau)
+                  self.weight_decay, self.beta_gossip, self.beta_ea, self.tau, self.batch)
         h._keep = arr  # keep the array alive with the struct
         return h
 
@@ -156,7 +157,14 @@ def lib():
         _lib.dsgdo_step_size_at.argtypes = [C.POINTER(Hyper), C.c_uint64]
         _lib.dsgdo_pull_schedule.argtypes = [C.c_uint64, C.c_char_p, C.c_uint32, C.c_uint32,
                                              C.c_uint64, C.c_void_p]
+        _lib.dsgdo_sigmoid.restype = C.c_double
+        _lib.dsgdo_sigmoid.argtypes = [C.c_double]
+        _lib.dsgdo_draw_rows.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32,
+                                         C.c_void_p]
         for sfx in ("f64", "f32"):
+            getattr(_lib, f"dsgdo_logistic_grad_{sfx}").argtypes = [
+                C.c_uint64, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p, C.c_uint32,
+                C.c_void_p, C.c_void_p]
             getattr(_lib, f"dsgdo_run_{sfx}").argtypes = [C.POINTER(Sim), C.c_void_p,
                                                          C.c_void_p, C.c_void_p, C.c_void_p]
             getattr(_lib, f"dsgdo_push_mix_{sfx}").restype = C.c_int
@@ -192,6 +200,10 @@ def ref():
                                    C.c_uint32, C.c_uint32]
         _ref.ref_ring_allreduce.argtypes = [C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p,
                                             C.c_uint64]
+        _ref.ref_set_logistic.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64,
+                                          C.c_double, C.c_void_p, C.c_uint32]
+        _ref.ref_logistic_grad.argtypes = [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint64,
+                                           C.c_uint64, C.c_uint64, C.c_void_p]
         _ref.ref_time_rounds.restype = C.c_double
         _ref.ref_time_rounds.argtypes = [C.c_int, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int,
                                          C.POINTER(Hyper)]
@@ -230,6 +242,12 @@ class Stream:
 
     def uniform_index(self, n: int) -> int:
         return lib().dsgdo_uniform_index(self._buf, n)
+
+    def draw_rows(self, begin: int, end: int, batch: int) -> np.ndarray:
+        """LogisticObjective minibatch rows (objectives.cpp:154-157)."""
+        out = np.zeros(batch, dtype=np.uint64)
+        lib().dsgdo_draw_rows(self._buf, begin, end, batch, _ptr(out))
+        return out
 
 
 def derive_stream_seed(seed: int, run_id: str, node: int, purpose: str) -> int:
@@ -439,8 +457,48 @@ def run(cfg: SimConfig, dtype=np.float64):
     return theta, dprev, t, center
 
 
+def sigmoid(z: float) -> float:
+    """objectives.cpp:34-38"""
+    return lib().dsgdo_sigmoid(z)
+
+
+def logistic_grad(X: np.ndarray, y, l2: float, theta: np.ndarray, rows) -> np.ndarray:
+    """LogisticObjective::stochastic_gradient (objectives.cpp:147-162) restated
+    for given minibatch rows; dtype of X/theta picks fp64 or the fp32 policy."""
+    X = np.ascontiguousarray(X)
+    theta = np.ascontiguousarray(theta, dtype=X.dtype)
+    y = np.ascontiguousarray(y, dtype=np.int32)
+    rows = np.ascontiguousarray(rows, dtype=np.uint64)
+    out = np.zeros(X.shape[1], dtype=X.dtype)
+    getattr(lib(), f"dsgdo_logistic_grad_{_sfx(X.dtype)}")(
+        C.c_uint64(X.shape[1]), _ptr(X), _ptr(y), C.c_double(l2), _ptr(theta),
+        C.c_uint32(len(rows)), _ptr(rows), _ptr(out))
+    return out
+
+
 # --------------------------------------------------------------------------
 # The compiled reference (oracle/_ref)
+def ref_set_logistic(X, y, l2: float, ranges=None):
+    """Install a LogisticObjective dataset for ref_round(obj='logistic') and
+    ref_run (node i samples rows ranges[i]); ref_set_logistic(None, ...) clears."""
+    if X is None:
+        ref().ref_clear_logistic()
+        return
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.int32)
+    rg = None if ranges is None else np.ascontiguousarray(ranges, dtype=np.uint64).reshape(-1)
+    _ref_check(ref().ref_set_logistic(_ptr(X), _ptr(y), X.shape[0], X.shape[1], l2, _ptr(rg),
+                                      0 if rg is None else len(rg) // 2))
+
+
+def ref_logistic_grad(theta, batch: int, sample_seed: int, begin: int, end: int) -> np.ndarray:
+    theta = np.ascontiguousarray(theta, dtype=np.float64)
+    out = np.zeros_like(theta)
+    _ref_check(ref().ref_logistic_grad(_ptr(theta), len(theta), batch, sample_seed, begin, end,
+                                       _ptr(out)))
+    return out
+
+
 def _ref_check(rc):
     if rc != 0:
         raise ValueError(ref().ref_last_error().decode())
@@ -471,7 +529,10 @@ def ref_round(kind: str, nodes: Nodes, h: HyperParams, partner=None, spec=None, 
     """One reference round from explicit state (streams fresh from (seed, run_id))."""
     assert nodes.dtype == np.float64
     kind_id = REF_ROUND[kind]
-    okind, s, o, g = _obj_args(nodes, spec, opt, gfixed)
+    if isinstance(spec, str) and spec == "logistic":  # the dataset of ref_set_logistic
+        okind, s, o, g = 2, None, None, None
+    else:
+        okind, s, o, g = _obj_args(nodes, spec, opt, gfixed)
     pm = None if partner is None else np.ascontiguousarray(partner, dtype=np.uint32)
     hc = h.to_c()
     _ref_check(ref().ref_round(kind_id, nodes.p, nodes.d, _ptr(nodes.theta), _ptr(nodes.dprev),

@@ -165,3 +165,16 @@ void dsgdo_pull_schedule(uint64_t seed, const char* run_id, uint32_t p, uint32_t
 #include "dsgd_oracle_impl.inc"
 #undef R
 #undef SFX
+
+/* ---- LogisticObjective helpers (objectives.cpp:34-38, 147-162) ---- */
+double dsgdo_sigmoid(double z) {
+  if (z >= 0.0) return 1.0 / (1.0 + exp(-z));
+  const double e = exp(z);
+  return e / (1.0 + e);
+}
+
+void dsgdo_draw_rows(dsgdo_rng* sample, uint64_t begin, uint64_t end, uint32_t batch,
+                     uint64_t* rows) {
+  const uint32_t span = (uint32_t)(end - begin);
+  for (uint32_t b = 0; b < batch; ++b) rows[b] = begin + dsgdo_uniform_index(sample, span);
+}

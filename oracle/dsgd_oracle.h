@@ -63,6 +63,7 @@ typedef struct {
   double beta_gossip;
   double beta_ea;
   uint32_t tau;
+  uint32_t batch; /* minibatch size b (core.hpp:63; LogisticObjective only) */
 } dsgdo_hyper;
 
 double dsgdo_step_size_at(const dsgdo_hyper* h, uint64_t t);
@@ -83,7 +84,16 @@ void dsgdo_pull_schedule(uint64_t seed, const char* run_id, uint32_t p, uint32_t
  * kind 1 = fixed gradient (an Objective whose stochastic_gradient returns
  *          a given vector; the plugin slot the GPU's external-gradient mode
  *          fills).  For per-node objectives `grad` is p*d. */
-enum { DSGDO_OBJ_QUADRATIC = 0, DSGDO_OBJ_FIXED = 1 };
+enum { DSGDO_OBJ_QUADRATIC = 0, DSGDO_OBJ_FIXED = 1, DSGDO_OBJ_LOGISTIC = 2 /* ref_shim only */ };
+
+/* ---- LogisticObjective (objectives.cpp:80-162).  Minibatch rows are drawn
+ * by the caller from the node's sample stream, in batch order:
+ *   row = begin + uniform_index(end - begin)          (objectives.cpp:154-157)
+ * dsgdo_draw_rows does exactly that.  The logistic gradient itself is
+ * dsgdo_logistic_grad_{f64,f32} below. */
+void dsgdo_draw_rows(dsgdo_rng* sample, uint64_t begin, uint64_t end, uint32_t batch,
+                     uint64_t* rows);
+double dsgdo_sigmoid(double z);
 
 /* ---- run drivers (simulator.cpp run_sync 214-374 / run_async 380-449) */
 enum {
@@ -160,6 +170,9 @@ typedef struct {
                                     uint32_t i, uint32_t j, int obj_kind, const R* spec,  \
                                     const R* opt, const R* gfixed, const R* noise,        \
                                     const dsgdo_hyper* h);                                \
+  void dsgdo_logistic_grad_##SFX(uint64_t d, const R* X, const int32_t* y, double l2,    \
+                                  const R* theta, uint32_t batch, const uint64_t* rows,   \
+                                  R* out);                                                \
   int dsgdo_run_##SFX(const dsgdo_sim* cfg, R* theta_out, R* dprev_out, uint64_t* t_out, \
                       R* center_out);                                                     \
   void dsgdo_trace_##SFX(uint32_t p, uint64_t d, const R* theta, const R* spec,          \

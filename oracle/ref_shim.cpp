@@ -57,6 +57,7 @@ Hyperparams to_hyper(const dsgdo_hyper& h) {
   out.beta_gossip = h.beta_gossip;
   out.beta_ea = h.beta_ea;
   out.tau = h.tau;
+  out.batch = h.batch == 0 ? 1 : h.batch;
   return out;
 }
 
@@ -102,6 +103,24 @@ SimConfig to_sim(const dsgdo_sim& c) {
   return cfg;
 }
 
+// LogisticObjective dataset for obj_kind DSGDO_OBJ_LOGISTIC (ref_set_logistic);
+// node i samples rows [ranges[2i], ranges[2i+1]) (LogisticObjective::set_sample_range).
+struct LogisticData {
+  bool set = false;
+  std::vector<std::vector<double>> X;
+  std::vector<int> y;
+  double l2 = 0.0;
+  std::vector<std::uint64_t> ranges;
+};
+LogisticData g_logistic;
+
+std::unique_ptr<LogisticObjective> logistic_for(std::uint32_t node) {
+  auto o = std::make_unique<LogisticObjective>(g_logistic.X, g_logistic.y, g_logistic.l2);
+  if (!g_logistic.ranges.empty())
+    o->set_sample_range(g_logistic.ranges[2 * node], g_logistic.ranges[2 * node + 1]);
+  return o;
+}
+
 void export_nodes(const std::vector<NodeState>& nodes, std::uint64_t d, double* theta,
                   double* dprev, std::uint64_t* t) {
   for (std::size_t i = 0; i < nodes.size(); ++i) {
@@ -139,15 +158,71 @@ void ref_stream_draws(std::uint64_t seed, int kind, std::uint32_t n, std::uint64
   }
 }
 
+// LogisticObjective dataset used by ref_round (obj_kind 2) and ref_run while
+// set: X is n*d row-major, labels 0/1, ranges (optional) 2*p sample ranges.
+int ref_set_logistic(const double* X, const std::int32_t* y, std::uint64_t n, std::uint64_t d,
+                     double l2, const std::uint64_t* ranges, std::uint32_t p) {
+  try {
+    g_logistic = LogisticData{};
+    for (std::uint64_t r = 0; r < n; ++r) {
+      g_logistic.X.emplace_back(X + r * d, X + (r + 1) * d);
+      g_logistic.y.push_back(y[r]);
+    }
+    g_logistic.l2 = l2;
+    if (ranges) g_logistic.ranges.assign(ranges, ranges + 2 * p);
+    (void)LogisticObjective(g_logistic.X, g_logistic.y, l2);  // the constructor's checks
+    g_logistic.set = true;
+    return 0;
+  } catch (const std::exception& e) {
+    g_logistic = LogisticData{};
+    g_err = e.what();
+    return -1;
+  }
+}
+
+void ref_clear_logistic() { g_logistic = LogisticData{}; }
+
+// LogisticObjective::stochastic_gradient(theta, batch, RngStream(sample_seed))
+// on rows [begin, end).
+int ref_logistic_grad(const double* theta, std::uint64_t d, std::uint32_t batch,
+                      std::uint64_t sample_seed, std::uint64_t begin, std::uint64_t end,
+                      double* out) {
+  try {
+    LogisticObjective o(g_logistic.X, g_logistic.y, g_logistic.l2);
+    o.set_sample_range(begin, end);
+    RngStream s(sample_seed);
+    const ParamVec g =
+        o.stochastic_gradient(ParamVec(std::vector<double>(theta, theta + d)), batch, s);
+    std::memcpy(out, g.raw(), sizeof(double) * d);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 // Full run through the reference drivers (run_simulation). Returns 0, or -1
 // with ref_last_error() set when the reference throws.
 int ref_run(const dsgdo_sim* c, double* theta, double* dprev, std::uint64_t* t,
             double* center) {
   try {
     const SimConfig cfg = to_sim(*c);
-    QuadraticObjective obj(std::vector<double>(c->spectrum, c->spectrum + c->d),
-                           ParamVec(std::vector<double>(c->opt, c->opt + c->d)));
-    const RunResult r = run_simulation(cfg, obj);
+    RunResult r;
+    if (g_logistic.set) {  // sharded logistic objectives (runner.cpp:100-115 shape)
+      LogisticObjective eval(g_logistic.X, g_logistic.y, g_logistic.l2);
+      std::vector<std::unique_ptr<LogisticObjective>> own;
+      std::vector<const Objective*> objs;
+      for (std::uint32_t i = 0; i < c->p; ++i) {
+        own.push_back(logistic_for(i));
+        objs.push_back(own.back().get());
+      }
+      r = (cfg.clock.kind == ClockModel::Kind::kPoisson) ? run_async(cfg, eval, objs)
+                                                         : run_sync(cfg, eval, objs);
+    } else {
+      QuadraticObjective obj(std::vector<double>(c->spectrum, c->spectrum + c->d),
+                             ParamVec(std::vector<double>(c->opt, c->opt + c->d)));
+      r = run_simulation(cfg, obj);
+    }
     export_nodes(r.final_nodes, c->d, theta, dprev, t);
     if (center && r.final_server) {
       std::memcpy(center, r.final_server->theta_center.raw(), sizeof(double) * c->d);
@@ -204,6 +279,8 @@ int ref_round(int protocol, std::uint32_t p, std::uint64_t d, double* theta, dou
       if (obj_kind == DSGDO_OBJ_QUADRATIC) {
         own.push_back(std::make_unique<QuadraticObjective>(
             std::vector<double>(spec, spec + d), ParamVec(std::vector<double>(opt, opt + d))));
+      } else if (obj_kind == DSGDO_OBJ_LOGISTIC) {
+        own.push_back(logistic_for(i));
       } else {
         own.push_back(std::make_unique<FixedGradientObjective>(
             std::vector<double>(gfixed + i * d, gfixed + (i + 1) * d)));

@@ -21,7 +21,7 @@ PURPOSE = {"gradient-noise": 0, "sample": 1, "partner-choice": 2, "clock": 3,
            "straggler": 4, "init": 5}
 CTX_QUADRATIC, CTX_GRAD, CTX_NOISE, CTX_CENTER = 1, 2, 4, 8
 BUF_THETA, BUF_DELTA, BUF_GRAD, BUF_NOISE, BUF_SPECTRUM, BUF_OPT, BUF_CENTER = range(7)
-GRAD_QUADRATIC, GRAD_BUFFER = 0, 1
+GRAD_QUADRATIC, GRAD_BUFFER, GRAD_LOGISTIC = 0, 1, 2
 K_STEP, K_ALLREDUCE, K_AR_DELTA, K_AR_APPLY, K_NCCL, K_EA, K_PUSH, K_OTHER = range(8)
 KERNEL_NAMES = ["step", "allreduce_local", "ar_delta", "ar_apply", "allreduce_comm",
                 "ea", "push", "other"]
@@ -59,7 +59,8 @@ class CtxDesc(C.Structure):
 class GradSpec(C.Structure):
     _fields_ = [("source", C.c_int), ("grad", C.POINTER(C.c_void_p)),
                 ("use_noise", C.c_uint32), ("grad_norm_out", C.POINTER(C.c_double)),
-                ("noise_sigma", C.c_double), ("noise_seed", C.c_uint64)]
+                ("noise_sigma", C.c_double), ("noise_seed", C.c_uint64),
+                ("rows", C.POINTER(C.c_uint64))]
 
 
 class RunDesc(C.Structure):
@@ -102,6 +103,8 @@ _SIGS = {
     "dsgd_get_state": (C.c_int, [_P, C.c_uint32, _P, _P, _U64P]),
     "dsgd_set_vector": (C.c_int, [_P, C.c_uint32, C.c_int, _P]),
     "dsgd_get_vector": (C.c_int, [_P, C.c_uint32, C.c_int, _P]),
+    "dsgd_set_logistic": (C.c_int, [_P, _P, _P, C.c_uint64, C.c_double]),
+    "dsgd_logistic_set_sample_range": (C.c_int, [_P, C.c_uint32, C.c_uint64, C.c_uint64]),
     "dsgd_upload_async": (C.c_int, [_P, C.c_uint32, C.c_int, _P, C.c_uint64]),
     "dsgd_download_async": (C.c_int, [_P, C.c_uint32, C.c_int, _P, C.c_uint64]),
     "dsgd_copy_in_async": (C.c_int, [_P, C.c_uint32, C.c_int, _P, C.c_uint64]),

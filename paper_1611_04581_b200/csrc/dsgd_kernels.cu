@@ -1466,7 +1466,10 @@ cudaError_t launch_allreduce_local(const AllreduceArgs<T>& a, int vec, int norm,
 // coordinate the center is one register carried through the clients in node
 // order -- u = beta*(theta_i - c); theta_i -= u; SGD step; c += u
 // (protocols.cpp:148-151, 156) -- so the serial server order costs nothing.
-template <typename T, bool VEC, bool NORM>
+// MIX: the client/server half only (theta_i -= u, c += u, no SGD step): the
+// logistic gradient source evaluates its minibatch gradient at the moved
+// theta before the step (a global dot product per row).
+template <typename T, bool VEC, bool NORM, bool MIX = false>
 __global__ void __launch_bounds__(kBlock) k_ea_local(const __grid_constant__ EaArgs<T> a) {
   using L = Lanes<T, VEC>;
   constexpr int W = L::W;
@@ -1483,6 +1486,18 @@ __global__ void __launch_bounds__(kBlock) k_ea_local(const __grid_constant__ EaA
       const NodeIO<T>& n = a.node[i];
       L x, dp, gb, s, o, xi, ot, od, uo;
       ld(x, n.theta_in, k);
+      if constexpr (MIX) {
+#pragma unroll
+        for (int l = 0; l < W; ++l) {
+          const T u = rmul(a.beta, rsub(x.v[l], c.v[l]));
+          ot.v[l] = rsub(x.v[l], u);
+          uo.v[l] = u;
+          c.v[l] = radd(c.v[l], u);
+        }
+        st(n.theta_out, k, ot);
+        if (n.aux) st(n.aux, k, uo);
+        continue;
+      }
       ld(dp, n.delta, k);
       ld_grad_inputs(gb, s, o, xi, n, a.spec, a.opt, a.quad, k);
       double dummy = 0.0;
@@ -1512,7 +1527,12 @@ __global__ void __launch_bounds__(kBlock) k_ea_local(const __grid_constant__ EaA
 }
 
 template <typename T>
-cudaError_t launch_ea_local(const EaArgs<T>& a, int vec, int norm, uint32_t grid, cudaStream_t s) {
+cudaError_t launch_ea_local(const EaArgs<T>& a, int vec, int norm, uint32_t grid, cudaStream_t s,
+                            bool mix_only) {
+  if (mix_only) {  // gated client/server half only (the gradient comes later)
+    k_ea_local<T, false, false, true><<<grid, kBlock, 0, s>>>(a);
+    return cudaGetLastError();
+  }
   if (vec) {
     if (norm)
       k_ea_local<T, true, true><<<grid, kBlock, 0, s>>>(a);
@@ -1624,7 +1644,7 @@ cudaError_t launch_push(const PushArgs<T>& a, int vec, uint32_t grid, cudaStream
 // center of this chunk into our c_in, run the client update + step, forward
 // the center to the next rank over NVLink and publish the chunk flag.  The
 // per-coordinate operation order is the single-context sweep's exactly.
-template <typename T, bool VEC>
+template <typename T, bool VEC, bool MIX = false>
 __global__ void __launch_bounds__(kBlock) k_ea_chain(const __grid_constant__ EaChainArgs<T> a) {
   __shared__ int ok;
   const NodeIO<T>& n = a.node;
@@ -1646,6 +1666,11 @@ __global__ void __launch_bounds__(kBlock) k_ea_chain(const __grid_constant__ EaC
             T xv = n.theta_in[kk];
             const T u = rmul(a.beta, rsub(xv, cv0));
             xv = rsub(xv, u);
+            if constexpr (MIX) {
+              n.theta_out[kk] = xv;
+              a.c_out[kk] = radd(cv0, u);
+              continue;
+            }
             const T gb = a.quad ? T(0) : n.grad[kk];
             const T sv = a.quad ? a.spec[kk] : T(0), ov = a.quad ? a.opt[kk] : T(0);
             const T xiv = noise_at(n, kk);
@@ -1662,6 +1687,17 @@ __global__ void __launch_bounds__(kBlock) k_ea_chain(const __grid_constant__ EaC
       L cv, x, dp, gb, s, o, xi, ot, od;
       ld(cv, a.c_in, k);
       ld(x, n.theta_in, k);
+      if constexpr (MIX) {
+#pragma unroll
+        for (int l = 0; l < W; ++l) {
+          const T u = rmul(a.beta, rsub(x.v[l], cv.v[l]));
+          ot.v[l] = rsub(x.v[l], u);
+          cv.v[l] = radd(cv.v[l], u);
+        }
+        st(n.theta_out, k, ot);
+        st(a.c_out, k, cv);
+        continue;
+      }
       ld(dp, n.delta, k);
       ld_grad_inputs(gb, s, o, xi, n, a.spec, a.opt, a.quad, k);
 #pragma unroll
@@ -1688,11 +1724,102 @@ __global__ void __launch_bounds__(kBlock) k_ea_chain(const __grid_constant__ EaC
 }
 
 template <typename T>
-cudaError_t launch_ea_chain(const EaChainArgs<T>& a, int vec, uint32_t grid, cudaStream_t s) {
+cudaError_t launch_ea_chain(const EaChainArgs<T>& a, int vec, uint32_t grid, cudaStream_t s,
+                            bool mix_only) {
+  if (mix_only) {
+    if (vec)
+      k_ea_chain<T, true, true><<<grid, kBlock, 0, s>>>(a);
+    else
+      k_ea_chain<T, false, true><<<grid, kBlock, 0, s>>>(a);
+    return cudaGetLastError();
+  }
   if (vec)
     k_ea_chain<T, true><<<grid, kBlock, 0, s>>>(a);
   else
     k_ea_chain<T, false><<<grid, kBlock, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------- logistic gradient source
+// LogisticObjective::stochastic_gradient objectives.cpp:147-162 in three
+// launches.  (1) per (node, row) and per slice of d: partial dot products
+// z = sum_k x_k * la_k in fp64 (products of two context-dtype values are
+// exact in fp64); (2) per (node, row): the slices summed in a fixed order
+// (deterministic run to run; the reference sums k sequentially, so fp64 z
+// agrees to rounding, not bitwise), coeff = sigmoid(z) - y (34-38, 131);
+// (3) elementwise in the reference order: g = 0; g += coeff_b * x_b over b
+// (132-133, 155); g *= 1/batch (158); g += l2 * la (159).
+template <typename T>
+__device__ __forceinline__ T logistic_point(const LogisticArgs<T>& a, uint32_t n, uint64_t k) {
+  const T x = a.theta[n][k];
+  return a.lookahead ? radd(x, rmul(a.mu, a.delta[n][k])) : x;
+}
+
+__device__ __forceinline__ double block_sum_fixed(double v) {
+  __shared__ double red[kBlock / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+  return s;  // valid in thread 0
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_logit_partial(const __grid_constant__ LogisticArgs<T> a) {
+  const uint32_t r = blockIdx.y;          // node * batch + b
+  const uint32_t n = r / a.batch;
+  const T* x = a.X + a.rows[r] * a.d;
+  const uint64_t span = (a.d + a.nblk - 1) / a.nblk;
+  const uint64_t lo = (uint64_t)blockIdx.x * span;
+  const uint64_t hi = lo + span < a.d ? lo + span : a.d;
+  double acc = 0.0;
+  for (uint64_t k = lo + threadIdx.x; k < hi; k += blockDim.x)
+    acc += (double)x[k] * (double)logistic_point(a, n, k);
+  const double s = block_sum_fixed(acc);
+  if (threadIdx.x == 0) a.partial[(uint64_t)r * a.nblk + blockIdx.x] = s;
+}
+
+__device__ __forceinline__ double sigmoid_ref(double z) {
+  if (z >= 0.0) return 1.0 / (1.0 + exp(-z));
+  const double e = exp(z);
+  return e / (1.0 + e);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(32) k_logit_coeff(const __grid_constant__ LogisticArgs<T> a) {
+  const uint32_t r = blockIdx.x;
+  double v = 0.0;
+  for (uint32_t b = threadIdx.x; b < a.nblk; b += 32) v += a.partial[(uint64_t)r * a.nblk + b];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (threadIdx.x == 0) a.coeff[r] = sigmoid_ref(v) - (double)a.y[a.rows[r]];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_logistic_grad(const __grid_constant__ LogisticArgs<T> a) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < a.d; k += stride) {
+    for (uint32_t n = 0; n < a.n_nodes; ++n) {
+      T g = T(0);
+      for (uint32_t b = 0; b < a.batch; ++b) {
+        const uint32_t r = n * a.batch + b;
+        g = radd(g, rmul((T)a.coeff[r], a.X[a.rows[r] * a.d + k]));
+      }
+      g = rmul(g, a.inv_batch);
+      a.out[n][k] = radd(g, rmul(a.l2, logistic_point(a, n, k)));
+    }
+  }
+}
+
+template <typename T>
+cudaError_t launch_logistic(const LogisticArgs<T>& a, uint32_t grid, cudaStream_t s) {
+  const uint32_t nr = a.n_nodes * a.batch;
+  k_logit_partial<T><<<dim3(a.nblk, nr), kBlock, 0, s>>>(a);
+  k_logit_coeff<T><<<nr, 32, 0, s>>>(a);
+  k_logistic_grad<T><<<grid, kBlock, 0, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -1809,9 +1936,12 @@ cudaError_t launch_fill_normal(T* out, uint64_t n, double sigma, uint64_t seed, 
   template cudaError_t launch_step<T>(int, const StepArgs<T>&, int, uint32_t, cudaStream_t);       \
   template cudaError_t launch_allreduce_local<T>(const AllreduceArgs<T>&, int, int, uint32_t,      \
                                                  cudaStream_t);                                    \
-  template cudaError_t launch_ea_local<T>(const EaArgs<T>&, int, int, uint32_t, cudaStream_t);     \
+  template cudaError_t launch_ea_local<T>(const EaArgs<T>&, int, int, uint32_t, cudaStream_t,      \
+                                          bool);                                                   \
+  template cudaError_t launch_logistic<T>(const LogisticArgs<T>&, uint32_t, cudaStream_t);         \
   template cudaError_t launch_push<T>(const PushArgs<T>&, int, uint32_t, cudaStream_t);            \
-  template cudaError_t launch_ea_chain<T>(const EaChainArgs<T>&, int, uint32_t, cudaStream_t);     \
+  template cudaError_t launch_ea_chain<T>(const EaChainArgs<T>&, int, uint32_t, cudaStream_t,      \
+                                          bool);                                                   \
   template cudaError_t launch_ar_reduce<T>(const ArReduceArgs<T>&, uint32_t, cudaStream_t);        \
   template cudaError_t launch_trace<T>(const TraceArgs<T>&, uint32_t, cudaStream_t);               \
   template cudaError_t launch_ar_oneshot<T>(const ArOneShotArgs<T>&, int, uint32_t, cudaStream_t); \

@@ -176,6 +176,25 @@ struct PushArgs {
 // its client update + SGD step, and forwards the center to the next rank.
 constexpr uint64_t kEaChunk = 1024;  // elements per chunk (kBlock * 4)
 
+// LogisticObjective::stochastic_gradient (objectives.cpp:147-162) for a set
+// of local nodes: node n's minibatch rows are rows[n * batch + b]; its
+// evaluation point is theta[n] (+ mu * delta[n] when lookahead).
+template <typename T>
+struct LogisticArgs {
+  const T* X;                 // n_samples x d, row-major
+  const int32_t* y;           // labels 0/1
+  const T* theta[kMaxLocal];
+  const T* delta[kMaxLocal];
+  T* out[kMaxLocal];          // the node's gradient buffer
+  const uint64_t* rows;       // device, n_nodes * batch
+  double* partial;            // n_nodes * batch * nblk partial dot products
+  double* coeff;              // n_nodes * batch: sigmoid(z) - y
+  uint64_t d;
+  uint32_t n_nodes, batch, nblk;
+  T mu, l2, inv_batch;
+  int lookahead;
+};
+
 template <typename T>
 struct EaChainArgs {
   NodeIO<T> node;
@@ -203,11 +222,15 @@ template <typename T>
 cudaError_t launch_allreduce_local(const AllreduceArgs<T>& a, int vec, int norm, uint32_t grid,
                                    cudaStream_t s);
 template <typename T>
-cudaError_t launch_ea_local(const EaArgs<T>& a, int vec, int norm, uint32_t grid, cudaStream_t s);
+cudaError_t launch_ea_local(const EaArgs<T>& a, int vec, int norm, uint32_t grid, cudaStream_t s,
+                            bool mix_only = false);
+template <typename T>
+cudaError_t launch_logistic(const LogisticArgs<T>& a, uint32_t grid, cudaStream_t s);
 template <typename T>
 cudaError_t launch_push(const PushArgs<T>& a, int vec, uint32_t grid, cudaStream_t s);
 template <typename T>
-cudaError_t launch_ea_chain(const EaChainArgs<T>& a, int vec, uint32_t grid, cudaStream_t s);
+cudaError_t launch_ea_chain(const EaChainArgs<T>& a, int vec, uint32_t grid, cudaStream_t s,
+                            bool mix_only = false);
 template <typename T>
 cudaError_t launch_ar_reduce(const ArReduceArgs<T>& a, uint32_t grid, cudaStream_t s);
 template <typename T>

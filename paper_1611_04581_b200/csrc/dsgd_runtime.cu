@@ -196,9 +196,21 @@ struct dsgd_ctx {
   std::vector<void*> ipc_opened;
   ncclComm_t comm = nullptr;
 
+  // LogisticObjective dataset (dsgd_set_logistic), replicated per context
+  char* lg_X = nullptr;                       // n x d, context dtype
+  int32_t* lg_y = nullptr;
+  uint64_t lg_n = 0;
+  double lg_l2 = 0.0;
+  std::vector<uint64_t> lg_begin, lg_end;     // per local node sample range
+  uint64_t* lg_rows = nullptr;                // device minibatch rows
+  double* lg_scratch = nullptr;               // partial dots + coefficients
+  size_t lg_rows_cap = 0, lg_scratch_cap = 0;
+  std::vector<uint64_t> lg_rows_host;
+
   // worker-loop streams
   std::vector<dsgd_stream*> partner_streams;  // all p (every context draws the full map)
   std::vector<dsgd_stream*> noise_streams;    // local nodes
+  std::vector<dsgd_stream*> sample_streams;   // local nodes (logistic minibatch rows)
   double* noise_host = nullptr;               // d doubles
 
   // measurement
@@ -291,6 +303,8 @@ T* as(char* p) {
 // Resolved gradient source for one launch.
 struct GradSel {
   int quad = 0;
+  bool logistic = false;          // produce the gradient into c->grad first
+  const uint64_t* rows = nullptr; // caller-drawn logistic rows (host), or null
   const void* grad[kMaxLocal] = {};
   bool noise = false;
   bool norm = false;
@@ -310,6 +324,11 @@ dsgd_status resolve_grad(dsgd_ctx* c, const dsgd_grad_spec* g, GradSel* out) {
       s.grad[i] = g->grad ? g->grad[i] : c->grad[i];
       if (!s.grad[i]) return set_error(DSGD_EINVAL, "missing gradient buffer");
     }
+  } else if (g->source == DSGD_GRAD_LOGISTIC) {
+    if (!c->lg_X) return set_error(DSGD_ESTATE, "no logistic dataset (dsgd_set_logistic)");
+    s.logistic = true;
+    s.rows = g->rows;
+    for (uint32_t i = 0; i < c->n_local; ++i) s.grad[i] = c->grad[i];
   } else {
     return set_error(DSGD_EINVAL, "unknown gradient source");
   }
@@ -485,6 +504,88 @@ dsgd_status run_step_mode(dsgd_ctx* c, int mode, int kid, const dsgd_hyperparams
   DSGD_CUDA(dsgd::launch_step<T>(mode, a, vec ? 1 : 0, grid, c->stream));
   if (c->distributed()) c->seq += 1;
   return DSGD_OK;
+}
+
+// LogisticObjective::stochastic_gradient (objectives.cpp:147-162) of the
+// local nodes `nodes` at theta[cur] (+ mu * delta_prev when lookahead, the
+// compute_local_delta evaluation point protocols.cpp:90-93), written into
+// their gradient buffers.  Rows come from the caller (gs.rows) or from each
+// node's sample stream, in batch order (objectives.cpp:154-157).
+template <typename T>
+dsgd_status produce_logistic(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& gs,
+                             const std::vector<uint32_t>& nodes, bool lookahead) {
+  if (!gs.logistic || nodes.empty()) return DSGD_OK;
+  const uint32_t B = h->batch;
+  if (B == 0) return set_error(DSGD_EINVAL, "batch must be >= 1");
+  const uint32_t nn = (uint32_t)nodes.size();
+  c->lg_rows_host.resize((size_t)nn * B);
+  for (uint32_t q = 0; q < nn; ++q) {
+    const uint32_t i = nodes[q];
+    for (uint32_t b = 0; b < B; ++b) {
+      uint64_t row;
+      if (gs.rows) {
+        row = gs.rows[(size_t)i * B + b];
+        if (row >= c->lg_n) return set_error(DSGD_EINVAL, "logistic row out of range");
+      } else {
+        if (c->sample_streams.size() != c->n_local)
+          return set_error(DSGD_ESTATE, "dsgd_ctx_seed_streams first");
+        uint32_t j = 0;
+        DSGD_TRY(dsgd_stream_uniform_index(c->sample_streams[i],
+                                           (uint32_t)(c->lg_end[i] - c->lg_begin[i]), &j));
+        row = c->lg_begin[i] + j;
+      }
+      c->lg_rows_host[(size_t)q * B + b] = row;
+    }
+  }
+  const uint32_t nblk = (uint32_t)std::min<uint64_t>(
+      64, std::max<uint64_t>(1, (c->d + 8 * kBlockU - 1) / (8 * kBlockU)));
+  const size_t nr = (size_t)nn * B;
+  if (c->lg_rows_cap < nr) {
+    cudaFree(c->lg_rows);
+    c->lg_rows = nullptr;
+    DSGD_CUDA(cudaMalloc(&c->lg_rows, nr * sizeof(uint64_t)));
+    c->lg_rows_cap = nr;
+  }
+  if (c->lg_scratch_cap < nr * (nblk + 1)) {
+    cudaFree(c->lg_scratch);
+    c->lg_scratch = nullptr;
+    DSGD_CUDA(cudaMalloc(&c->lg_scratch, nr * (nblk + 1) * sizeof(double)));
+    c->lg_scratch_cap = nr * (nblk + 1);
+  }
+  // pageable source: the copy is staged before the call returns, so the
+  // host vector can be refilled next round
+  DSGD_CUDA(cudaMemcpyAsync(c->lg_rows, c->lg_rows_host.data(), nr * sizeof(uint64_t),
+                            cudaMemcpyHostToDevice, c->stream));
+  dsgd::LogisticArgs<T> a{};
+  a.X = as<T>(c->lg_X);
+  a.y = c->lg_y;
+  for (uint32_t q = 0; q < nn; ++q) {
+    const uint32_t i = nodes[q];
+    a.theta[q] = as<T>(c->theta_ptr(i, c->cur));
+    a.delta[q] = as<T>(c->delta[i]);
+    a.out[q] = as<T>(c->grad[i]);
+  }
+  a.rows = c->lg_rows;
+  a.partial = c->lg_scratch;
+  a.coeff = c->lg_scratch + nr * nblk;
+  a.d = c->d;
+  a.n_nodes = nn;
+  a.batch = B;
+  a.nblk = nblk;
+  a.mu = (T)h->mu;
+  a.l2 = (T)c->lg_l2;
+  a.inv_batch = (T)(1.0 / (double)B);
+  a.lookahead = lookahead && h->mu != 0.0;
+  LaunchScope ls(c, DSGD_K_OTHER);
+  DSGD_CUDA(dsgd::launch_logistic<T>(a, blocks_for(c, c->d, 1), c->stream));
+  c->kernels += 2;  // three launches under one scope
+  return DSGD_OK;
+}
+
+std::vector<uint32_t> all_local(const dsgd_ctx* c) {
+  std::vector<uint32_t> v(c->n_local);
+  for (uint32_t i = 0; i < c->n_local; ++i) v[i] = i;
+  return v;
 }
 
 template <typename T>
@@ -840,7 +941,8 @@ dsgd_status do_allreduce(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& 
 }
 
 template <typename T>
-dsgd_status do_ea(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& gs, int gated) {
+dsgd_status do_ea(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& gs, int gated,
+                  bool mix_only = false) {
   if (!c->distributed()) {
     if (!(c->flags & DSGD_CTX_CENTER)) return set_error(DSGD_ESTATE, "no center (DSGD_CTX_CENTER)");
     dsgd::EaArgs<T> a{};
@@ -857,7 +959,7 @@ dsgd_status do_ea(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& gs, int
     const uint64_t W = vec ? 16 / sizeof(T) : 1;
     const uint32_t grid = blocks_for(c, c->d / W, 1);
     LaunchScope ls(c, DSGD_K_EA);
-    DSGD_CUDA(dsgd::launch_ea_local<T>(a, vec, gs.norm, grid, c->stream));
+    DSGD_CUDA(dsgd::launch_ea_local<T>(a, vec, gs.norm, grid, c->stream, mix_only));
     c->prev_readers.clear();
     return DSGD_OK;
   }
@@ -894,7 +996,7 @@ dsgd_status do_ea(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& gs, int
   // the order the previous rank produces them)
   const uint32_t grid = (uint32_t)std::min<uint64_t>(a.n_chunks, 0x7fffffffu);
   LaunchScope ls(c, DSGD_K_EA);
-  DSGD_CUDA(dsgd::launch_ea_chain<T>(a, vec, grid, c->stream));
+  DSGD_CUDA(dsgd::launch_ea_chain<T>(a, vec, grid, c->stream, mix_only));
   c->prev_readers.clear();
   return DSGD_OK;
 }
@@ -1157,7 +1259,12 @@ void dsgd_ctx_destroy(dsgd_ctx* c) {
   cudaFree(c->arena);
   for (auto* s : c->partner_streams) dsgd_stream_destroy(s);
   for (auto* s : c->noise_streams) dsgd_stream_destroy(s);
+  for (auto* s : c->sample_streams) dsgd_stream_destroy(s);
   delete[] c->noise_host;
+  cudaFree(c->lg_X);
+  cudaFree(c->lg_y);
+  cudaFree(c->lg_rows);
+  cudaFree(c->lg_scratch);
   for (const Prof& p : c->prof_pending) {
     cudaEventDestroy(p.a);
     cudaEventDestroy(p.b);
@@ -1243,6 +1350,52 @@ dsgd_status dsgd_set_vector(dsgd_ctx* c, uint32_t local, dsgd_buffer which, cons
   return upload_vec(c, p, host);
 }
 
+dsgd_status dsgd_set_logistic(dsgd_ctx* c, const double* features, const int32_t* labels,
+                              uint64_t n_samples, double l2) {
+  DSGD_TRY(check_ctx(c));
+  // the LogisticObjective constructor's checks, objectives.cpp:83-101
+  if (n_samples == 0 || !features || !labels)
+    return set_error(DSGD_EINVAL, "logistic dataset is empty");
+  if (!(l2 > 0.0))
+    return set_error(DSGD_EINVAL, "logistic l2 must be positive (strong convexity)");
+  for (uint64_t r = 0; r < n_samples; ++r)
+    if (labels[r] != 0 && labels[r] != 1)
+      return set_error(DSGD_EINVAL, "logistic labels must be 0 or 1");
+  DeviceGuard g(c->device);
+  DSGD_CUDA(cudaStreamSynchronize(c->stream));
+  const size_t vb = c->d * c->es;
+  for (uint32_t i = 0; i < c->n_local; ++i)
+    if (!c->grad[i]) {  // the produced gradient lands in the node's gradient buffer
+      DSGD_CUDA(cudaMalloc(&c->grad[i], vb));
+      DSGD_CUDA(cudaMemset(c->grad[i], 0, vb));
+    }
+  cudaFree(c->lg_X);
+  cudaFree(c->lg_y);
+  c->lg_X = nullptr;
+  c->lg_y = nullptr;
+  DSGD_CUDA(cudaMalloc(&c->lg_X, n_samples * vb));
+  DSGD_CUDA(cudaMalloc(&c->lg_y, n_samples * sizeof(int32_t)));
+  for (uint64_t r = 0; r < n_samples; ++r)
+    DSGD_TRY(upload_vec(c, c->lg_X + r * vb, features + r * c->d));
+  DSGD_CUDA(cudaMemcpy(c->lg_y, labels, n_samples * sizeof(int32_t), cudaMemcpyHostToDevice));
+  c->lg_n = n_samples;
+  c->lg_l2 = l2;
+  c->lg_begin.assign(c->n_local, 0);
+  c->lg_end.assign(c->n_local, n_samples);
+  return DSGD_OK;
+}
+
+dsgd_status dsgd_logistic_set_sample_range(dsgd_ctx* c, uint32_t local, uint64_t begin,
+                                           uint64_t end) {
+  DSGD_TRY(check_ctx(c));
+  if (!c->lg_X) return set_error(DSGD_ESTATE, "no logistic dataset (dsgd_set_logistic)");
+  if (local >= c->n_local) return set_error(DSGD_EINVAL, "local node out of range");
+  if (begin >= end || end > c->lg_n) return set_error(DSGD_EINVAL, "invalid sample range");
+  c->lg_begin[local] = begin;
+  c->lg_end[local] = end;
+  return DSGD_OK;
+}
+
 dsgd_status dsgd_get_vector(dsgd_ctx* c, uint32_t local, dsgd_buffer which, double* host) {
   DSGD_TRY(check_ctx(c));
   if (which == DSGD_BUF_THETA || which == DSGD_BUF_DELTA) DSGD_TRY(flush_pending(c));
@@ -1314,6 +1467,7 @@ dsgd_status dsgd_local_sgd_step(dsgd_ctx* c, const dsgd_hyperparams* h, const ds
   return dispatch(c, [&](auto z) -> dsgd_status {
     using T = decltype(z);
     DSGD_TRY(norm_begin(c, gs));
+    DSGD_TRY(produce_logistic<T>(c, h, gs, all_local(c), true));
     DSGD_TRY(do_local_step<T>(c, h, gs));
     finish_round(c, true);
     return norm_end(c, gs, g);
@@ -1328,9 +1482,11 @@ dsgd_status dsgd_allreduce_round(dsgd_ctx* c, const dsgd_hyperparams* h, const d
   DSGD_TRY(check_common_round(c));
   GradSel gs;
   DSGD_TRY(resolve_grad(c, g, &gs));
+  if (gs.logistic) DSGD_TRY(flush_pending(c));  // the gradient reads the applied theta
   return dispatch(c, [&](auto z) -> dsgd_status {
     using T = decltype(z);
     DSGD_TRY(norm_begin(c, gs));
+    DSGD_TRY(produce_logistic<T>(c, h, gs, all_local(c), true));
     DSGD_TRY(do_allreduce<T>(c, h, gs, scope));
     finish_round(c, !c->distributed());  // multi-GPU: do_allreduce tracks the buffers
     return norm_end(c, gs, g);
@@ -1348,7 +1504,18 @@ dsgd_status dsgd_ea_round(dsgd_ctx* c, const dsgd_hyperparams* h, const dsgd_gra
   return dispatch(c, [&](auto z) -> dsgd_status {
     using T = decltype(z);
     DSGD_TRY(norm_begin(c, gs));
-    DSGD_TRY(do_ea<T>(c, h, gs, gated));
+    if (gs.logistic && gated) {
+      // client/server half, then the minibatch gradient at the moved theta,
+      // then the step (ea_client_step protocols.cpp:146-151)
+      DSGD_TRY(do_ea<T>(c, h, gs, gated, true));
+      finish_round(c, true, false);
+      c->rounds_done -= 1;
+      DSGD_TRY(produce_logistic<T>(c, h, gs, all_local(c), true));
+      DSGD_TRY(do_local_step<T>(c, h, gs));
+    } else {
+      DSGD_TRY(produce_logistic<T>(c, h, gs, all_local(c), true));
+      DSGD_TRY(do_ea<T>(c, h, gs, gated));
+    }
     finish_round(c, true);
     return norm_end(c, gs, g);
   });
@@ -1367,10 +1534,20 @@ dsgd_status dsgd_pull_gossip_round(dsgd_ctx* c, const dsgd_hyperparams* h,
   return dispatch(c, [&](auto z) -> dsgd_status {
     using T = decltype(z);
     DSGD_TRY(norm_begin(c, gs));
-    if (partner_of)
-      DSGD_TRY(do_pull<T>(c, h, gs, partner_of, dsgd::kModePull, T(0.5)));
-    else
+    if (partner_of && gs.logistic) {
+      // pull_mix, then the minibatch gradient at the mixed theta, then the
+      // step (protocols.cpp:173-185)
+      DSGD_TRY(do_pull<T>(c, nullptr, gs, partner_of, dsgd::kModeMix, T(0.5)));
+      finish_round(c, true, false);
+      c->rounds_done -= 1;
+      DSGD_TRY(produce_logistic<T>(c, h, gs, all_local(c), true));
       DSGD_TRY(do_local_step<T>(c, h, gs));
+    } else if (partner_of) {
+      DSGD_TRY(do_pull<T>(c, h, gs, partner_of, dsgd::kModePull, T(0.5)));
+    } else {
+      DSGD_TRY(produce_logistic<T>(c, h, gs, all_local(c), true));
+      DSGD_TRY(do_local_step<T>(c, h, gs));
+    }
     finish_round(c, true);
     return norm_end(c, gs, g);
   });
@@ -1391,7 +1568,15 @@ dsgd_status dsgd_push_gossip_round(dsgd_ctx* c, const dsgd_hyperparams* h,
   return dispatch(c, [&](auto z) -> dsgd_status {
     using T = decltype(z);
     DSGD_TRY(norm_begin(c, gs));
-    DSGD_TRY(do_push<T>(c, h, &gs, target_of));
+    if (gs.logistic) {  // push_mix, gradient at the mixed theta, step (230-242)
+      DSGD_TRY(do_push<T>(c, nullptr, nullptr, target_of));
+      finish_round(c, true, false);
+      c->rounds_done -= 1;
+      DSGD_TRY(produce_logistic<T>(c, h, gs, all_local(c), true));
+      DSGD_TRY(do_local_step<T>(c, h, gs));
+    } else {
+      DSGD_TRY(do_push<T>(c, h, &gs, target_of));
+    }
     finish_round(c, true);
     return norm_end(c, gs, g);
   });
@@ -1409,6 +1594,7 @@ dsgd_status dsgd_gossip_stale_round(dsgd_ctx* c, const dsgd_hyperparams* h,
   return dispatch(c, [&](auto z) -> dsgd_status {
     using T = decltype(z);
     DSGD_TRY(norm_begin(c, gs));
+    DSGD_TRY(produce_logistic<T>(c, h, gs, all_local(c), true));
     DSGD_TRY(do_pull<T>(c, h, gs, partner_of, dsgd::kModeStale, (T)h->beta_gossip));
     finish_round(c, true);
     return norm_end(c, gs, g);
@@ -1429,6 +1615,7 @@ dsgd_status dsgd_gossip_fresh_round(dsgd_ctx* c, const dsgd_hyperparams* h,
     DSGD_TRY(norm_begin(c, gs));
     // every node steps (theta' into the other buffer), then mixes with the
     // partner's post-step theta' (simulator.cpp:305-319)
+    DSGD_TRY(produce_logistic<T>(c, h, gs, all_local(c), true));
     DSGD_TRY(do_local_step<T>(c, h, gs));
     finish_round(c, true, true);
     c->rounds_done -= 1;
@@ -1451,6 +1638,8 @@ dsgd_status dsgd_async_pull_event(dsgd_ctx* c, const dsgd_hyperparams* h,
   return dispatch(c, [&](auto z) -> dsgd_status {
     using T = decltype(z);
     DSGD_TRY(norm_begin(c, gs));
+    // model_gradient at theta_i itself (protocols.cpp:287: no lookahead)
+    DSGD_TRY(produce_logistic<T>(c, h, gs, {i}, false));
     // in place on node i (only node i changes; j == i reads the pre-event value)
     dsgd::StepArgs<T> a{};
     fill_node<T>(c, i, gs, h, &a.node[0], true);
@@ -1581,6 +1770,12 @@ dsgd_status dsgd_ea_client_event(dsgd_ctx* c, const dsgd_hyperparams* h,
     a.p = 1;
     const bool vec = gs.quad || aligned16(gs.grad[i]);
     const uint64_t W = vec ? 16 / sizeof(T) : 1;
+    if (gs.logistic && gated) {  // client/server half in place, then the gradient
+      LaunchScope ls(c, DSGD_K_EA);
+      DSGD_CUDA(dsgd::launch_ea_local<T>(a, 0, 0, blocks_for(c, c->d, 1), c->stream, true));
+      a.gated = 0;
+    }
+    DSGD_TRY(produce_logistic<T>(c, h, gs, {i}, true));
     {
       LaunchScope ls(c, DSGD_K_EA);
       DSGD_CUDA(dsgd::launch_ea_local<T>(a, vec, gs.norm, blocks_for(c, c->d / W, 1), c->stream));
@@ -1668,6 +1863,11 @@ dsgd_status dsgd_ctx_seed_streams(dsgd_ctx* c, uint64_t seed, const char* run_id
   for (auto* s : c->noise_streams) dsgd_stream_destroy(s);
   c->partner_streams.assign(c->p, nullptr);
   c->noise_streams.assign(c->n_local, nullptr);
+  for (auto* s : c->sample_streams) dsgd_stream_destroy(s);
+  c->sample_streams.assign(c->n_local, nullptr);
+  for (uint32_t i = 0; i < c->n_local; ++i)
+    DSGD_TRY(dsgd_stream_make(seed, run_id, c->first + i, DSGD_PURPOSE_SAMPLE,
+                              &c->sample_streams[i]));
   for (uint32_t i = 0; i < c->p; ++i)
     DSGD_TRY(dsgd_stream_make(seed, run_id, i, DSGD_PURPOSE_PARTNER, &c->partner_streams[i]));
   for (uint32_t i = 0; i < c->n_local; ++i)

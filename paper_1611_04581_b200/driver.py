@@ -16,7 +16,7 @@ import numpy as np
 
 from . import _native as N
 from .engine import Group, Hyperparams, Stream
-from .protocols import InvalidArgument, NoiseModel, QuadraticObjective
+from .protocols import InvalidArgument, LogisticObjective, NoiseModel, QuadraticObjective
 
 PROTOCOLS = {"all-reduce": N.ALLREDUCE, "elastic-avg": N.ELASTIC_AVG,
              "pull-gossip": N.PULL_GOSSIP, "push-gossip": N.PUSH_GOSSIP,
@@ -64,12 +64,14 @@ def make_initial_nodes(cfg: SimConfig, obj: QuadraticObjective) -> np.ndarray:
     if kind == "zeros":
         base = np.zeros(d)
     elif kind == "offset-ones":
+        if opt is None:
+            raise InvalidArgument("offset-ones init requires an objective with a known optimum")
         if not cfg.init.target_sq_err > 0:
             raise InvalidArgument("init target_sq_err must be positive")
         c = math.sqrt(cfg.init.target_sq_err / (float(cfg.p) * float(d)))
         base = opt + c
     elif kind == "gaussian-spread":
-        base = opt.copy()
+        base = np.zeros(d) if opt is None else opt.copy()
     elif kind == "explicit":
         if cfg.init.values is None or len(cfg.init.values) != d:
             raise InvalidArgument("explicit init size must match objective dimension")
@@ -84,16 +86,50 @@ def make_initial_nodes(cfg: SimConfig, obj: QuadraticObjective) -> np.ndarray:
     return thetas
 
 
-def _group_for(cfg: SimConfig, d: int, dtype: str) -> Group:
+def _group_for(cfg: SimConfig, d: int, dtype: str, center: bool = False,
+               obj=None, node_objs=None, device: int = 0) -> Group:
     noise = cfg.noise is not None and cfg.noise.kind != "zero"
-    return Group(d, cfg.p, dtype=dtype, quadratic=True, noise=noise,
-                 center=cfg.protocol == "elastic-avg")
+    logistic = isinstance(obj, LogisticObjective)
+    g = Group(d, cfg.p, dtype=dtype, quadratic=not logistic, noise=noise, center=center,
+              device=device)
+    try:
+        _set_objective(g, cfg, obj, node_objs)
+    except Exception:
+        g.close()
+        raise
+    return g
+
+
+def _set_objective(g: Group, cfg: SimConfig, obj, node_objs):
+    """Quadratic: spectrum/optimum buffers.  Logistic: the dataset, and each
+    node's sample range from node_objs (run_sync(cfg, eval_obj, node_objs),
+    simulator.hpp:134-140; the sharded runs of runner.cpp:100-115)."""
+    if isinstance(obj, LogisticObjective):
+        g.set_logistic(obj.features, obj.labels, obj.l2)
+        objs = node_objs if node_objs is not None else [obj] * cfg.p
+        if len(objs) != cfg.p:
+            raise InvalidArgument("node objective count must equal p")
+        for i, o in enumerate(objs):
+            if not isinstance(o, LogisticObjective) or o.dim() != obj.dim():
+                raise InvalidArgument("node objectives must share the evaluation dimension")
+            if not np.array_equal(o.features, obj.features) or o.l2 != obj.l2:
+                raise InvalidArgument("node objectives must share the device dataset")
+            g.logistic_set_sample_range(i, *o.range)
+        g.seed_streams(cfg.seed, cfg.run_id)
+    else:
+        g.set_quadratic(obj.spectrum, obj.opt)
+
+
+def _grad_kind(obj) -> str:
+    return "logistic" if isinstance(obj, LogisticObjective) else "quadratic"
 
 
 def run_sync(cfg: SimConfig, obj: QuadraticObjective, dtype: str = "f64",
-             device: int = 0) -> RunResult:
+             device: int = 0, node_objs=None) -> RunResult:
     """run_sync for all-reduce, elastic-avg, pull/push gossip, gossip-stale
-    and gossip-fresh -- every round one fused kernel (two for fresh)."""
+    and gossip-fresh -- every round one fused kernel (two for fresh).  With
+    a LogisticObjective the minibatch gradient of each node is computed on
+    the device first (rows from the node's sample stream)."""
     if cfg.protocol not in PROTOCOLS or cfg.protocol == "async-pull":
         raise InvalidArgument("async-pull requires the asynchronous driver")
     if cfg.rounds == 0:
@@ -102,9 +138,8 @@ def run_sync(cfg: SimConfig, obj: QuadraticObjective, dtype: str = "f64",
     if cfg.noise is not None and cfg.noise.dim != d:
         raise InvalidArgument("noise dimension must match objective dimension")
     thetas = make_initial_nodes(cfg, obj)
-    g = _group_for(cfg, d, dtype)
+    g = _group_for(cfg, d, dtype, cfg.protocol == "elastic-avg", obj, node_objs, device)
     try:
-        g.set_quadratic(obj.spectrum, obj.opt)
         for i in range(cfg.p):
             g.set_state(i, thetas[i])
         if cfg.protocol == "elastic-avg":
@@ -112,7 +147,7 @@ def run_sync(cfg: SimConfig, obj: QuadraticObjective, dtype: str = "f64",
         g.seed_streams(cfg.seed, cfg.run_id)
         sigma = cfg.noise.sigma if cfg.noise is not None and cfg.noise.kind != "zero" else 0.0
         g.run_rounds(PROTOCOLS[cfg.protocol], cfg.hyper, cfg.rounds,
-                     scope=cfg.momentum_scope, grad="quadratic", host_noise_sigma=sigma)
+                     scope=cfg.momentum_scope, grad=_grad_kind(obj), host_noise_sigma=sigma)
         th = np.zeros((cfg.p, d))
         dp = np.zeros((cfg.p, d))
         t = np.zeros(cfg.p, dtype=np.uint64)
@@ -125,7 +160,7 @@ def run_sync(cfg: SimConfig, obj: QuadraticObjective, dtype: str = "f64",
 
 
 def run_async_elastic(cfg: SimConfig, obj: QuadraticObjective, dtype: str = "f64",
-                      device: int = 0) -> RunResult:
+                      device: int = 0, node_objs=None) -> RunResult:
     """run_async for elastic-avg under the Poisson clock (simulator.cpp:
     380-449): master clock (gap, then node); the ticking client runs
     ea_client_step + ea_server_apply when gated on its own t, else a local
@@ -135,10 +170,8 @@ def run_async_elastic(cfg: SimConfig, obj: QuadraticObjective, dtype: str = "f64
     d = obj.dim()
     thetas = make_initial_nodes(cfg, obj)
     use_noise = cfg.noise is not None and cfg.noise.kind != "zero"
-    g = Group(d, cfg.p, dtype=dtype, quadratic=True, noise=use_noise, center=True,
-              device=device)
+    g = _group_for(cfg, d, dtype, True, obj, node_objs, device)
     try:
-        g.set_quadratic(obj.spectrum, obj.opt)
         for i in range(cfg.p):
             g.set_state(i, thetas[i])
         g.ea_init_center()
@@ -152,7 +185,7 @@ def run_async_elastic(cfg: SimConfig, obj: QuadraticObjective, dtype: str = "f64
             if use_noise:
                 g.set_vector(i, N.BUF_NOISE, noise[i].fill_normal(cfg.noise.sigma, d))
             gated = t[i] > 0 and t[i] % tau == 0
-            g.ea_client_event(cfg.hyper, i, gated, grad="quadratic", noise=use_noise)
+            g.ea_client_event(cfg.hyper, i, gated, grad=_grad_kind(obj), noise=use_noise)
             t[i] += 1
         th = np.zeros((cfg.p, d))
         dp = np.zeros((cfg.p, d))
@@ -165,7 +198,7 @@ def run_async_elastic(cfg: SimConfig, obj: QuadraticObjective, dtype: str = "f64
 
 
 def run_async_pull(cfg: SimConfig, obj: QuadraticObjective, dtype: str = "f64",
-                   device: int = 0) -> RunResult:
+                   device: int = 0, node_objs=None) -> RunResult:
     """run_async for async-pull (simulator.cpp:380-449): master Poisson clock
     (gap, then node), partner from the ticking node's stream, one fused
     event kernel per tick."""
@@ -174,9 +207,8 @@ def run_async_pull(cfg: SimConfig, obj: QuadraticObjective, dtype: str = "f64",
     d = obj.dim()
     thetas = make_initial_nodes(cfg, obj)
     use_noise = cfg.noise is not None and cfg.noise.kind != "zero"
-    g = Group(d, cfg.p, dtype=dtype, quadratic=True, noise=use_noise)
+    g = _group_for(cfg, d, dtype, False, obj, node_objs, device)
     try:
-        g.set_quadratic(obj.spectrum, obj.opt)
         for i in range(cfg.p):
             g.set_state(i, thetas[i])
         clock = Stream.make(cfg.seed, cfg.run_id, 0xFFFFFFFF, "clock")
@@ -188,7 +220,7 @@ def run_async_pull(cfg: SimConfig, obj: QuadraticObjective, dtype: str = "f64",
             j = partner[i].uniform_index(cfg.p)
             if use_noise:
                 g.set_vector(i, N.BUF_NOISE, noise[i].fill_normal(cfg.noise.sigma, d))
-            g.async_pull_event(cfg.hyper, i, j, grad="quadratic", noise=use_noise)
+            g.async_pull_event(cfg.hyper, i, j, grad=_grad_kind(obj), noise=use_noise)
         th = np.zeros((cfg.p, d))
         dp = np.zeros((cfg.p, d))
         t = np.zeros(cfg.p, dtype=np.uint64)

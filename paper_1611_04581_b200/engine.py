@@ -244,9 +244,26 @@ class Group:
         N.check(self.lib.dsgd_download_async(self._ctx, local, which, host_ptr, count))
 
     # -------------------------------------------------------- update rules
-    def _grad(self, grad, noise, grad_norm: bool):
+    def set_logistic(self, features, labels, l2: float) -> None:
+        """LogisticObjective(features, labels, l2) (objectives.cpp:80-106) on
+        this context; use grad='logistic' in the rules."""
+        X = np.ascontiguousarray(features, dtype=np.float64)
+        if X.ndim != 2 or (X.shape[0] and X.shape[1] != self.d):
+            raise ValueError("logistic feature rows have inconsistent width")
+        y = np.ascontiguousarray(labels, dtype=np.int32)
+        if len(y) != X.shape[0]:
+            raise ValueError("logistic features/labels size mismatch")
+        N.check(self.lib.dsgd_set_logistic(self._ctx, X.ctypes.data if X.size else None,
+                                           y.ctypes.data if y.size else None, X.shape[0], l2))
+
+    def logistic_set_sample_range(self, local: int, begin: int, end: int) -> None:
+        N.check(self.lib.dsgd_logistic_set_sample_range(self._ctx, local, begin, end))
+
+    def _grad(self, grad, noise, grad_norm: bool, rows=None):
         """grad: None -> quadratic objective if present else the context's
-        gradient buffers; 'quadratic'; or a list of device pointers.
+        gradient buffers; 'quadratic'; 'logistic' (the dataset of
+        set_logistic; rows = n_local x batch minibatch rows, or None to draw
+        them from the nodes' sample streams); or a list of device pointers.
         noise: False (zero noise), True (the context's noise buffers) or
         ('device', sigma, seed) for Philox noise drawn inside the kernel."""
         keep = None
@@ -254,7 +271,8 @@ class Group:
             src = N.GRAD_QUADRATIC if self.flags & N.CTX_QUADRATIC else N.GRAD_BUFFER
             ptr = None
         elif isinstance(grad, str):
-            src, ptr = {"quadratic": N.GRAD_QUADRATIC, "buffer": N.GRAD_BUFFER}[grad], None
+            src, ptr = {"quadratic": N.GRAD_QUADRATIC, "buffer": N.GRAD_BUFFER,
+                        "logistic": N.GRAD_LOGISTIC}[grad], None
         else:
             keep = (C.c_void_p * len(grad))(*grad)
             src, ptr = N.GRAD_BUFFER, C.cast(keep, C.POINTER(C.c_void_p))
@@ -263,14 +281,18 @@ class Group:
             mode, sigma, seed = 2, float(noise[1]), int(noise[2])
         elif noise:
             mode = 1
+        rp = None
+        if rows is not None:
+            rows = np.ascontiguousarray(rows, dtype=np.uint64)
+            rp = rows.ctypes.data_as(C.POINTER(C.c_uint64))
         gs = N.GradSpec(src, ptr, mode, C.pointer(self._norm) if grad_norm else None,
-                        sigma, seed)
-        gs._keep = keep
+                        sigma, seed, rp)
+        gs._keep = (keep, rows)
         return gs
 
-    def _run(self, fn, *args, grad=None, noise=False, grad_norm=False):
+    def _run(self, fn, *args, grad=None, noise=False, grad_norm=False, rows=None):
         self._norm.value = 0.0
-        gs = self._grad(grad, noise, grad_norm)
+        gs = self._grad(grad, noise, grad_norm, rows)
         N.check(fn(self._ctx, *args[:1], C.byref(gs), *args[1:]))
         return self._norm.value if grad_norm else None
 

@@ -68,7 +68,56 @@ class GradientObjective:
         return self.gradient.size
 
 
-Objective = Union[QuadraticObjective, GradientObjective]
+class LogisticObjective:
+    """l2-regularised logistic regression on a fixed design matrix
+    (objectives.hpp:75-107, objectives.cpp:80-162): the dataset lives on the
+    device and the minibatch gradient is computed there (DSGD_GRAD_LOGISTIC)."""
+
+    def __init__(self, features, labels: Sequence[int], l2: float):
+        rows = [np.asarray(r, dtype=np.float64) for r in features]
+        if not rows:
+            raise InvalidArgument("logistic dataset is empty")
+        if len(rows) != len(labels):
+            raise InvalidArgument("logistic features/labels size mismatch")
+        if not l2 > 0.0:
+            raise InvalidArgument("logistic l2 must be positive (strong convexity)")
+        d = rows[0].size
+        if any(r.size != d for r in rows):
+            raise InvalidArgument("logistic feature rows have inconsistent width")
+        if any(int(y) not in (0, 1) for y in labels):
+            raise InvalidArgument("logistic labels must be 0 or 1")
+        self.features = np.stack(rows)
+        self.labels = np.asarray(labels, dtype=np.int32)
+        self.l2 = float(l2)
+        self.range = (0, len(rows))
+        self.lipschitz = self.l2 + 0.25 * float((self.features ** 2).sum(axis=1).max())
+
+    def dim(self) -> int:
+        return self.features.shape[1]
+
+    def num_samples(self) -> int:
+        return self.features.shape[0]
+
+    def optimum(self):
+        return None
+
+    def set_sample_range(self, begin: int, end: int) -> None:
+        """objectives.cpp:108-114"""
+        if begin >= end or end > self.num_samples():
+            raise InvalidArgument("invalid sample range")
+        self.range = (begin, end)
+
+    def shard(self, begin: int, end: int) -> "LogisticObjective":
+        o = LogisticObjective.__new__(LogisticObjective)
+        o.__dict__.update(self.__dict__)
+        o.set_sample_range(begin, end)
+        return o
+
+    def convexity_params(self):
+        return self.l2, self.lipschitz
+
+
+Objective = Union[QuadraticObjective, GradientObjective, LogisticObjective]
 
 
 @dataclass
@@ -172,15 +221,34 @@ def _objs(obj, p: int) -> List[Objective]:
 
 
 def _load(g: Group, nodes: Sequence[NodeState], objs: Sequence[Objective],
-          noise: Optional[NoiseModel], draw: Sequence[bool]):
-    """Upload states, objective and this step's noise; returns the grad spec."""
+          noise: Optional[NoiseModel], draw: Sequence[bool], h: Optional[Hyperparams] = None):
+    """Upload states, objective and this step's noise; returns the gradient
+    keyword arguments of the Group rule call."""
     d = g.d
     for i, n in enumerate(nodes):
         if n.theta.size != d or n.delta_prev.size != d:
             raise InvalidArgument("ParamVec dimension mismatch")
         g.set_state(i, n.theta, n.delta_prev, n.t)
     quad = isinstance(objs[0], QuadraticObjective)
-    if quad:
+    rows = None
+    if isinstance(objs[0], LogisticObjective):
+        # the dataset on the device; each drawing node's minibatch rows from its
+        # own sample stream (objectives.cpp:154-157), consumed here on the host
+        base = objs[0]
+        if any(not isinstance(o, LogisticObjective) or o.dim() != d for o in objs):
+            raise InvalidArgument("stochastic_gradient: dimension mismatch")
+        if any(not np.array_equal(o.features, base.features) or o.l2 != base.l2 for o in objs):
+            raise InvalidArgument("per-node logistic objectives must share one dataset")
+        g.set_logistic(base.features, base.labels, base.l2)
+        batch = h.batch if h is not None else 1
+        if batch == 0:
+            raise InvalidArgument("batch must be >= 1")
+        rows = np.zeros((len(nodes), batch), dtype=np.uint64)
+        for i, (n, o) in enumerate(zip(nodes, objs)):
+            b, e = o.range
+            rows[i] = [b + n.rng.sample.uniform_index(e - b) for _ in range(batch)] \
+                if draw[i] else b
+    elif quad:
         for o in objs:
             if not isinstance(o, QuadraticObjective) or not (
                     o.spectrum is objs[0].spectrum or np.array_equal(o.spectrum, objs[0].spectrum)) \
@@ -201,7 +269,9 @@ def _load(g: Group, nodes: Sequence[NodeState], objs: Sequence[Objective],
         for i, n in enumerate(nodes):
             xi = noise.sample(n.rng.noise) if draw[i] else np.zeros(d)
             g.set_vector(i, N.BUF_NOISE, xi)
-    return ("quadratic" if quad else "buffer"), use_noise
+    if rows is not None:
+        return dict(grad="logistic", noise=use_noise, rows=rows)
+    return dict(grad="quadratic" if quad else "buffer", noise=use_noise)
 
 
 def _store(g: Group, nodes: Sequence[NodeState]) -> List[NodeState]:
@@ -227,8 +297,8 @@ def local_sgd_step(node: NodeState, obj: Objective, noise: NoiseModel, h: Hyperp
     """protocols.cpp:102-108 (fused kernel k_step, mode step)."""
     node = node.copy()
     g = _group(1, node.theta.size, dtype)
-    src, nz = _load(g, [node], _objs(obj, 1), noise, [True])
-    _norm_update(grad_norm_out, g.local_sgd_step(h, grad=src, noise=nz,
+    kw = _load(g, [node], _objs(obj, 1), noise, [True], h)
+    _norm_update(grad_norm_out, g.local_sgd_step(h, **kw,
                                                  grad_norm=grad_norm_out is not None))
     return _store(g, [node])[0]
 
@@ -238,8 +308,8 @@ def compute_local_delta(node: NodeState, obj: Objective, noise: NoiseModel, h: H
     """protocols.cpp:85-100: the step's delta; consumes node's noise stream
     (node is taken by reference), leaves theta and t untouched."""
     g = _group(1, node.theta.size, dtype)
-    src, nz = _load(g, [node], _objs(obj, 1), noise, [True])
-    _norm_update(grad_norm_out, g.local_sgd_step(h, grad=src, noise=nz,
+    kw = _load(g, [node], _objs(obj, 1), noise, [True], h)
+    _norm_update(grad_norm_out, g.local_sgd_step(h, **kw,
                                                  grad_norm=grad_norm_out is not None))
     return g.get_state(0)[1]
 
@@ -254,8 +324,8 @@ def allreduce_round(nodes: Sequence[NodeState], obj, noise: NoiseModel, h: Hyper
         raise InvalidArgument("synchronous round requires equal node clocks")
     nodes = _by_value(nodes)
     g = _group(len(nodes), nodes[0].theta.size, dtype)
-    src, nz = _load(g, nodes, _objs(obj, len(nodes)), noise, [True] * len(nodes))
-    _norm_update(grad_norm_out, g.allreduce_round(h, scope=scope, grad=src, noise=nz,
+    kw = _load(g, nodes, _objs(obj, len(nodes)), noise, [True] * len(nodes), h)
+    _norm_update(grad_norm_out, g.allreduce_round(h, scope=scope, **kw,
                                                   grad_norm=grad_norm_out is not None))
     return _store(g, nodes)
 
@@ -270,13 +340,13 @@ def ea_client_step(node: NodeState, center, obj: Objective, noise: NoiseModel,
         raise InvalidArgument("ea_client_step center dimension mismatch")
     node = node.copy()
     g = _group(1, node.theta.size, dtype)
-    src, nz = _load(g, [node], _objs(obj, 1), noise, [True])
+    kw = _load(g, [node], _objs(obj, 1), noise, [True], h)
     g.set_center(center)
     upd = torch.empty(node.theta.size, dtype=torch.float64 if dtype == "f64" else torch.float32,
                       device=f"cuda:{g.device}")
     g.ea_set_update_out([upd.data_ptr()])
     try:
-        _norm_update(grad_norm_out, g.ea_round(h, gated=True, grad=src, noise=nz,
+        _norm_update(grad_norm_out, g.ea_round(h, gated=True, **kw,
                                                grad_norm=grad_norm_out is not None))
         g.sync()
     finally:
@@ -305,9 +375,9 @@ def ea_sweep(nodes: Sequence[NodeState], server: ServerState, obj, noise: NoiseM
     client in node order against the serially updated center, one kernel."""
     nodes = _by_value(nodes)
     g = _group(len(nodes), nodes[0].theta.size, dtype)
-    src, nz = _load(g, nodes, _objs(obj, len(nodes)), noise, [True] * len(nodes))
+    kw = _load(g, nodes, _objs(obj, len(nodes)), noise, [True] * len(nodes), h)
     g.set_center(server.theta_center)
-    _norm_update(grad_norm_out, g.ea_round(h, gated=gated, grad=src, noise=nz,
+    _norm_update(grad_norm_out, g.ea_round(h, gated=gated, **kw,
                                            grad_norm=grad_norm_out is not None))
     return _store(g, nodes), ServerState(g.get_center(),
                                          server.applied_updates + (len(nodes) if gated else 0))
@@ -342,8 +412,8 @@ def pull_gossip_round(nodes: Sequence[NodeState], partner_of, obj, noise: NoiseM
     nodes = _by_value(nodes)
     m = _check_partners(len(nodes), partner_of)
     g = _group(len(nodes), nodes[0].theta.size, dtype)
-    src, nz = _load(g, nodes, _objs(obj, len(nodes)), noise, [True] * len(nodes))
-    _norm_update(grad_norm_out, g.pull_gossip_round(h, m, grad=src, noise=nz,
+    kw = _load(g, nodes, _objs(obj, len(nodes)), noise, [True] * len(nodes), h)
+    _norm_update(grad_norm_out, g.pull_gossip_round(h, m, **kw,
                                                     grad_norm=grad_norm_out is not None))
     return _store(g, nodes)
 
@@ -375,8 +445,8 @@ def push_gossip_round(nodes: Sequence[NodeState], target_of, obj, noise: NoiseMo
     nodes = _by_value(nodes)
     m = _check_targets(len(nodes), target_of)
     g = _group(len(nodes), nodes[0].theta.size, dtype)
-    src, nz = _load(g, nodes, _objs(obj, len(nodes)), noise, [True] * len(nodes))
-    _norm_update(grad_norm_out, g.push_gossip_round(h, m, grad=src, noise=nz,
+    kw = _load(g, nodes, _objs(obj, len(nodes)), noise, [True] * len(nodes), h)
+    _norm_update(grad_norm_out, g.push_gossip_round(h, m, **kw,
                                                     grad_norm=grad_norm_out is not None))
     return _store(g, nodes)
 
@@ -396,10 +466,10 @@ def gossip_stale_step(node: NodeState, partner_theta, obj: Objective, noise: Noi
     node = node.copy()
     pair = _pair(node, partner_theta)
     g = _group(2, node.theta.size, dtype)
-    objs = [obj, obj if isinstance(obj, QuadraticObjective) else GradientObjective(
+    objs = [obj, obj if isinstance(obj, (QuadraticObjective, LogisticObjective)) else GradientObjective(
         np.zeros(node.theta.size))]
-    src, nz = _load(g, pair, objs, noise, [True, False])
-    _norm_update(grad_norm_out, g.gossip_stale_round(h, [1, 1], grad=src, noise=nz,
+    kw = _load(g, pair, objs, noise, [True, False], h)
+    _norm_update(grad_norm_out, g.gossip_stale_round(h, [1, 1], **kw,
                                                      grad_norm=grad_norm_out is not None))
     return _store(g, pair)[0]
 
@@ -433,8 +503,8 @@ def async_pull_event(nodes: Sequence[NodeState], i: int, j: int, obj: Objective,
     nodes = _by_value(nodes)
     g = _group(len(nodes), nodes[0].theta.size, dtype)
     objs = [obj] * len(nodes)
-    src, nz = _load(g, nodes, objs, noise, [k == i for k in range(len(nodes))])
-    _norm_update(grad_norm_out, g.async_pull_event(h, i, j, grad=src, noise=nz,
+    kw = _load(g, nodes, objs, noise, [k == i for k in range(len(nodes))], h)
+    _norm_update(grad_norm_out, g.async_pull_event(h, i, j, **kw,
                                                    grad_norm=grad_norm_out is not None))
     return _store(g, nodes)
 

@@ -53,9 +53,73 @@ def transport_case(p: int) -> "O.SimConfig":
                        rounds=25, per_node_scope=False, run_id="mg/all-reduce")
 
 
+def logistic_dataset():
+    """A small LogisticObjective (F1 row of SURVEY §8(f)): n = 48 rows,
+    d = 37 (not a multiple of any vector width), labels from a planted model,
+    l2 = 0.05; node i of p = 4 samples rows [12 i, 12 i + 12) (sharded, the
+    runner.cpp:100-115 shape)."""
+    rng = np.random.default_rng(1611)
+    n, d = 48, 37
+    X = rng.standard_normal((n, d)) / np.sqrt(d)
+    w = rng.standard_normal(d) * 3.0
+    y = (X @ w + 0.3 * rng.standard_normal(n) > 0).astype(np.int32)
+    ranges = np.array([[12 * i, 12 * i + 12] for i in range(4)], dtype=np.uint64)
+    return X, y, 0.05, ranges
+
+
+def _lg(protocol, **kw):
+    hk = dict(alpha0=0.5, anneal_at=(25,), mu=0.9, weight_decay=1e-4, batch=3, beta_gossip=0.4,
+              beta_ea=0.2, tau=1)
+    hk.update(kw.pop("hyper", {}))
+    base = dict(protocol=protocol, p=4, hyper=H(**hk), sigma=0.01, spectrum=[1.0] * 37,
+                init_kind=O.INIT_GAUSSIAN, init_scale=0.5, rounds=40, run_id="lg/" + str(protocol))
+    base.update(kw)
+    return O.SimConfig(**base)
+
+
+# The logistic trajectories (run_sync / run_async with sharded LogisticObjective
+# node objectives; spectrum only carries d).
+LOGISTIC_CASES = {
+    "lg_allreduce": _lg(O.ALLREDUCE, per_node_scope=True),
+    "lg_allreduce_agg": _lg(O.ALLREDUCE, per_node_scope=False, hyper=dict(batch=1)),
+    "lg_pull": _lg(O.PULL),
+    "lg_push": _lg(O.PUSH, hyper=dict(tau=2)),
+    "lg_ea": _lg(O.ELASTIC, hyper=dict(batch=2)),
+    "lg_stale": _lg(O.STALE),
+    "lg_fresh": _lg(O.FRESH, hyper=dict(tau=2)),
+    "lg_async": _lg(O.ASYNC_PULL, hyper=dict(mu=0.0), events=120, rounds=1),
+    "lg_ea_poisson": _lg(O.ELASTIC, poisson=True, events=120, hyper=dict(tau=2)),
+}
+
+
+def make_logistic():
+    X, y, l2, ranges = logistic_dataset()
+    out = {"X": X, "y": y, "l2": np.float64(l2), "ranges": ranges}
+    # stochastic_gradient known answers: theta, sample-stream seed, range, batch
+    rng = np.random.default_rng(7)
+    for k, (batch, b, e) in enumerate(((1, 0, 48), (3, 12, 24), (8, 0, 48))):
+        theta = rng.standard_normal(X.shape[1])
+        seed = O.derive_stream_seed(3, "lg/kat", k, "sample")
+        O.ref_set_logistic(X, y, l2)
+        out[f"kat{k}_theta"] = theta
+        out[f"kat{k}_meta"] = np.array([batch, b, e, seed], dtype=np.uint64)
+        out[f"kat{k}_grad"] = O.ref_logistic_grad(theta, batch, seed, b, e)
+    for name, cfg in LOGISTIC_CASES.items():
+        O.ref_set_logistic(X, y, l2, ranges)
+        th, dp, t, c = O.ref_run(cfg)
+        out.update({f"{name}_theta": th, f"{name}_dprev": dp, f"{name}_t": t,
+                    f"{name}_center": c})
+    O.ref_set_logistic(None, None, 0.0)
+    np.savez(os.path.join(HERE, "logistic.npz"), **out)
+
+
 def main():
     if not O.ref_available():
         raise SystemExit("oracle/_ref not built: needs /root/reference")
+    if sys.argv[1:] == ["logistic"]:
+        make_logistic()
+        return
+    make_logistic()
     seed = 0x5EED
     np.savez(os.path.join(HERE, "streams.npz"), seed=np.uint64(seed), n=np.uint64(7),
              u64=O.ref_stream(seed, 0, 1000), normal=O.ref_stream(seed, 2, 500),

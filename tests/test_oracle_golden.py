@@ -408,3 +408,68 @@ def test_golden_transport_allreduce_restatement():
         n = O.run_transport_allreduce(transport_case(p))
         assert n.theta.tobytes() == g[f"p{p}_theta"].tobytes()
         assert n.dprev.tobytes() == g[f"p{p}_dprev"].tobytes()
+
+
+# ------------------------------------------ LogisticObjective (F1)
+def test_golden_logistic_gradient_kats():
+    """The restated stochastic_gradient (rows from the node's sample stream,
+    objectives.cpp:147-162) equals the compiled reference's bit for bit."""
+    g = _golden("logistic.npz")
+    X, y, l2 = g["X"], g["y"], float(g["l2"])
+    for k in range(3):
+        batch, b, e, seed = (int(v) for v in g[f"kat{k}_meta"])
+        rows = O.Stream(seed).draw_rows(b, e, batch)
+        assert all(b <= r < e for r in rows)
+        got = O.logistic_grad(X, y, l2, g[f"kat{k}_theta"], rows)
+        assert got.tobytes() == g[f"kat{k}_grad"].tobytes(), k
+
+
+def test_logistic_tiny_hand_values():
+    """test_objectives.cpp tiny_logistic: at theta = 0 every z = 0, so
+    sigmoid = 1/2 and the single-row gradient is (1/2 - y) x + l2 * 0."""
+    X = np.array([[1.0, 0.0], [0.0, 1.0], [1.0, 1.0], [-1.0, 0.5]])
+    y = np.array([1, 0, 1, 0], dtype=np.int32)
+    assert O.sigmoid(0.0) == 0.5
+    for r in range(4):
+        g = O.logistic_grad(X, y, 0.1, np.zeros(2), [r])
+        assert g.tolist() == ((0.5 - y[r]) * X[r]).tolist()
+    # batch mean then l2 * theta, in that order
+    th = np.array([0.3, -0.2])
+    g = O.logistic_grad(X, y, 0.1, th, [0, 3, 3])
+    acc = np.zeros(2)
+    for r in (0, 3, 3):
+        acc = acc + (O.sigmoid(float(X[r] @ th)) - y[r]) * X[r]
+    assert np.allclose(g, acc * (1.0 / 3) + 0.1 * th, rtol=0, atol=1e-15)
+
+
+def test_logistic_fp32_policy_close_to_fp64():
+    g = _golden("logistic.npz")
+    X, y, l2 = g["X"], g["y"], float(g["l2"])
+    th = g["kat2_theta"]
+    rows = np.arange(0, 48, 5)
+    g64 = O.logistic_grad(X, y, l2, th, rows)
+    g32 = O.logistic_grad(X.astype(np.float32), y, l2, th.astype(np.float32), rows)
+    assert np.abs(g32 - g64).max() <= 1e-6 * np.abs(g64).max()
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_ref_logistic_gradient_random_bit_exact():
+    rng = np.random.default_rng(3)
+    for n, d, batch in ((5, 3, 1), (17, 64, 4), (40, 129, 9)):
+        X = rng.standard_normal((n, d))
+        y = rng.integers(0, 2, n).astype(np.int32)
+        O.ref_set_logistic(X, y, 0.01)
+        th = rng.standard_normal(d)
+        seed = O.derive_stream_seed(9, "lg", n, "sample")
+        want = O.ref_logistic_grad(th, batch, seed, 1, n)
+        got = O.logistic_grad(X, y, 0.01, th, O.Stream(seed).draw_rows(1, n, batch))
+        assert got.tobytes() == want.tobytes()
+    O.ref_set_logistic(None, None, 0.0)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_ref_logistic_constructor_errors():
+    with pytest.raises(ValueError, match="l2 must be positive"):
+        O.ref_set_logistic(np.ones((2, 2)), [0, 1], 0.0)
+    with pytest.raises(ValueError, match="labels must be 0 or 1"):
+        O.ref_set_logistic(np.ones((2, 2)), [0, 2], 0.1)
