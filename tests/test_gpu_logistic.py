@@ -267,21 +267,21 @@ def test_logistic_errors():
     g = Group(8, 2, dtype="f64")
     with pytest.raises(N.DsgdError, match="no logistic dataset"):
         g.local_sgd_step(Hyperparams(**HK()), grad="logistic")
-    with pytest.raises(N.DsgdError, match="logistic dataset is empty"):
+    with pytest.raises(N.InvalidArgument, match="logistic dataset is empty"):
         g.set_logistic(np.zeros((0, 8)), [], 0.1)
-    with pytest.raises(N.DsgdError, match="l2 must be positive"):
+    with pytest.raises(N.InvalidArgument, match="l2 must be positive"):
         g.set_logistic(np.ones((2, 8)), [0, 1], 0.0)
-    with pytest.raises(N.DsgdError, match="labels must be 0 or 1"):
+    with pytest.raises(N.InvalidArgument, match="labels must be 0 or 1"):
         g.set_logistic(np.ones((2, 8)), [0, 3], 0.1)
     g.set_logistic(np.ones((4, 8)), [0, 1, 1, 0], 0.1)
-    with pytest.raises(N.DsgdError, match="invalid sample range"):
+    with pytest.raises(N.InvalidArgument, match="invalid sample range"):
         g.logistic_set_sample_range(0, 3, 3)
-    with pytest.raises(N.DsgdError, match="invalid sample range"):
+    with pytest.raises(N.InvalidArgument, match="invalid sample range"):
         g.logistic_set_sample_range(1, 0, 5)
-    with pytest.raises(N.DsgdError, match="batch must be >= 1"):
+    with pytest.raises(N.InvalidArgument, match="batch must be >= 1"):
         g.local_sgd_step(Hyperparams(**HK(batch=0)), grad="logistic",
                          rows=np.zeros((2, 1), np.uint64))
-    with pytest.raises(N.DsgdError, match="row out of range"):
+    with pytest.raises(N.InvalidArgument, match="row out of range"):
         g.local_sgd_step(Hyperparams(**HK(batch=1)), grad="logistic",
                          rows=np.array([[0], [4]], np.uint64))
     with pytest.raises(N.DsgdError, match="seed_streams"):
