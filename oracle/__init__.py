@@ -159,6 +159,9 @@ def lib():
                                              C.c_uint64, C.c_void_p]
         _lib.dsgdo_sigmoid.restype = C.c_double
         _lib.dsgdo_sigmoid.argtypes = [C.c_double]
+        _lib.dsgdo_logistic_value.restype = C.c_double
+        _lib.dsgdo_logistic_value.argtypes = [C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
+                                              C.c_double, C.c_void_p]
         _lib.dsgdo_draw_rows.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32,
                                          C.c_void_p]
         for sfx in ("f64", "f32"):
@@ -204,6 +207,8 @@ def ref():
                                           C.c_double, C.c_void_p, C.c_uint32]
         _ref.ref_logistic_grad.argtypes = [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint64,
                                            C.c_uint64, C.c_uint64, C.c_void_p]
+        _ref.ref_logistic_value.restype = C.c_double
+        _ref.ref_logistic_value.argtypes = [C.c_void_p, C.c_uint64]
         _ref.ref_time_rounds.restype = C.c_double
         _ref.ref_time_rounds.argtypes = [C.c_int, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int,
                                          C.POINTER(Hyper)]
@@ -474,6 +479,19 @@ def logistic_grad(X: np.ndarray, y, l2: float, theta: np.ndarray, rows) -> np.nd
         C.c_uint64(X.shape[1]), _ptr(X), _ptr(y), C.c_double(l2), _ptr(theta),
         C.c_uint32(len(rows)), _ptr(rows), _ptr(out))
     return out
+
+
+def logistic_value(X, y, l2: float, theta) -> float:
+    """LogisticObjective::value (objectives.cpp:116-125), fp64."""
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.int32)
+    theta = np.ascontiguousarray(theta, dtype=np.float64)
+    return lib().dsgdo_logistic_value(X.shape[0], X.shape[1], _ptr(X), _ptr(y), l2, _ptr(theta))
+
+
+def ref_logistic_value(theta) -> float:
+    theta = np.ascontiguousarray(theta, dtype=np.float64)
+    return ref().ref_logistic_value(_ptr(theta), len(theta))
 
 
 # --------------------------------------------------------------------------

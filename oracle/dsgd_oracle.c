@@ -178,3 +178,21 @@ void dsgdo_draw_rows(dsgdo_rng* sample, uint64_t begin, uint64_t end, uint32_t b
   const uint32_t span = (uint32_t)(end - begin);
   for (uint32_t b = 0; b < batch; ++b) rows[b] = begin + dsgdo_uniform_index(sample, span);
 }
+
+static double log1pexp(double z) { /* objectives.cpp:29-32 */
+  if (z > 0.0) return z + log1p(exp(-z));
+  return log1p(exp(z));
+}
+
+double dsgdo_logistic_value(uint64_t n, uint64_t d, const double* X, const int32_t* y, double l2,
+                            const double* theta) {
+  double s = 0.0;
+  for (uint64_t i = 0; i < n; ++i) {
+    double z = 0.0;
+    for (uint64_t k = 0; k < d; ++k) z += X[i * d + k] * theta[k];
+    s += log1pexp(z) - (double)y[i] * z;
+  }
+  double sq = 0.0; /* ParamVec::squared_norm: sequential sum of squares */
+  for (uint64_t k = 0; k < d; ++k) sq += theta[k] * theta[k];
+  return s / (double)n + 0.5 * l2 * sq;
+}

@@ -94,6 +94,10 @@ enum { DSGDO_OBJ_QUADRATIC = 0, DSGDO_OBJ_FIXED = 1, DSGDO_OBJ_LOGISTIC = 2 /* r
 void dsgdo_draw_rows(dsgdo_rng* sample, uint64_t begin, uint64_t end, uint32_t batch,
                      uint64_t* rows);
 double dsgdo_sigmoid(double z);
+/* LogisticObjective::value objectives.cpp:116-125 (fp64): mean over all rows
+ * of log1pexp(z) - y z, plus 0.5 l2 ||theta||^2 */
+double dsgdo_logistic_value(uint64_t n, uint64_t d, const double* X, const int32_t* y, double l2,
+                            const double* theta);
 
 /* ---- run drivers (simulator.cpp run_sync 214-374 / run_async 380-449) */
 enum {

@@ -201,6 +201,12 @@ int ref_logistic_grad(const double* theta, std::uint64_t d, std::uint32_t batch,
   }
 }
 
+// LogisticObjective::value on the installed dataset.
+double ref_logistic_value(const double* theta, std::uint64_t d) {
+  LogisticObjective o(g_logistic.X, g_logistic.y, g_logistic.l2);
+  return o.value(ParamVec(std::vector<double>(theta, theta + d)));
+}
+
 // Full run through the reference drivers (run_simulation). Returns 0, or -1
 // with ref_last_error() set when the reference throws.
 int ref_run(const dsgdo_sim* c, double* theta, double* dprev, std::uint64_t* t,

@@ -1769,17 +1769,20 @@ __device__ __forceinline__ double block_sum_fixed(double v) {
 
 template <typename T>
 __global__ void __launch_bounds__(kBlock) k_logit_partial(const __grid_constant__ LogisticArgs<T> a) {
-  const uint32_t r = blockIdx.y;          // node * batch + b
-  const uint32_t n = r / a.batch;
-  const T* x = a.X + a.rows[r] * a.d;
+  const uint32_t nr = a.n_nodes * a.batch;
   const uint64_t span = (a.d + a.nblk - 1) / a.nblk;
   const uint64_t lo = (uint64_t)blockIdx.x * span;
   const uint64_t hi = lo + span < a.d ? lo + span : a.d;
-  double acc = 0.0;
-  for (uint64_t k = lo + threadIdx.x; k < hi; k += blockDim.x)
-    acc += (double)x[k] * (double)logistic_point(a, n, k);
-  const double s = block_sum_fixed(acc);
-  if (threadIdx.x == 0) a.partial[(uint64_t)r * a.nblk + blockIdx.x] = s;
+  for (uint32_t r = blockIdx.y; r < nr; r += gridDim.y) {  // r = node * batch + b
+    const uint32_t n = r / a.batch;
+    const T* x = a.X + a.rows[r] * a.d;
+    double acc = 0.0;
+    for (uint64_t k = lo + threadIdx.x; k < hi; k += blockDim.x)
+      acc += (double)x[k] * (double)logistic_point(a, n, k);
+    const double s = block_sum_fixed(acc);
+    if (threadIdx.x == 0) a.partial[(uint64_t)r * a.nblk + blockIdx.x] = s;
+    __syncthreads();  // block_sum_fixed's smem is reused by the next row
+  }
 }
 
 __device__ __forceinline__ double sigmoid_ref(double z) {
@@ -1795,7 +1798,13 @@ __global__ void __launch_bounds__(32) k_logit_coeff(const __grid_constant__ Logi
   for (uint32_t b = threadIdx.x; b < a.nblk; b += 32) v += a.partial[(uint64_t)r * a.nblk + b];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if (threadIdx.x == 0) a.coeff[r] = sigmoid_ref(v) - (double)a.y[a.rows[r]];
+  if (threadIdx.x == 0) {
+    const double y = (double)a.y[a.rows[r]];
+    if (a.value_mode)  // log1pexp objectives.cpp:29-32, value 116-125
+      a.coeff[r] = (v > 0.0 ? v + log1p(exp(-v)) : log1p(exp(v))) - y * v;
+    else
+      a.coeff[r] = sigmoid_ref(v) - y;
+  }
 }
 
 template <typename T>
@@ -1817,9 +1826,9 @@ __global__ void __launch_bounds__(kBlock) k_logistic_grad(const __grid_constant_
 template <typename T>
 cudaError_t launch_logistic(const LogisticArgs<T>& a, uint32_t grid, cudaStream_t s) {
   const uint32_t nr = a.n_nodes * a.batch;
-  k_logit_partial<T><<<dim3(a.nblk, nr), kBlock, 0, s>>>(a);
+  k_logit_partial<T><<<dim3(a.nblk, nr < 65535u ? nr : 65535u), kBlock, 0, s>>>(a);
   k_logit_coeff<T><<<nr, 32, 0, s>>>(a);
-  k_logistic_grad<T><<<grid, kBlock, 0, s>>>(a);
+  if (!a.value_mode) k_logistic_grad<T><<<grid, kBlock, 0, s>>>(a);
   return cudaGetLastError();
 }
 

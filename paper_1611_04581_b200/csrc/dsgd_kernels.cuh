@@ -193,6 +193,7 @@ struct LogisticArgs {
   uint32_t n_nodes, batch, nblk;
   T mu, l2, inv_batch;
   int lookahead;
+  int value_mode;             // coeff[r] = log1pexp(z) - y z (LogisticObjective::value terms)
 };
 
 template <typename T>

@@ -582,6 +582,63 @@ dsgd_status produce_logistic(dsgd_ctx* c, const dsgd_hyperparams* h, const GradS
   return DSGD_OK;
 }
 
+// sum over all p nodes of the data term of LogisticObjective::value
+// (objectives.cpp:116-125), each node's rows summed in row order on the host.
+template <typename T>
+dsgd_status logistic_values(dsgd_ctx* c, double* data) {
+  const uint32_t p = c->p;
+  const uint64_t n = c->lg_n;
+  const size_t nr = (size_t)p * n;
+  if (nr > 0xffffffffull) return set_error(DSGD_EINVAL, "trace: logistic dataset too large");
+  const uint32_t nblk = (uint32_t)std::min<uint64_t>(
+      64, std::max<uint64_t>(1, (c->d + 8 * kBlockU - 1) / (8 * kBlockU)));
+  if (c->lg_rows_cap < nr) {
+    cudaFree(c->lg_rows);
+    c->lg_rows = nullptr;
+    DSGD_CUDA(cudaMalloc(&c->lg_rows, nr * sizeof(uint64_t)));
+    c->lg_rows_cap = nr;
+  }
+  if (c->lg_scratch_cap < nr * (nblk + 1)) {
+    cudaFree(c->lg_scratch);
+    c->lg_scratch = nullptr;
+    DSGD_CUDA(cudaMalloc(&c->lg_scratch, nr * (nblk + 1) * sizeof(double)));
+    c->lg_scratch_cap = nr * (nblk + 1);
+  }
+  c->lg_rows_host.resize(nr);
+  for (size_t r = 0; r < nr; ++r) c->lg_rows_host[r] = r % n;
+  DSGD_CUDA(cudaMemcpyAsync(c->lg_rows, c->lg_rows_host.data(), nr * sizeof(uint64_t),
+                            cudaMemcpyHostToDevice, c->stream));
+  dsgd::LogisticArgs<T> a{};
+  a.X = as<T>(c->lg_X);
+  a.y = c->lg_y;
+  for (uint32_t k = 0; k < p; ++k) a.theta[k] = as<T>(c->peers[k].theta[c->cur]);
+  a.rows = c->lg_rows;
+  a.partial = c->lg_scratch;
+  a.coeff = c->lg_scratch + nr * nblk;
+  a.d = c->d;
+  a.n_nodes = p;
+  a.batch = (uint32_t)n;
+  a.nblk = nblk;
+  a.value_mode = 1;
+  {
+    LaunchScope ls(c, DSGD_K_OTHER);
+    DSGD_CUDA(dsgd::launch_logistic<T>(a, 1, c->stream));
+    c->kernels += 1;
+  }
+  std::vector<double> terms(nr);
+  DSGD_CUDA(cudaMemcpyAsync(terms.data(), a.coeff, nr * sizeof(double), cudaMemcpyDeviceToHost,
+                            c->stream));
+  DSGD_CUDA(cudaStreamSynchronize(c->stream));
+  double total = 0.0;
+  for (uint32_t k = 0; k < p; ++k) {
+    double s = 0.0;
+    for (uint64_t r = 0; r < n; ++r) s += terms[(size_t)k * n + r];
+    total += s / (double)n;
+  }
+  *data = total;
+  return DSGD_OK;
+}
+
 std::vector<uint32_t> all_local(const dsgd_ctx* c) {
   std::vector<uint32_t> v(c->n_local);
   for (uint32_t i = 0; i < c->n_local; ++i) v[i] = i;
@@ -1820,6 +1877,14 @@ dsgd_status dsgd_trace(dsgd_ctx* c, double* sq_err_consensus, double* loss_mean,
     if (sq_err_consensus) *sq_err_consensus = c->norm_host[0];
     if (loss_mean) *loss_mean = c->spec ? 0.5 * c->norm_host[1] / c->p : 0.0;
     if (sq_err_opt) *sq_err_opt = c->spec ? c->norm_host[2] : 0.0;
+    if (loss_mean && c->lg_X) {
+      // LogisticObjective::value objectives.cpp:116-125 of every node:
+      // mean over rows of log1pexp(z) - y z, plus 0.5 l2 ||theta||^2 (the
+      // trace kernel's sum of squares with no optimum)
+      double data = 0.0;
+      DSGD_TRY(logistic_values<T>(c, &data));
+      *loss_mean = (data + 0.5 * c->lg_l2 * c->norm_host[2]) / c->p;
+    }
     return DSGD_OK;
   });
 }

@@ -29,6 +29,9 @@ def main():
              "gossip-fresh": O.FRESH}
     if len(sys.argv) > 2 and sys.argv[2] == "allreduce-only":
         names = {"all-reduce": O.ALLREDUCE, "all-reduce-pn": O.ALLREDUCE}
+    if len(sys.argv) > 2 and sys.argv[2] == "logistic":
+        logistic(rank, world, local, dtype, dist)
+        return
     for proto, oid in names.items():
         d = 1031
         hk = dict(alpha0=0.05, anneal_at=(20,), mu=0.9, weight_decay=1e-4, beta_gossip=0.4,
@@ -104,6 +107,71 @@ def main():
                               "backend": getattr(g, "allreduce_backend", "")}
         dist.barrier()
         g.close()
+    if rank == 0:
+        print("RESULT " + json.dumps(results), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def logistic(rank, world, local, dtype, dist):
+    """F1 on one node per GPU: the sharded LogisticObjective (rows from each
+    rank's sample stream) through every protocol; rank 0 compares with the
+    single-context run of the same configuration (itself pinned to the
+    reference's trajectories by tests/test_gpu_logistic.py).  Gossip and
+    EASGD run the same kernels in the same order -> bit-exact; the
+    all-reduce sums in ring order vs the pivot mean -> tolerance."""
+    from paper_1611_04581_b200 import driver as D
+    from paper_1611_04581_b200 import protocols as P
+    from paper_1611_04581_b200.engine import Group, Hyperparams
+    from tests.golden.make_golden import logistic_dataset
+    X, y, l2, _ = logistic_dataset()
+    n, d = X.shape
+    obj = P.LogisticObjective(X, y, l2)
+    shards = [obj.shard(n * i // world, n * (i + 1) // world) for i in range(world)]
+    hk = dict(alpha0=0.5, anneal_at=(10,), mu=0.9, weight_decay=1e-4, beta_gossip=0.4,
+              beta_ea=0.15, tau=1, batch=3)
+    results = {}
+    for proto in ("all-reduce", "elastic-avg", "pull-gossip", "push-gossip", "gossip-stale",
+                  "gossip-fresh"):
+        dcfg = D.SimConfig(protocol=proto, p=world, hyper=Hyperparams(**hk),
+                           noise=P.NoiseModel.gaussian_per_coord(0.01, d),
+                           init=D.InitSpec("gaussian-spread", scale=0.5),
+                           momentum_scope="aggregate", rounds=20, run_id=f"mgl/{proto}")
+        thetas = D.make_initial_nodes(dcfg, obj)
+        g = Group.distributed(d, rank, world, local, dtype=dtype, noise=True,
+                              center=proto == "elastic-avg")
+        g.set_timeout(20.0)
+        g.set_logistic(X, y, l2)
+        g.logistic_set_sample_range(0, *shards[rank].range)
+        g.set_state(0, thetas[rank])
+        if proto == "elastic-avg" and rank == 0:
+            npd = np.float64 if dtype == "f64" else np.float32
+            th = thetas.astype(npd)
+            dev = np.zeros(d, dtype=npd)
+            for i in range(1, world):
+                dev = dev + (th[i] - th[0])
+            g.set_center((th[0] + dev * (npd(1) / npd(world))).astype(np.float64))
+        dist.barrier()
+        g.seed_streams(1, f"mgl/{proto}")
+        g.run_rounds(D.PROTOCOLS[proto], Hyperparams(**hk), 20, scope="aggregate",
+                     grad="logistic", host_noise_sigma=0.01)
+        g.sync()
+        th, dp, t = g.get_state(0)
+        center = g.get_center() if proto == "elastic-avg" and rank == 0 else None
+        allst = [None] * world
+        dist.all_gather_object(allst, (th, dp, t))
+        dist.barrier()
+        g.close()
+        if rank == 0:
+            r = D.run_sync(dcfg, obj, dtype=dtype, device=local, node_objs=shards)
+            dev_th = np.array([s_[0] for s_ in allst])
+            rel = float(np.abs(dev_th - r.theta).max() / np.abs(r.theta).max())
+            res = {"bit_exact": dev_th.tobytes() == r.theta.tobytes(), "max_rel": rel,
+                   "t_ok": [int(s_[2]) for s_ in allst] == r.t.tolist()}
+            if center is not None:
+                res["center_exact"] = center.tobytes() == r.center.tobytes()
+            results[proto] = res
+        dist.barrier()
     if rank == 0:
         print("RESULT " + json.dumps(results), flush=True)
     dist.barrier()

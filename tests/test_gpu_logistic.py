@@ -287,3 +287,18 @@ def test_logistic_errors():
     with pytest.raises(N.DsgdError, match="seed_streams"):
         g.local_sgd_step(Hyperparams(**HK(batch=1)), grad="logistic")
     g.close()
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_logistic_trace_loss_matches_oracle(dtype):
+    """make_trace_record's loss_mean (simulator.cpp:101-110) with the
+    logistic objective: mean over nodes of LogisticObjective::value."""
+    X, y, l2 = dataset(n=30, d=2001)
+    p = 5
+    g, theta, _, _, _ = setup(p, dtype, X, y, l2, seed=8)
+    th = theta.astype(np.float64)
+    want = np.mean([O.logistic_value(X.astype(NP[dtype]).astype(np.float64), y, l2, th[i])
+                    for i in range(p)])
+    tr = g.trace()
+    assert tr["loss_mean"] == pytest.approx(want, rel=1e-12)
+    g.close()

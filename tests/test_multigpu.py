@@ -58,3 +58,30 @@ def test_multi_gpu_protocols_match_oracle(world, dtype, backend):
             assert r["bit_exact"], (proto, r)
         if r["center_exact"] is not None:
             assert r["center_exact"], (proto, r)
+
+
+@pytest.mark.skipif("n_gpus() < 2")
+@pytest.mark.parametrize("world", worlds())
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_multi_gpu_logistic_matches_single_context(world, dtype):
+    """F1 across GPUs: the device logistic gradient with sharded sample
+    ranges, one node per GPU, against the single-context run (gossip/EASGD
+    bit-exact; all-reduce within 1e-12 / 1e-5: ring vs pivot summation)."""
+    port = 29711 + 4 * (world // 2) + (dtype == "f32")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(ROOT, "tests", "mgpu_worker.py"), dtype, "logistic"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    line = [l for l in out.stdout.splitlines() if l.startswith("RESULT ")][0]
+    res = json.loads(line[7:])
+    assert set(res) == {"all-reduce", "elastic-avg", "pull-gossip", "push-gossip",
+                        "gossip-stale", "gossip-fresh"}
+    for proto, r in res.items():
+        assert r["t_ok"], (proto, r)
+        if proto == "all-reduce":
+            assert r["max_rel"] <= (1e-12 if dtype == "f64" else 1e-5), (proto, r)
+        else:
+            assert r["bit_exact"], (proto, r)
+        if "center_exact" in r:
+            assert r["center_exact"], (proto, r)

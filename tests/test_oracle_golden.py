@@ -473,3 +473,15 @@ def test_ref_logistic_constructor_errors():
         O.ref_set_logistic(np.ones((2, 2)), [0, 1], 0.0)
     with pytest.raises(ValueError, match="labels must be 0 or 1"):
         O.ref_set_logistic(np.ones((2, 2)), [0, 2], 0.1)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_ref_logistic_value_bit_exact():
+    rng = np.random.default_rng(12)
+    X = rng.standard_normal((30, 17)) * 3
+    y = rng.integers(0, 2, 30).astype(np.int32)
+    O.ref_set_logistic(X, y, 0.2)
+    for _ in range(3):
+        th = rng.standard_normal(17) * 4
+        assert O.logistic_value(X, y, 0.2, th) == O.ref_logistic_value(th)
+    O.ref_set_logistic(None, None, 0.0)
