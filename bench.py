@@ -292,14 +292,18 @@ def main():
         kdesc = "k_step<ApplyDelta>: read theta, avg, g; write theta', delta' (then ncclAllReduce)"
     kms, kn = prof.get(kname, (0.0, 0))
     kavg_ms = kms / max(1, kn)
-    achieved = (bpp * d / (kavg_ms * 1e-3) / 1e9) if kn else None
-    t_hbm = bpp * d / (peak * 1e9)
-    t_nv = nv_bytes / (nv_peak * 1e9) if (world > 1 and kname == "allreduce_comm") else 0.0
+    # parameters one launch processes: d, or d / K with K pipelines per round
+    units = d * args.steps / kn if kn else d
+    achieved = (bpp * units / (kavg_ms * 1e-3) / 1e9) if kn else None
+    t_hbm = bpp * units / (peak * 1e9)
+    t_nv = (nv_bytes * units / d / (nv_peak * 1e9)
+            if (world > 1 and kname == "allreduce_comm") else 0.0)
     bound = "nvlink" if t_nv > t_hbm else "hbm"
     roofline = {"bound": bound, "kernel": kdesc, "achieved": achieved, "peak": peak,
                 "peak_source": peak_src, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": None,
-                "algorithmic_bytes_per_launch": bpp * d,
+                "algorithmic_bytes_per_launch": bpp * units,
+                "params_per_launch": units,
                 "kernel_avg_us": kavg_ms * 1e3,
                 "roofline_time_us": max(t_hbm, t_nv) * 1e6,
                 "frac_of_roofline_time": (max(t_hbm, t_nv) / (kavg_ms * 1e-3)) if kn else None,
@@ -308,14 +312,27 @@ def main():
     if world > 1:
         nms, nn = prof.get("allreduce_comm", (0.0, 0))
         t_c = nms / max(1, nn) * 1e-3
+        nv_launch = nv_bytes * (args.steps / nn if nn else 1.0)  # per launch (K pipelines)
         roofline["allreduce_backend"] = backend
+        roofline["allreduce_launches_per_round"] = nn / args.steps if nn else None
         if getattr(grp, "nvls_unavailable", None):
             roofline["nvls_unavailable"] = grp.nvls_unavailable
         roofline["allreduce_comm_us"] = t_c * 1e6
-        roofline["nvlink_bytes_per_direction"] = nv_bytes
-        roofline["nvlink_achieved_gbs"] = nv_bytes / t_c / 1e9 if nn else None
+        roofline["nvlink_bytes_per_direction_per_round"] = nv_bytes
+        roofline["nvlink_achieved_gbs"] = nv_launch / t_c / 1e9 if nn else None
         roofline["nvlink_peak_gbs"] = nv_peak
-        roofline["nvlink_frac"] = (nv_bytes / t_c / 1e9 / nv_peak) if nn else None
+        roofline["nvlink_frac"] = (nv_launch / t_c / 1e9 / nv_peak) if nn else None
+        # SM-issued symmetric exchange measured on this pool (both GPUs of a
+        # pair reading / writing each other at once, profiles/r1_nvlink_probe.txt)
+        roofline["nvlink_sm_exchange_gbs"] = {"peer_read": 630.0, "peer_write": 668.0}
+        if bound == "nvlink" and nn:
+            # the dominant kernel is NVLink-bound: report it against the link
+            roofline["hbm_achieved"] = roofline["achieved"]
+            roofline["hbm_frac"] = roofline["frac"]
+            roofline["achieved"] = nv_launch / t_c / 1e9
+            roofline["peak"] = nv_peak
+            roofline["peak_source"] = "B200_PROFILING.md measured peer copy per direction"
+            roofline["frac"] = roofline["achieved"] / nv_peak
     per_kernel = {k: {"ms_total": v[0], "launches": v[1]} for k, v in prof.items() if v[1]}
 
     # ---------------- end-to-end through the C ABI (host gradients, pinned)
