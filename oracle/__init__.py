@@ -209,6 +209,9 @@ def ref():
                                            C.c_uint64, C.c_uint64, C.c_void_p]
         _ref.ref_logistic_value.restype = C.c_double
         _ref.ref_logistic_value.argtypes = [C.c_void_p, C.c_uint64]
+        _ref.ref_run_traced.restype = C.c_long
+        _ref.ref_run_traced.argtypes = [C.POINTER(Sim), C.c_uint64, C.c_void_p, C.c_uint64,
+                                        C.c_char_p, C.c_uint64]
         _ref.ref_time_rounds.restype = C.c_double
         _ref.ref_time_rounds.argtypes = [C.c_int, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int,
                                          C.POINTER(Hyper)]
@@ -535,6 +538,19 @@ def ref_run(cfg: SimConfig, transport: bool = False, chaos_seed: int = 0):
     else:
         _ref_check(ref().ref_run(C.byref(s), _ptr(theta), _ptr(dprev), _ptr(t), _ptr(center)))
     return theta, dprev, t, center
+
+
+def ref_run_traced(cfg: SimConfig, trace_every: int, max_records: int = 4096):
+    """run_simulation with trace_every: records [n, 6] = (t, sim_time,
+    sq_err_opt, sq_err_consensus, loss_mean, alpha), NaN for an absent
+    optional, and the reference's own JSONL text (trace_io.cpp) when built."""
+    rec = np.zeros((max_records, 6))
+    buf = C.create_string_buffer(1 << 20)
+    s = cfg.to_c()
+    n = ref().ref_run_traced(C.byref(s), trace_every, _ptr(rec), max_records, buf, len(buf))
+    if n < 0:
+        raise ValueError(ref().ref_last_error().decode())
+    return rec[:n], buf.value.decode()
 
 
 REF_ROUND = {"allreduce": 0, "ea": 1, "pull": 2, "push": 3, "stale": 4, "fresh": 5,

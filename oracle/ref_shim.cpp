@@ -12,6 +12,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <limits>
 #include <memory>
 #include <span>
 #include <string>
@@ -25,6 +26,9 @@
 #include "dsgd/simulator.hpp"
 #include "dsgd/transport.hpp"
 #include "dsgd_oracle.h"
+#ifdef REF_HAVE_TRACE_IO
+#include "dsgd/trace_io.hpp"
+#endif
 
 using namespace dsgd;
 
@@ -234,6 +238,59 @@ int ref_run(const dsgdo_sim* c, double* theta, double* dprev, std::uint64_t* t,
       std::memcpy(center, r.final_server->theta_center.raw(), sizeof(double) * c->d);
     }
     return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// run_simulation with trace_every: the trace records as rows of
+// {t, sim_time (NaN: none), sq_err_opt (NaN: none), sq_err_consensus,
+// loss_mean, alpha} and, when trace_io.cpp is compiled in, the JSONL text
+// of write_trace_jsonl (trace_io.cpp:40-51).  Returns the record count or -1.
+long ref_run_traced(const dsgdo_sim* c, std::uint64_t trace_every, double* rec,
+                    std::uint64_t max_rec, char* jsonl, std::uint64_t jsonl_cap) {
+  try {
+    SimConfig cfg = to_sim(*c);
+    cfg.trace_every = trace_every;
+    RunResult r;
+    if (g_logistic.set) {
+      LogisticObjective eval(g_logistic.X, g_logistic.y, g_logistic.l2);
+      std::vector<std::unique_ptr<LogisticObjective>> own;
+      std::vector<const Objective*> objs;
+      for (std::uint32_t i = 0; i < c->p; ++i) {
+        own.push_back(logistic_for(i));
+        objs.push_back(own.back().get());
+      }
+      r = (cfg.clock.kind == ClockModel::Kind::kPoisson) ? run_async(cfg, eval, objs)
+                                                         : run_sync(cfg, eval, objs);
+    } else {
+      QuadraticObjective obj(std::vector<double>(c->spectrum, c->spectrum + c->d),
+                             ParamVec(std::vector<double>(c->opt, c->opt + c->d)));
+      r = run_simulation(cfg, obj);
+    }
+    const double nan = std::numeric_limits<double>::quiet_NaN();
+    std::string text;
+    for (std::size_t k = 0; k < r.trace.size() && k < max_rec; ++k) {
+      const TraceRecord& t = r.trace[k];
+      double* o = rec + 6 * k;
+      o[0] = static_cast<double>(t.t);
+      o[1] = t.sim_time.value_or(nan);
+      o[2] = t.sq_err_opt.value_or(nan);
+      o[3] = t.sq_err_consensus;
+      o[4] = t.loss_mean;
+      o[5] = t.alpha;
+#ifdef REF_HAVE_TRACE_IO
+      text += trace_record_to_json_line(t);
+      text += "\n";
+#endif
+    }
+    if (jsonl && jsonl_cap) {
+      const std::size_t n = std::min<std::size_t>(text.size(), jsonl_cap - 1);
+      std::memcpy(jsonl, text.data(), n);
+      jsonl[n] = 0;
+    }
+    return static_cast<long>(r.trace.size());
   } catch (const std::exception& e) {
     g_err = e.what();
     return -1;

@@ -8,14 +8,15 @@ make_initial_nodes (simulator.cpp:162-208) and collects the result.
 """
 from __future__ import annotations
 
+import json
 import math
 from dataclasses import dataclass, field
-from typing import Optional, Sequence
+from typing import List, Optional, Sequence
 
 import numpy as np
 
 from . import _native as N
-from .engine import Group, Hyperparams, Stream
+from .engine import Group, Hyperparams, Stream, step_size_at
 from .protocols import InvalidArgument, LogisticObjective, NoiseModel, QuadraticObjective
 
 PROTOCOLS = {"all-reduce": N.ALLREDUCE, "elastic-avg": N.ELASTIC_AVG,
@@ -47,6 +48,53 @@ class SimConfig:
     rate_per_node: float = 1.0
     seed: int = 1
     run_id: str = "run"
+    trace_every: int = 10             # simulator.hpp:86
+    exchange_latency: float = 0.0     # added to gated gossip rounds (virtual time)
+    straggler_constant: float = 1.0   # StragglerModel kConstant (the default model)
+
+
+@dataclass
+class TraceRecord:
+    """dsgd::TraceRecord (core.hpp:105-116)."""
+    run_id: str
+    protocol: str
+    t: int
+    sim_time: Optional[float]
+    sq_err_opt: Optional[float]
+    sq_err_consensus: float
+    loss_mean: float
+    alpha: float
+
+    def to_json_line(self) -> str:
+        """trace_record_to_json_line (trace_io.cpp:40-51): nlohmann's
+        default object is a std::map, so keys come out sorted; compact."""
+        j = {"run_id": self.run_id, "protocol": self.protocol, "t": int(self.t),
+             "sim_time": self.sim_time, "sq_err_opt": self.sq_err_opt,
+             "sq_err_consensus": self.sq_err_consensus, "loss_mean": self.loss_mean,
+             "alpha": self.alpha}
+        return json.dumps(j, sort_keys=True, separators=(",", ":"))
+
+    @staticmethod
+    def from_json_line(line: str) -> "TraceRecord":
+        """trace_record_from_json_line (trace_io.cpp:53-77)."""
+        try:
+            j = json.loads(line)
+        except ValueError as e:
+            raise RuntimeError(f"trace line is not valid JSON: {e}")
+        try:
+            proto = j["protocol"]
+            if proto not in PROTOCOLS:
+                raise RuntimeError("unknown protocol name: " + str(proto))
+            opt = lambda k: None if j[k] is None else float(j[k])  # noqa: E731
+            return TraceRecord(str(j["run_id"]), proto, int(j["t"]), opt("sim_time"),
+                               opt("sq_err_opt"), float(j["sq_err_consensus"]),
+                               float(j["loss_mean"]), float(j["alpha"]))
+        except (KeyError, TypeError) as e:
+            raise RuntimeError(f"trace line missing or mistyped field: {e}")
+
+
+def write_trace_jsonl(trace: Sequence[TraceRecord]) -> str:
+    return "".join(r.to_json_line() + "\n" for r in trace)
 
 
 @dataclass
@@ -55,6 +103,8 @@ class RunResult:
     delta_prev: np.ndarray     # [p, d]
     t: np.ndarray              # [p]
     center: Optional[np.ndarray] = None
+    trace: List[TraceRecord] = field(default_factory=list)
+    sim_time: float = 0.0
 
 
 def make_initial_nodes(cfg: SimConfig, obj: QuadraticObjective) -> np.ndarray:
@@ -124,6 +174,27 @@ def _grad_kind(obj) -> str:
     return "logistic" if isinstance(obj, LogisticObjective) else "quadratic"
 
 
+def _record(g: Group, cfg: SimConfig, obj, t: int, sim_time: float, alpha: float) -> TraceRecord:
+    """make_trace_record (simulator.cpp:92-123) on the device: one fused
+    reduction over every node's theta (fp64 accumulation)."""
+    m = g.trace()
+    return TraceRecord(cfg.run_id, cfg.protocol, t, sim_time,
+                       m["sq_err_opt"] if obj.optimum() is not None else None,
+                       m["sq_err_consensus"], m["loss_mean"], alpha)
+
+
+def _round_time(cfg: SimConfig, gated: bool) -> float:
+    """Virtual time of one synchronous round under the constant straggler
+    model (simulator.cpp:240-349): every node takes `constant`, gated gossip
+    rounds add the exchange latency (push only when p > 1)."""
+    lat = 0.0
+    if gated and cfg.protocol in ("pull-gossip", "gossip-stale", "gossip-fresh"):
+        lat = cfg.exchange_latency
+    if gated and cfg.protocol == "push-gossip" and cfg.p > 1:
+        lat = cfg.exchange_latency
+    return cfg.straggler_constant + lat
+
+
 def run_sync(cfg: SimConfig, obj: QuadraticObjective, dtype: str = "f64",
              device: int = 0, node_objs=None) -> RunResult:
     """run_sync for all-reduce, elastic-avg, pull/push gossip, gossip-stale
@@ -134,6 +205,10 @@ def run_sync(cfg: SimConfig, obj: QuadraticObjective, dtype: str = "f64",
         raise InvalidArgument("async-pull requires the asynchronous driver")
     if cfg.rounds == 0:
         raise InvalidArgument("rounds must be >= 1")
+    if cfg.trace_every == 0:
+        raise InvalidArgument("trace_every must be >= 1")
+    if not cfg.straggler_constant > 0:
+        raise InvalidArgument("straggler constant must be positive")
     d = obj.dim()
     if cfg.noise is not None and cfg.noise.dim != d:
         raise InvalidArgument("noise dimension must match objective dimension")
@@ -146,15 +221,26 @@ def run_sync(cfg: SimConfig, obj: QuadraticObjective, dtype: str = "f64",
             g.ea_init_center()   # spatial_mean(theta_0)  simulator.cpp:62-67
         g.seed_streams(cfg.seed, cfg.run_id)
         sigma = cfg.noise.sigma if cfg.noise is not None and cfg.noise.kind != "zero" else 0.0
-        g.run_rounds(PROTOCOLS[cfg.protocol], cfg.hyper, cfg.rounds,
-                     scope=cfg.momentum_scope, grad=_grad_kind(obj), host_noise_sigma=sigma)
+        h = cfg.hyper
+        trace = [_record(g, cfg, obj, 0, 0.0, step_size_at(h, 0))]
+        done, sim_time = 0, 0.0
+        while done < cfg.rounds:
+            # run up to the next trace point in one library call (the round
+            # loop itself runs in C++)
+            k = min(cfg.trace_every - done % cfg.trace_every, cfg.rounds - done)
+            g.run_rounds(PROTOCOLS[cfg.protocol], h, k,
+                         scope=cfg.momentum_scope, grad=_grad_kind(obj), host_noise_sigma=sigma)
+            for r in range(done, done + k):
+                sim_time += _round_time(cfg, r > 0 and r % h.tau == 0)
+            done += k
+            trace.append(_record(g, cfg, obj, done, sim_time, step_size_at(h, done)))
         th = np.zeros((cfg.p, d))
         dp = np.zeros((cfg.p, d))
         t = np.zeros(cfg.p, dtype=np.uint64)
         for i in range(cfg.p):
             th[i], dp[i], t[i] = g.get_state(i)
         center = g.get_center() if cfg.protocol == "elastic-avg" else None
-        return RunResult(th, dp, t, center)
+        return RunResult(th, dp, t, center, trace, sim_time)
     finally:
         g.close()
 
@@ -167,6 +253,8 @@ def run_async_elastic(cfg: SimConfig, obj: QuadraticObjective, dtype: str = "f64
     step -- one fused event kernel per tick."""
     if cfg.events == 0:
         raise InvalidArgument("events must be >= 1")
+    if cfg.trace_every == 0:
+        raise InvalidArgument("trace_every must be >= 1")
     d = obj.dim()
     thetas = make_initial_nodes(cfg, obj)
     use_noise = cfg.noise is not None and cfg.noise.kind != "zero"
@@ -179,20 +267,25 @@ def run_async_elastic(cfg: SimConfig, obj: QuadraticObjective, dtype: str = "f64
         noise = [Stream.make(cfg.seed, cfg.run_id, i, "gradient-noise") for i in range(cfg.p)]
         t = [0] * cfg.p
         tau = cfg.hyper.tau
-        for _ in range(cfg.events):
-            clock.exponential(cfg.p * cfg.rate_per_node)
+        trace = [_record(g, cfg, obj, 0, 0.0, step_size_at(cfg.hyper, 0))]
+        sim_time = 0.0
+        for k in range(cfg.events):
+            sim_time += clock.exponential(cfg.p * cfg.rate_per_node)
             i = clock.uniform_index(cfg.p)
+            alpha = step_size_at(cfg.hyper, t[i])
             if use_noise:
                 g.set_vector(i, N.BUF_NOISE, noise[i].fill_normal(cfg.noise.sigma, d))
             gated = t[i] > 0 and t[i] % tau == 0
             g.ea_client_event(cfg.hyper, i, gated, grad=_grad_kind(obj), noise=use_noise)
             t[i] += 1
+            if (k + 1) % cfg.trace_every == 0 or k + 1 == cfg.events:
+                trace.append(_record(g, cfg, obj, k + 1, sim_time, alpha))
         th = np.zeros((cfg.p, d))
         dp = np.zeros((cfg.p, d))
         tt = np.zeros(cfg.p, dtype=np.uint64)
         for i in range(cfg.p):
             th[i], dp[i], tt[i] = g.get_state(i)
-        return RunResult(th, dp, tt, g.get_center())
+        return RunResult(th, dp, tt, g.get_center(), trace, sim_time)
     finally:
         g.close()
 
@@ -204,6 +297,8 @@ def run_async_pull(cfg: SimConfig, obj: QuadraticObjective, dtype: str = "f64",
     event kernel per tick."""
     if cfg.events == 0:
         raise InvalidArgument("events must be >= 1")
+    if cfg.trace_every == 0:
+        raise InvalidArgument("trace_every must be >= 1")
     d = obj.dim()
     thetas = make_initial_nodes(cfg, obj)
     use_noise = cfg.noise is not None and cfg.noise.kind != "zero"
@@ -214,18 +309,25 @@ def run_async_pull(cfg: SimConfig, obj: QuadraticObjective, dtype: str = "f64",
         clock = Stream.make(cfg.seed, cfg.run_id, 0xFFFFFFFF, "clock")
         partner = [Stream.make(cfg.seed, cfg.run_id, i, "partner-choice") for i in range(cfg.p)]
         noise = [Stream.make(cfg.seed, cfg.run_id, i, "gradient-noise") for i in range(cfg.p)]
-        for _ in range(cfg.events):
-            clock.exponential(cfg.p * cfg.rate_per_node)
+        tn = [0] * cfg.p
+        trace = [_record(g, cfg, obj, 0, 0.0, step_size_at(cfg.hyper, 0))]
+        sim_time = 0.0
+        for k in range(cfg.events):
+            sim_time += clock.exponential(cfg.p * cfg.rate_per_node)
             i = clock.uniform_index(cfg.p)
+            alpha = step_size_at(cfg.hyper, tn[i])
             j = partner[i].uniform_index(cfg.p)
             if use_noise:
                 g.set_vector(i, N.BUF_NOISE, noise[i].fill_normal(cfg.noise.sigma, d))
             g.async_pull_event(cfg.hyper, i, j, grad=_grad_kind(obj), noise=use_noise)
+            tn[i] += 1
+            if (k + 1) % cfg.trace_every == 0 or k + 1 == cfg.events:
+                trace.append(_record(g, cfg, obj, k + 1, sim_time, alpha))
         th = np.zeros((cfg.p, d))
         dp = np.zeros((cfg.p, d))
         t = np.zeros(cfg.p, dtype=np.uint64)
         for i in range(cfg.p):
             th[i], dp[i], t[i] = g.get_state(i)
-        return RunResult(th, dp, t)
+        return RunResult(th, dp, t, None, trace, sim_time)
     finally:
         g.close()

@@ -113,13 +113,36 @@ def make_logistic():
     np.savez(os.path.join(HERE, "logistic.npz"), **out)
 
 
+# make_trace_record cadence cases: (RUN_CASES / LOGISTIC_CASES name, trace_every)
+TRACE_CASES = {"c1_allreduce": 250, "pull8": 7, "push5": 9, "ea8": 10, "stale4": 10,
+               "fresh4": 6, "async8": 50, "ea8_poisson": 40, "lg_pull": 8}
+
+
+def make_traces():
+    out = {}
+    X, y, l2, ranges = logistic_dataset()
+    for name, every in TRACE_CASES.items():
+        if name.startswith("lg_"):
+            O.ref_set_logistic(X, y, l2, ranges)
+            cfg = LOGISTIC_CASES[name]
+        else:
+            O.ref_set_logistic(None, None, 0.0)
+            cfg = RUN_CASES[name]
+        rec, text = O.ref_run_traced(cfg, every)
+        out[f"{name}_rec"] = rec
+        out[f"{name}_jsonl"] = np.array(text)
+    O.ref_set_logistic(None, None, 0.0)
+    np.savez(os.path.join(HERE, "traces.npz"), **out)
+
+
 def main():
     if not O.ref_available():
         raise SystemExit("oracle/_ref not built: needs /root/reference")
-    if sys.argv[1:] == ["logistic"]:
-        make_logistic()
+    if sys.argv[1:] in (["logistic"], ["traces"]):
+        {"logistic": make_logistic, "traces": make_traces}[sys.argv[1]]()
         return
     make_logistic()
+    make_traces()
     seed = 0x5EED
     np.savez(os.path.join(HERE, "streams.npz"), seed=np.uint64(seed), n=np.uint64(7),
              u64=O.ref_stream(seed, 0, 1000), normal=O.ref_stream(seed, 2, 500),

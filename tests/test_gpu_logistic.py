@@ -302,3 +302,19 @@ def test_logistic_trace_loss_matches_oracle(dtype):
     tr = g.trace()
     assert tr["loss_mean"] == pytest.approx(want, rel=1e-12)
     g.close()
+
+
+def test_logistic_trace_records_match_reference():
+    """The logistic run's trace (no optimum: sq_err_opt null; loss =
+    LogisticObjective::value) against the reference's records."""
+    from tests.golden.make_golden import TRACE_CASES
+    cfg, dc, obj, shards = _driver_case("lg_pull")
+    dc.trace_every = TRACE_CASES["lg_pull"]
+    r = D.run_sync(dc, obj, dtype="f64", node_objs=shards)
+    gold = np.load("tests/golden/traces.npz")["lg_pull_rec"]
+    assert len(r.trace) == len(gold)
+    for rec, g in zip(r.trace, gold):
+        assert rec.t == int(g[0]) and rec.sim_time == g[1] and rec.alpha == g[5]
+        assert rec.sq_err_opt is None and np.isnan(g[2])
+        assert rec.sq_err_consensus == pytest.approx(g[3], rel=1e-8)
+        assert rec.loss_mean == pytest.approx(g[4], rel=1e-9)

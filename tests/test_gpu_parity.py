@@ -561,3 +561,33 @@ def test_device_tracer_records_launches():
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                          timeout=120, cwd=__import__("os").path.dirname(__import__("os").path.dirname(__file__)))
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr
+
+
+@pytest.mark.parametrize("name", ["c1_allreduce", "pull8", "push5", "ea8", "stale4", "fresh4",
+                                  "async8", "ea8_poisson"])
+def test_trace_records_match_reference(name):
+    """F3: run_sync / run_async trace records (make_trace_record every
+    trace_every rounds/events, simulator.cpp:356-361 / 431-434) against the
+    compiled reference's: t, sim_time and alpha exact; the metrics are fp64
+    reductions in another order (relative 1e-11)."""
+    from tests.golden.make_golden import RUN_CASES, TRACE_CASES
+    cfg = RUN_CASES[name]
+    gold = np.load("tests/golden/traces.npz")[f"{name}_rec"]
+    obj = P.QuadraticObjective(cfg.spectrum, cfg.opt)
+    dc = to_driver(cfg)
+    dc.trace_every = TRACE_CASES[name]
+    if cfg.protocol == O.ASYNC_PULL:
+        r = D.run_async_pull(dc, obj, dtype="f64")
+    elif cfg.poisson:
+        r = D.run_async_elastic(dc, obj, dtype="f64")
+    else:
+        r = D.run_sync(dc, obj, dtype="f64")
+    assert len(r.trace) == len(gold)
+    for rec, g in zip(r.trace, gold):
+        assert rec.t == int(g[0])
+        assert rec.sim_time == g[1]
+        assert rec.alpha == g[5]
+        assert rec.sq_err_opt == pytest.approx(g[2], rel=1e-11, abs=1e-300)
+        assert rec.sq_err_consensus == pytest.approx(g[3], rel=1e-11, abs=1e-300)
+        assert rec.loss_mean == pytest.approx(g[4], rel=1e-11, abs=1e-300)
+        assert rec.protocol == dc.protocol and rec.run_id == cfg.run_id

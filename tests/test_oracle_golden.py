@@ -485,3 +485,28 @@ def test_ref_logistic_value_bit_exact():
         th = rng.standard_normal(17) * 4
         assert O.logistic_value(X, y, 0.2, th) == O.ref_logistic_value(th)
     O.ref_set_logistic(None, None, 0.0)
+
+
+def test_golden_trace_jsonl_schema_round_trips():
+    """trace_record_to_json_line / _from_json_line (trace_io.cpp:40-77):
+    the driver's TraceRecord re-emits the reference's own JSONL lines byte
+    for byte (sorted keys, compact, shortest round-trip doubles, null for an
+    absent sim_time / sq_err_opt)."""
+    from paper_1611_04581_b200.driver import TraceRecord
+    g = _golden("traces.npz")
+    n = 0
+    for key in [k for k in g.files if k.endswith("_jsonl")]:
+        text = str(g[key])
+        if not text:
+            pytest.skip("fixture made without trace_io")
+        for line in text.splitlines():
+            assert TraceRecord.from_json_line(line).to_json_line() == line
+            n += 1
+    assert n > 50
+    with pytest.raises(RuntimeError, match="not valid JSON"):
+        TraceRecord.from_json_line("{")
+    with pytest.raises(RuntimeError, match="unknown protocol name"):
+        TraceRecord.from_json_line('{"alpha":1,"loss_mean":0,"protocol":"x","run_id":"r",'
+                                   '"sim_time":null,"sq_err_consensus":0,"sq_err_opt":null,"t":0}')
+    with pytest.raises(RuntimeError, match="missing or mistyped"):
+        TraceRecord.from_json_line('{"alpha":1}')
