@@ -131,6 +131,20 @@ def peaks():
 
 
 # ------------------------------------------------------------ reference arm
+def host_info() -> dict:
+    """CPU model and usable host threads of the box the baseline ran on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": len(os.sched_getaffinity(0))}
+
+
 def cpu_reference(protocol: int, p: int, d: int, rounds: int, threaded: bool):
     import oracle as O
     h = O.HyperParams(alpha0=0.1, anneal_at=(), mu=0.9, weight_decay=1e-4, beta_ea=0.1)
@@ -160,7 +174,7 @@ def run_reference(args, world, rank):
             "config": {"workload": "all-reduce SGD round, momentum 0.9, wd 1e-4 (configs[3])",
                        "d_per_worker": d_sample, "p": p, "parallelism": f"dp{p} (threads)"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
-                             "sample": sample},
+                             "sample": sample, "host": host_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -382,7 +396,8 @@ def main():
             cpu = {"value": d_s / (sec / rounds_cpu), "unit": UNIT, "cores": 1,
                    "kind": "reference" if O.ref_available() else "port",
                    "sample": f"{rounds_cpu} allreduce_round (p=1, d={d_s}) of the compiled "
-                             f"reference (oracle/_ref, -O3, fp64), single thread as the simulator"}
+                             f"reference (oracle/_ref, -O3, fp64), single thread as the simulator",
+                   "host": host_info()}
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
                    "sample": f"failed: {e}"}
