@@ -206,6 +206,10 @@ struct dsgd_ctx {
   double* lg_scratch = nullptr;               // partial dots + coefficients
   size_t lg_rows_cap = 0, lg_scratch_cap = 0;
   std::vector<uint64_t> lg_rows_host;
+  uint64_t* lg_pin[4] = {};                   // pinned staging ring for the rows (async H2D)
+  cudaEvent_t lg_ev[4] = {};
+  size_t lg_pin_cap = 0;
+  uint32_t lg_slot = 0;
 
   // worker-loop streams
   std::vector<dsgd_stream*> partner_streams;  // all p (every context draws the full map)
@@ -506,6 +510,31 @@ dsgd_status run_step_mode(dsgd_ctx* c, int mode, int kid, const dsgd_hyperparams
   return DSGD_OK;
 }
 
+// Copies lg_rows_host[0, nr) to the device rows buffer through a ring of
+// pinned slots (an async copy; a slot is reused once its copy completed), so
+// the host does not wait for the stream every round.
+dsgd_status stage_rows(dsgd_ctx* c, size_t nr) {
+  if (c->lg_pin_cap < nr) {
+    for (int k = 0; k < 4; ++k) {
+      if (c->lg_ev[k]) DSGD_CUDA(cudaEventSynchronize(c->lg_ev[k]));
+      cudaFreeHost(c->lg_pin[k]);
+      c->lg_pin[k] = nullptr;
+    }
+    for (int k = 0; k < 4; ++k) {
+      DSGD_CUDA(cudaMallocHost(&c->lg_pin[k], nr * sizeof(uint64_t)));
+      if (!c->lg_ev[k]) DSGD_CUDA(cudaEventCreateWithFlags(&c->lg_ev[k], cudaEventDisableTiming));
+    }
+    c->lg_pin_cap = nr;
+  }
+  const uint32_t k = c->lg_slot++ % 4;
+  DSGD_CUDA(cudaEventSynchronize(c->lg_ev[k]));
+  std::memcpy(c->lg_pin[k], c->lg_rows_host.data(), nr * sizeof(uint64_t));
+  DSGD_CUDA(cudaMemcpyAsync(c->lg_rows, c->lg_pin[k], nr * sizeof(uint64_t),
+                            cudaMemcpyHostToDevice, c->stream));
+  DSGD_CUDA(cudaEventRecord(c->lg_ev[k], c->stream));
+  return DSGD_OK;
+}
+
 // LogisticObjective::stochastic_gradient (objectives.cpp:147-162) of the
 // local nodes `nodes` at theta[cur] (+ mu * delta_prev when lookahead, the
 // compute_local_delta evaluation point protocols.cpp:90-93), written into
@@ -552,10 +581,7 @@ dsgd_status produce_logistic(dsgd_ctx* c, const dsgd_hyperparams* h, const GradS
     DSGD_CUDA(cudaMalloc(&c->lg_scratch, nr * (nblk + 1) * sizeof(double)));
     c->lg_scratch_cap = nr * (nblk + 1);
   }
-  // pageable source: the copy is staged before the call returns, so the
-  // host vector can be refilled next round
-  DSGD_CUDA(cudaMemcpyAsync(c->lg_rows, c->lg_rows_host.data(), nr * sizeof(uint64_t),
-                            cudaMemcpyHostToDevice, c->stream));
+  DSGD_TRY(stage_rows(c, nr));
   dsgd::LogisticArgs<T> a{};
   a.X = as<T>(c->lg_X);
   a.y = c->lg_y;
@@ -606,8 +632,7 @@ dsgd_status logistic_values(dsgd_ctx* c, double* data) {
   }
   c->lg_rows_host.resize(nr);
   for (size_t r = 0; r < nr; ++r) c->lg_rows_host[r] = r % n;
-  DSGD_CUDA(cudaMemcpyAsync(c->lg_rows, c->lg_rows_host.data(), nr * sizeof(uint64_t),
-                            cudaMemcpyHostToDevice, c->stream));
+  DSGD_TRY(stage_rows(c, nr));
   dsgd::LogisticArgs<T> a{};
   a.X = as<T>(c->lg_X);
   a.y = c->lg_y;
@@ -1322,6 +1347,10 @@ void dsgd_ctx_destroy(dsgd_ctx* c) {
   cudaFree(c->lg_y);
   cudaFree(c->lg_rows);
   cudaFree(c->lg_scratch);
+  for (int k = 0; k < 4; ++k) {
+    cudaFreeHost(c->lg_pin[k]);
+    if (c->lg_ev[k]) cudaEventDestroy(c->lg_ev[k]);
+  }
   for (const Prof& p : c->prof_pending) {
     cudaEventDestroy(p.a);
     cudaEventDestroy(p.b);
