@@ -156,19 +156,23 @@ def run_reference(args, world, rank):
         return
     import oracle as O
     p = max(1, args.gpus)
-    d_sample = min(args.d, 4_000_000)
+    d_sample = args.d              # the same per-worker size as our arm
     threaded = p > 1
-    cpu_reference(O.ALLREDUCE, p, d_sample, max(1, args.warmup), threaded)
-    sec = cpu_reference(O.ALLREDUCE, p, d_sample, max(1, args.steps), threaded)
-    per = sec / max(1, args.steps)
+    # bounded sample: at most 2 warm-up and 20 timed rounds (a 25M-param
+    # fp64 round takes ~0.7 s on one core), so the arm ends within minutes
+    steps = max(1, min(args.steps, 20))
+    cpu_reference(O.ALLREDUCE, p, d_sample, max(1, min(args.warmup, 2)), threaded)
+    sec = cpu_reference(O.ALLREDUCE, p, d_sample, steps, threaded)
+    per = sec / steps
     value = p * d_sample / per
     kind = "reference" if O.ref_available() else "port"
     cores = p if threaded else 1
-    sample = (f"{args.steps} allreduce_round steps of the compiled reference "
+    sample = (f"{steps} allreduce_round steps of the compiled reference "
               f"({'run_transport, ring_allreduce over p threads' if threaded else 'simulator rules, 1 thread'})"
               f", p={p}, d={d_sample} per worker (of {args.d})")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
+            "steps": steps, "steps_requested": args.steps, "warmup": args.warmup,
+            "ms_per_step": per * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": "all-reduce SGD round, momentum 0.9, wd 1e-4 (configs[3])",
