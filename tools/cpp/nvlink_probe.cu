@@ -93,6 +93,56 @@ __global__ void k_tma_write(char* dst, uint64_t ntiles) {
   }
 }
 
+// local HBM streaming (read 2 streams, write 1: the shape of an update kernel)
+__global__ void k_local(const uint4* __restrict__ a, const uint4* __restrict__ b,
+                        uint4* __restrict__ c, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint4 x = a[i], y = b[i];
+    c[i] = make_uint4(x.x ^ y.x, x.y ^ y.y, x.z ^ y.z, x.w ^ y.w);
+  }
+}
+
+// Concurrency: does SM-issued NVLink traffic slow a co-running HBM kernel?
+int interference(void* const* buf, uint4* const* sink) {
+  const uint64_t lb = 400ull << 20;  // 400 MB per local array
+  void *a, *b, *c;
+  CK(cudaSetDevice(0));
+  CK(cudaMalloc(&a, lb)); CK(cudaMalloc(&b, lb)); CK(cudaMalloc(&c, lb));
+  cudaStream_t s0, s1; CK(cudaStreamCreate(&s0)); CK(cudaStreamCreate(&s1));
+  cudaEvent_t ev[4]; for (auto& x : ev) CK(cudaEventCreate(&x));
+  const uint64_t nl = lb / 16, np = (100ull << 20) / 16;
+  for (int mode = 0; mode < 6; ++mode) {  // 0 local, 1 peer ld, 2 both, 3 peer st, 4 local+st, 5 local+bulk rd
+    float bl = 1e9f, bp = 1e9f;
+    for (int rep = 0; rep < 5; ++rep) {
+      CK(cudaDeviceSynchronize());
+      if (mode != 1 && mode != 3) {
+        CK(cudaEventRecord(ev[0], s0));
+        k_local<<<148 * 4, 512, 0, s0>>>((const uint4*)a, (const uint4*)b, (uint4*)c, nl);
+        CK(cudaEventRecord(ev[1], s0));
+      }
+      if (mode >= 1) {
+        CK(cudaEventRecord(ev[2], s1));
+        if (mode == 1 || mode == 2) k_read<<<148 * 2, 512, 0, s1>>>((const uint4*)buf[1], np, sink[0]);
+        if (mode == 3 || mode == 4) k_write<<<148 * 2, 512, 0, s1>>>((uint4*)buf[1], np);
+        if (mode == 5) k_tma_read<<<148, 512, 128 + STAGES * TB, s1>>>((const char*)buf[1], (100ull << 20) / TB, sink[0]);
+        CK(cudaEventRecord(ev[3], s1));
+      }
+      CK(cudaDeviceSynchronize());
+      float ms;
+      if (mode != 1 && mode != 3) { CK(cudaEventElapsedTime(&ms, ev[0], ev[1])); if (ms < bl) bl = ms; }
+      if (mode >= 1) { CK(cudaEventElapsedTime(&ms, ev[2], ev[3])); if (ms < bp) bp = ms; }
+    }
+    const char* nm[] = {"local alone", "peer ld alone", "local + peer ld", "peer st alone",
+                        "local + peer st", "local + bulk peer rd"};
+    printf("%-22s", nm[mode]);
+    if (mode != 1 && mode != 3) printf("  local %.1f us (%.0f GB/s)", bl * 1e3, 3.0 * lb / (bl * 1e6));
+    if (mode >= 1) printf("  peer %.1f us (%.0f GB/s)", bp * 1e3, (100ull << 20) / (bp * 1e6));
+    printf("\n");
+  }
+  return 0;
+}
+
 int main() {
   int n = 0;
   CK(cudaGetDeviceCount(&n));
@@ -139,5 +189,5 @@ int main() {
                bytes / (best[0] * 1e6), both ? "" : "\n");
         if (both) printf("  gpu1 %.1f GB/s\n", bytes / (best[1] * 1e6));
       }
-  return 0;
+  return interference(buf, sink);
 }
