@@ -160,7 +160,7 @@ def run_reference(args, world, rank):
     threaded = p > 1
     # bounded sample: at most 2 warm-up and 20 timed rounds (a 25M-param
     # fp64 round takes ~0.7 s on one core), so the arm ends within minutes
-    steps = max(1, min(args.steps, 20))
+    steps = max(1, min(args.steps, 20 if p == 1 else 10))
     cpu_reference(O.ALLREDUCE, p, d_sample, max(1, min(args.warmup, 2)), threaded)
     sec = cpu_reference(O.ALLREDUCE, p, d_sample, steps, threaded)
     per = sec / steps
