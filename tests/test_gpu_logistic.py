@@ -318,3 +318,31 @@ def test_logistic_trace_records_match_reference():
         assert rec.sq_err_opt is None and np.isnan(g[2])
         assert rec.sq_err_consensus == pytest.approx(g[3], rel=1e-8)
         assert rec.loss_mean == pytest.approx(g[4], rel=1e-9)
+
+
+def test_p_nodes_batch_b_match_one_node_batch_pb():
+    """test_protocols.cpp:221-247 through the value-semantic mirror: two
+    all-reduce nodes with batch 2 (rows from their own sample streams,
+    gradient on the device) track one node stepping with the mean of the
+    two shards' minibatch gradients (MeanOfStreamsObjective, 51-79) drawn
+    from copies of the same streams, within 1e-10; both nodes stay equal."""
+    X = np.array([[1.0, 0.0], [0.0, 1.0], [1.0, 1.0], [-1.0, 0.5], [0.5, -0.5], [2.0, 0.0]])
+    y = np.array([1, 0, 1, 0, 1, 0], dtype=np.int32)
+    data = P.LogisticObjective(X, y, 0.05)
+    noise = P.NoiseModel.zero(2)
+    h = Hyperparams(alpha0=0.1, anneal_at=(), mu=0.0, weight_decay=0.0, batch=2)
+    theta0 = np.array([0.3, -0.2])
+    nodes = [P.make_node(i, theta0, 9, "eq") for i in range(2)]
+    copies = [O.Stream.make(9, "eq", i, "sample") for i in range(2)]  # the merged objective's
+    single = O.Nodes(theta0[None].copy())
+    hs = O.HyperParams(alpha0=0.1, anneal_at=(), mu=0.0, weight_decay=0.0, batch=4)
+    for _ in range(20):
+        nodes = P.allreduce_round(nodes, data, noise, h)
+        th = single.theta[0]
+        acc = np.zeros(2)
+        for s in copies:
+            acc = acc + O.logistic_grad(X, y, 0.05, th, s.draw_rows(0, 6, 2))
+        acc = acc * (1.0 / 2)
+        O.local_sgd_step(single, hs, gfixed=acc[None])
+        assert np.abs(nodes[0].theta - single.theta[0]).max() <= 1e-10
+        assert nodes[0].theta.tobytes() == nodes[1].theta.tobytes()
