@@ -357,22 +357,40 @@ def main():
     e2e = None
     if True:
         host = [torch.randn(d, dtype=tdt).pin_memory() for _ in range(2)]
-        norm = ctypes.c_double(0.0)
         barrier()
         torch.cuda.synchronize()
         steps_e2e = max(3, min(args.steps, 20))
-        # warm
-        for s in range(2):
-            grp.upload_async(0, N.BUF_GRAD, host[s % 2].data_ptr(), d)
-            grp.allreduce_round(h, grad="buffer", grad_norm=True)
+        # a user's input pipeline: step s+1's gradient streams host -> device
+        # on a copy stream (double-buffered) while step s's round runs; the
+        # round reads it as its external gradient buffer and returns ||g||
+        # to the host (D2H + sync) every step
+        copy_stream = torch.cuda.Stream(device=f"cuda:{local}")
+        dbuf = [torch.empty(d, dtype=tdt, device=f"cuda:{local}") for _ in range(2)]
+        ready = [torch.cuda.Event() for _ in range(2)]
+
+        def upload(s):
+            with torch.cuda.stream(copy_stream):
+                # dbuf[s % 2] was last read by round s - 2, which has completed
+                # (every round syncs for its gradient norm)
+                dbuf[s % 2].copy_(host[s % 2], non_blocking=True)
+                ready[s % 2].record(copy_stream)
+
+        def e2e_steps(n):
+            upload(0)
+            for s in range(n):
+                if s + 1 < n:
+                    upload(s + 1)
+                stream.wait_event(ready[s % 2])
+                grp.allreduce_round(h, grad=[dbuf[s % 2].data_ptr()], grad_norm=True)
+
+        e2e_steps(2)  # warm
+        torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for s in range(steps_e2e):
-            grp.upload_async(0, N.BUF_GRAD, host[s % 2].data_ptr(), d)
-            gn = grp.allreduce_round(h, grad="buffer", grad_norm=True)  # D2H of ||g|| (syncs)
+        e0.record(copy_stream)
+        e2e_steps(steps_e2e)
         e1.record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
@@ -380,7 +398,8 @@ def main():
         e2e = {"value": world * d / (e_ms / steps_e2e * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": es * d * world, "d2h_bytes_per_step": 8 * world,
                "steps": steps_e2e, "ms_per_step": e_ms / steps_e2e,
-               "path": "dsgd_upload_async(pinned host gradient) + dsgd_allreduce_round(grad_norm_out)"}
+               "path": "pinned host gradient -> device (copy stream, double-buffered) + "
+                       "dsgd_allreduce_round(external gradient, grad_norm_out -> host)"}
 
     # ---------------- extras: gossip / EASGD shapes
     extras = {}
