@@ -1461,8 +1461,13 @@ dsgd_status dsgd_set_logistic(dsgd_ctx* c, const double* features, const int32_t
   c->lg_y = nullptr;
   DSGD_CUDA(cudaMalloc(&c->lg_X, n_samples * vb));
   DSGD_CUDA(cudaMalloc(&c->lg_y, n_samples * sizeof(int32_t)));
-  for (uint64_t r = 0; r < n_samples; ++r)
-    DSGD_TRY(upload_vec(c, c->lg_X + r * vb, features + r * c->d));
+  if (c->dtype == DSGD_F64) {
+    DSGD_CUDA(cudaMemcpy(c->lg_X, features, n_samples * vb, cudaMemcpyHostToDevice));
+  } else {  // the context dtype: round each feature to fp32 once, on the host
+    std::vector<float> f32(n_samples * c->d);
+    for (size_t k = 0; k < f32.size(); ++k) f32[k] = (float)features[k];
+    DSGD_CUDA(cudaMemcpy(c->lg_X, f32.data(), n_samples * vb, cudaMemcpyHostToDevice));
+  }
   DSGD_CUDA(cudaMemcpy(c->lg_y, labels, n_samples * sizeof(int32_t), cudaMemcpyHostToDevice));
   c->lg_n = n_samples;
   c->lg_l2 = l2;
