@@ -317,9 +317,19 @@ def main():
     t_nv = (nv_bytes * units / d / (nv_peak * 1e9)
             if (world > 1 and kname == "allreduce_comm") else 0.0)
     bound = "nvlink" if t_nv > t_hbm else "hbm"
+    traffic = None
+    if world == 1 and es == 4:  # DRAM bytes of the same kernel from the committed ncu capture
+        try:
+            with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                                   "r1_ncu_traffic.json")) as f:
+                t = json.load(f).get(f"k_local_tma<float>/d={d}")
+            if t:
+                traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
+        except (OSError, ValueError, KeyError):
+            traffic = None
     roofline = {"bound": bound, "kernel": kdesc, "achieved": achieved, "peak": peak,
                 "peak_source": peak_src, "unit": "GB/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": None,
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "algorithmic_bytes_per_launch": bpp * units,
                 "params_per_launch": units,
                 "kernel_avg_us": kavg_ms * 1e3,
