@@ -112,11 +112,13 @@ int interference(void* const* buf, uint4* const* sink) {
   cudaStream_t s0, s1; CK(cudaStreamCreate(&s0)); CK(cudaStreamCreate(&s1));
   cudaEvent_t ev[4]; for (auto& x : ev) CK(cudaEventCreate(&x));
   const uint64_t nl = lb / 16, np = (100ull << 20) / 16;
-  for (int mode = 0; mode < 6; ++mode) {  // 0 local, 1 peer ld, 2 both, 3 peer st, 4 local+st, 5 local+bulk rd
+  void* cebuf;
+  CK(cudaMalloc(&cebuf, 100ull << 20));
+  for (int mode = 0; mode < 8; ++mode) {  // 0 local, 1 peer ld, 2 both, 3 peer st, 4 local+st, 5 local+bulk rd, 6 CE peer copy, 7 local + CE
     float bl = 1e9f, bp = 1e9f;
     for (int rep = 0; rep < 5; ++rep) {
       CK(cudaDeviceSynchronize());
-      if (mode != 1 && mode != 3) {
+      if (mode != 1 && mode != 3 && mode != 6) {
         CK(cudaEventRecord(ev[0], s0));
         k_local<<<148 * 4, 512, 0, s0>>>((const uint4*)a, (const uint4*)b, (uint4*)c, nl);
         CK(cudaEventRecord(ev[1], s0));
@@ -125,18 +127,20 @@ int interference(void* const* buf, uint4* const* sink) {
         CK(cudaEventRecord(ev[2], s1));
         if (mode == 1 || mode == 2) k_read<<<148 * 2, 512, 0, s1>>>((const uint4*)buf[1], np, sink[0]);
         if (mode == 3 || mode == 4) k_write<<<148 * 2, 512, 0, s1>>>((uint4*)buf[1], np);
+        if (mode >= 6) CK(cudaMemcpyAsync(cebuf, buf[1], 100ull << 20, cudaMemcpyDefault, s1));
         if (mode == 5) k_tma_read<<<148, 512, 128 + STAGES * TB, s1>>>((const char*)buf[1], (100ull << 20) / TB, sink[0]);
         CK(cudaEventRecord(ev[3], s1));
       }
       CK(cudaDeviceSynchronize());
       float ms;
-      if (mode != 1 && mode != 3) { CK(cudaEventElapsedTime(&ms, ev[0], ev[1])); if (ms < bl) bl = ms; }
+      if (mode != 1 && mode != 3 && mode != 6) { CK(cudaEventElapsedTime(&ms, ev[0], ev[1])); if (ms < bl) bl = ms; }
       if (mode >= 1) { CK(cudaEventElapsedTime(&ms, ev[2], ev[3])); if (ms < bp) bp = ms; }
     }
     const char* nm[] = {"local alone", "peer ld alone", "local + peer ld", "peer st alone",
-                        "local + peer st", "local + bulk peer rd"};
+                        "local + peer st", "local + bulk peer rd", "CE peer copy alone",
+                        "local + CE peer copy"};
     printf("%-22s", nm[mode]);
-    if (mode != 1 && mode != 3) printf("  local %.1f us (%.0f GB/s)", bl * 1e3, 3.0 * lb / (bl * 1e6));
+    if (mode != 1 && mode != 3 && mode != 6) printf("  local %.1f us (%.0f GB/s)", bl * 1e3, 3.0 * lb / (bl * 1e6));
     if (mode >= 1) printf("  peer %.1f us (%.0f GB/s)", bp * 1e3, (100ull << 20) / (bp * 1e6));
     printf("\n");
   }
@@ -189,5 +193,49 @@ int main() {
                bytes / (best[0] * 1e6), both ? "" : "\n");
         if (both) printf("  gpu1 %.1f GB/s\n", bytes / (best[1] * 1e6));
       }
-  return interference(buf, sink);
+  if (interference(buf, sink)) return 1;
+  // both GPUs at once: each streams its own HBM and pulls 100 MB from the
+  // other with a copy engine (the shape of a CE-exchange all-reduce round)
+  {
+    const uint64_t lb = 400ull << 20;
+    void *a[2], *b[2], *c[2], *ce[2];
+    cudaStream_t sl[2], sc[2];
+    cudaEvent_t ev[2][4];
+    for (int g = 0; g < 2; ++g) {
+      CK(cudaSetDevice(g));
+      CK(cudaMalloc(&a[g], lb)); CK(cudaMalloc(&b[g], lb)); CK(cudaMalloc(&c[g], lb));
+      CK(cudaMalloc(&ce[g], 100ull << 20));
+      CK(cudaStreamCreate(&sl[g])); CK(cudaStreamCreate(&sc[g]));
+      for (auto& x : ev[g]) CK(cudaEventCreate(&x));
+    }
+    for (int with_local = 0; with_local < 2; ++with_local) {
+      float bl[2] = {1e9f, 1e9f}, bp[2] = {1e9f, 1e9f};
+      for (int rep = 0; rep < 5; ++rep) {
+        for (int g = 0; g < 2; ++g) { CK(cudaSetDevice(g)); CK(cudaDeviceSynchronize()); }
+        for (int g = 0; g < 2; ++g) {
+          CK(cudaSetDevice(g));
+          if (with_local) {
+            CK(cudaEventRecord(ev[g][0], sl[g]));
+            k_local<<<148 * 4, 512, 0, sl[g]>>>((const uint4*)a[g], (const uint4*)b[g], (uint4*)c[g], lb / 16);
+            CK(cudaEventRecord(ev[g][1], sl[g]));
+          }
+          CK(cudaEventRecord(ev[g][2], sc[g]));
+          CK(cudaMemcpyAsync(ce[g], buf[1 - g], 100ull << 20, cudaMemcpyDefault, sc[g]));
+          CK(cudaEventRecord(ev[g][3], sc[g]));
+        }
+        for (int g = 0; g < 2; ++g) {
+          CK(cudaSetDevice(g)); CK(cudaDeviceSynchronize());
+          float ms;
+          if (with_local) { CK(cudaEventElapsedTime(&ms, ev[g][0], ev[g][1])); if (ms < bl[g]) bl[g] = ms; }
+          CK(cudaEventElapsedTime(&ms, ev[g][2], ev[g][3])); if (ms < bp[g]) bp[g] = ms;
+        }
+      }
+      for (int g = 0; g < 2; ++g) {
+        printf("bidirectional CE%s gpu%d:", with_local ? " + local" : "", g);
+        if (with_local) printf("  local %.1f us (%.0f GB/s)", bl[g] * 1e3, 3.0 * lb / (bl[g] * 1e6));
+        printf("  CE %.1f us (%.0f GB/s)\n", bp[g] * 1e3, (100ull << 20) / (bp[g] * 1e6));
+      }
+    }
+  }
+  return 0;
 }
