@@ -240,8 +240,12 @@ dsgd_status dsgd_local_sgd_step(dsgd_ctx* ctx, const dsgd_hyperparams* h,
                                 const dsgd_grad_spec* g);
 /* allreduce_round protocols.cpp:110-131 (one context: pivot-form
  * spatial_mean, bit-exact with param_vec.cpp:19-40; one context per GPU:
- * ncclAllReduce over NVLink between a fused delta kernel and a fused apply
- * kernel, replacing ring_allreduce transport.cpp:183-248). */
+ * the mean over NVLink replacing ring_allreduce transport.cpp:183-248 --
+ * a one-shot peer-memory kernel (p <= 2, reference ring order, bit-exact),
+ * an NVSwitch multimem two-shot (p > 2), a two-shot over peer memory (ring
+ * order, bit-exact) or ncclAllReduce (DSGD_ALLREDUCE); theta += avg is
+ * deferred into the next round's delta kernel and materialised by any other
+ * call). */
 dsgd_status dsgd_allreduce_round(dsgd_ctx* ctx, const dsgd_hyperparams* h,
                                  const dsgd_grad_spec* g, dsgd_momentum_scope scope);
 /* Synchronous EASGD sweep simulator.cpp:332-351 = ea_client_step
