@@ -32,6 +32,9 @@ def main():
     if len(sys.argv) > 2 and sys.argv[2] == "logistic":
         logistic(rank, world, local, dtype, dist)
         return
+    if len(sys.argv) > 2 and sys.argv[2] == "timeout":
+        timeout_case(rank, world, local, dtype, dist)
+        return
     for proto, oid in names.items():
         d = 1031
         hk = dict(alpha0=0.05, anneal_at=(20,), mu=0.9, weight_decay=1e-4, beta_gossip=0.4,
@@ -109,6 +112,49 @@ def main():
         g.close()
     if rank == 0:
         print("RESULT " + json.dumps(results), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def timeout_case(rank, world, local, dtype, dist):
+    """A peer that never arrives: rank 0 keeps stepping, the others stop
+    after construction.  Rank 0's second pull round (RAW wait on its partner's
+    round counter) and its second all-reduce round must end with
+    TransportError after the configured timeout, not hang the GPU
+    (transport.cpp:123-133, test_transport.cpp:148-155)."""
+    import time
+
+    import numpy as np
+
+    from paper_1611_04581_b200 import _native as N
+    from paper_1611_04581_b200.engine import Group, Hyperparams
+    h = Hyperparams(alpha0=0.1, anneal_at=(), mu=0.9, weight_decay=0.0)
+    res = {}
+    for proto in ("pull-gossip", "all-reduce"):
+        g = Group.distributed(4096, rank, world, local, dtype=dtype, quadratic=True,
+                              allreduce=proto == "all-reduce")
+        g.set_timeout(0.5)
+        g.set_quadratic(np.ones(4096))
+        g.set_state(0, np.full(4096, float(rank)))
+        dist.barrier()
+        if rank == 0:
+            t0 = time.time()
+            err = None
+            try:
+                for _ in range(2):
+                    if proto == "pull-gossip":
+                        g.pull_gossip_round(h, [1] + [0] * (world - 1), grad="quadratic")
+                    else:
+                        g.allreduce_round(h, grad="quadratic")
+                g.sync()
+            except N.TransportError as e:
+                err = str(e)
+            res[proto] = {"timed_out": err is not None, "seconds": time.time() - t0,
+                          "message": err}
+        dist.barrier()
+        g.close()
+    if rank == 0:
+        print("RESULT " + json.dumps(res), flush=True)
     dist.barrier()
     dist.destroy_process_group()
 

@@ -85,3 +85,21 @@ def test_multi_gpu_logistic_matches_single_context(world, dtype):
             assert r["bit_exact"], (proto, r)
         if "center_exact" in r:
             assert r["center_exact"], (proto, r)
+
+
+@pytest.mark.skipif("n_gpus() < 2")
+def test_multi_gpu_missing_peer_times_out():
+    """A peer that never runs its round: the waiting kernel gives up after
+    the context timeout (%globaltimer-bounded flag waits) and the call
+    surfaces TransportError -- for the gossip RAW wait and the all-reduce."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29731",
+           os.path.join(ROOT, "tests", "mgpu_worker.py"), "f32", "timeout"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    line = [l for l in out.stdout.splitlines() if l.startswith("RESULT ")][0]
+    res = json.loads(line[7:])
+    for proto in ("pull-gossip", "all-reduce"):
+        assert res[proto]["timed_out"], res
+        assert "timed out" in res[proto]["message"]
+        assert res[proto]["seconds"] < 20.0, res
