@@ -316,6 +316,17 @@ typedef struct {
 dsgd_status dsgd_ctx_seed_streams(dsgd_ctx* ctx, uint64_t seed, const char* run_id);
 dsgd_status dsgd_run_rounds(dsgd_ctx* ctx, const dsgd_run_desc* run);
 dsgd_status dsgd_ctx_round(dsgd_ctx* ctx, uint64_t* round); /* rounds completed */
+/* run_async simulator.cpp:380-449 on one context (all p nodes): `events`
+ * ticks of the Poisson master clock (the run-level clock stream of
+ * dsgd_ctx_seed_streams: gap ~ Exp(p * rate_per_node), then the ticking
+ * node), each one async_pull_event (run->protocol DSGD_ASYNC_PULL; partner
+ * from the node's partner stream) or one EASGD client tick (DSGD_ELASTIC_AVG;
+ * ea_client_step + ea_server_apply when gated on the node's own t, else a
+ * local step).  The clock persists across calls; *sim_time accumulates the
+ * gaps and *alpha receives the step size of the last event (the trace
+ * record's alpha, simulator.cpp:411). */
+dsgd_status dsgd_run_events(dsgd_ctx* ctx, const dsgd_run_desc* run, uint64_t events,
+                            double rate_per_node, double* sim_time, double* alpha);
 
 /* ---------------------------------------------- multi-GPU group wiring
  * One context per GPU (n_local == 1).  Each context exports a fixed-size

@@ -130,6 +130,8 @@ _SIGS = {
     "dsgd_trace": (C.c_int, [_P, _DP, _DP, _DP]),
     "dsgd_ctx_seed_streams": (C.c_int, [_P, C.c_uint64, C.c_char_p]),
     "dsgd_run_rounds": (C.c_int, [_P, C.POINTER(RunDesc)]),
+    "dsgd_run_events": (C.c_int, [_P, C.POINTER(RunDesc), C.c_uint64, C.c_double,
+                                  C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "dsgd_ctx_round": (C.c_int, [_P, _U64P]),
     "dsgd_ctx_export_handle": (C.c_int, [_P, _P]),
     "dsgd_ctx_connect_peers": (C.c_int, [_P, _P]),

@@ -215,6 +215,7 @@ struct dsgd_ctx {
   std::vector<dsgd_stream*> partner_streams;  // all p (every context draws the full map)
   std::vector<dsgd_stream*> noise_streams;    // local nodes
   std::vector<dsgd_stream*> sample_streams;   // local nodes (logistic minibatch rows)
+  dsgd_stream* clock_stream = nullptr;        // run-level Poisson clock (async drivers)
   double* noise_host = nullptr;               // d doubles
 
   // measurement
@@ -1342,6 +1343,7 @@ void dsgd_ctx_destroy(dsgd_ctx* c) {
   for (auto* s : c->partner_streams) dsgd_stream_destroy(s);
   for (auto* s : c->noise_streams) dsgd_stream_destroy(s);
   for (auto* s : c->sample_streams) dsgd_stream_destroy(s);
+  if (c->clock_stream) dsgd_stream_destroy(c->clock_stream);
   delete[] c->noise_host;
   cudaFree(c->lg_X);
   cudaFree(c->lg_y);
@@ -1964,6 +1966,10 @@ dsgd_status dsgd_ctx_seed_streams(dsgd_ctx* c, uint64_t seed, const char* run_id
   c->noise_streams.assign(c->n_local, nullptr);
   for (auto* s : c->sample_streams) dsgd_stream_destroy(s);
   c->sample_streams.assign(c->n_local, nullptr);
+  if (c->clock_stream) dsgd_stream_destroy(c->clock_stream);
+  c->clock_stream = nullptr;
+  // run-level stream: node id kRunLevelNode = 0xFFFFFFFF (simulator.cpp:398)
+  DSGD_TRY(dsgd_stream_make(seed, run_id, 0xFFFFFFFFu, DSGD_PURPOSE_CLOCK, &c->clock_stream));
   for (uint32_t i = 0; i < c->n_local; ++i)
     DSGD_TRY(dsgd_stream_make(seed, run_id, c->first + i, DSGD_PURPOSE_SAMPLE,
                               &c->sample_streams[i]));
@@ -1972,6 +1978,56 @@ dsgd_status dsgd_ctx_seed_streams(dsgd_ctx* c, uint64_t seed, const char* run_id
   for (uint32_t i = 0; i < c->n_local; ++i)
     DSGD_TRY(dsgd_stream_make(seed, run_id, c->first + i, DSGD_PURPOSE_NOISE,
                               &c->noise_streams[i]));
+  return DSGD_OK;
+}
+
+dsgd_status dsgd_run_events(dsgd_ctx* c, const dsgd_run_desc* run, uint64_t events,
+                            double rate_per_node, double* sim_time, double* alpha) {
+  DSGD_TRY(check_ctx(c));
+  if (!run) return set_error(DSGD_EINVAL, "null run descriptor");
+  const dsgd_protocol proto = run->protocol;
+  if (proto != DSGD_ASYNC_PULL && proto != DSGD_ELASTIC_AVG)
+    return set_error(DSGD_EINVAL, "asynchronous driver supports async-pull and elastic-avg");
+  if (c->distributed()) return set_error(DSGD_EINVAL, "the asynchronous driver runs on one context");
+  if (!c->clock_stream || c->partner_streams.size() != c->p ||
+      c->noise_streams.size() != c->n_local)
+    return set_error(DSGD_ESTATE, "dsgd_ctx_seed_streams first");
+  if (!(rate_per_node > 0.0)) return set_error(DSGD_EINVAL, "poisson rate must be positive");
+  if (run->host_noise_sigma > 0.0) {
+    if (!c->noise[0]) return set_error(DSGD_ESTATE, "host noise needs DSGD_CTX_NOISE");
+    if (!c->noise_host) c->noise_host = new double[c->d];
+  }
+  const dsgd_hyperparams* h = &run->hyper;
+  double now = sim_time ? *sim_time : 0.0;
+  double last_alpha = alpha ? *alpha : 0.0;
+  for (uint64_t k = 0; k < events; ++k) {
+    // sample_next_event simulator.cpp:128-140: gap, then the ticking node
+    double gap = 0.0;
+    DSGD_TRY(dsgd_stream_exponential(c->clock_stream, (double)c->p * rate_per_node, &gap));
+    uint32_t i = 0;
+    DSGD_TRY(dsgd_stream_uniform_index(c->clock_stream, c->p, &i));
+    now += gap;
+    last_alpha = dsgd_step_size_at(h, c->t[i]);
+    dsgd_grad_spec g = run->grad;
+    uint32_t j = 0;
+    if (proto == DSGD_ASYNC_PULL)  // partner from the ticking node's stream (416-417)
+      DSGD_TRY(dsgd_stream_uniform_index(c->partner_streams[i], c->p, &j));
+    if (run->host_noise_sigma > 0.0) {  // NoiseModel::sample on node i's noise stream
+      dsgd_stream_fill_normal(c->noise_streams[i], run->host_noise_sigma, c->noise_host, c->d);
+      DSGD_TRY(dsgd_set_vector(c, i, DSGD_BUF_NOISE, c->noise_host));
+      g.use_noise = 1;
+    }
+    dsgd_status st;
+    if (proto == DSGD_ASYNC_PULL) {
+      st = dsgd_async_pull_event(c, h, &g, i, j);
+    } else {
+      const uint64_t ti = c->t[i];
+      st = dsgd_ea_client_event(c, h, &g, i, (ti > 0 && ti % h->tau == 0) ? 1 : 0);
+    }
+    if (st != DSGD_OK) return st;
+  }
+  if (sim_time) *sim_time = now;
+  if (alpha) *alpha = last_alpha;
   return DSGD_OK;
 }
 

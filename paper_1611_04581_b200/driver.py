@@ -183,6 +183,24 @@ def _record(g: Group, cfg: SimConfig, obj, t: int, sim_time: float, alpha: float
                        m["sq_err_consensus"], m["loss_mean"], alpha)
 
 
+def _run_events(g: Group, cfg: SimConfig, obj, protocol: int, use_noise: bool):
+    """The run_async event loop in the library (dsgd_run_events: clock,
+    partner and noise streams, one fused event kernel per tick), cut at the
+    trace points (simulator.cpp:431-434)."""
+    g.seed_streams(cfg.seed, cfg.run_id)
+    sigma = cfg.noise.sigma if use_noise else 0.0
+    trace = [_record(g, cfg, obj, 0, 0.0, step_size_at(cfg.hyper, 0))]
+    done, sim_time, alpha = 0, 0.0, 0.0
+    while done < cfg.events:
+        k = min(cfg.trace_every - done % cfg.trace_every, cfg.events - done)
+        sim_time, alpha = g.run_events(protocol, cfg.hyper, k, cfg.rate_per_node,
+                                       grad=_grad_kind(obj), host_noise_sigma=sigma,
+                                       sim_time=sim_time, alpha=alpha)
+        done += k
+        trace.append(_record(g, cfg, obj, done, sim_time, alpha))
+    return trace, sim_time
+
+
 def _round_time(cfg: SimConfig, gated: bool) -> float:
     """Virtual time of one synchronous round under the constant straggler
     model (simulator.cpp:240-349): every node takes `constant`, gated gossip
@@ -263,23 +281,7 @@ def run_async_elastic(cfg: SimConfig, obj: QuadraticObjective, dtype: str = "f64
         for i in range(cfg.p):
             g.set_state(i, thetas[i])
         g.ea_init_center()
-        clock = Stream.make(cfg.seed, cfg.run_id, 0xFFFFFFFF, "clock")
-        noise = [Stream.make(cfg.seed, cfg.run_id, i, "gradient-noise") for i in range(cfg.p)]
-        t = [0] * cfg.p
-        tau = cfg.hyper.tau
-        trace = [_record(g, cfg, obj, 0, 0.0, step_size_at(cfg.hyper, 0))]
-        sim_time = 0.0
-        for k in range(cfg.events):
-            sim_time += clock.exponential(cfg.p * cfg.rate_per_node)
-            i = clock.uniform_index(cfg.p)
-            alpha = step_size_at(cfg.hyper, t[i])
-            if use_noise:
-                g.set_vector(i, N.BUF_NOISE, noise[i].fill_normal(cfg.noise.sigma, d))
-            gated = t[i] > 0 and t[i] % tau == 0
-            g.ea_client_event(cfg.hyper, i, gated, grad=_grad_kind(obj), noise=use_noise)
-            t[i] += 1
-            if (k + 1) % cfg.trace_every == 0 or k + 1 == cfg.events:
-                trace.append(_record(g, cfg, obj, k + 1, sim_time, alpha))
+        trace, sim_time = _run_events(g, cfg, obj, N.ELASTIC_AVG, use_noise)
         th = np.zeros((cfg.p, d))
         dp = np.zeros((cfg.p, d))
         tt = np.zeros(cfg.p, dtype=np.uint64)
@@ -306,23 +308,7 @@ def run_async_pull(cfg: SimConfig, obj: QuadraticObjective, dtype: str = "f64",
     try:
         for i in range(cfg.p):
             g.set_state(i, thetas[i])
-        clock = Stream.make(cfg.seed, cfg.run_id, 0xFFFFFFFF, "clock")
-        partner = [Stream.make(cfg.seed, cfg.run_id, i, "partner-choice") for i in range(cfg.p)]
-        noise = [Stream.make(cfg.seed, cfg.run_id, i, "gradient-noise") for i in range(cfg.p)]
-        tn = [0] * cfg.p
-        trace = [_record(g, cfg, obj, 0, 0.0, step_size_at(cfg.hyper, 0))]
-        sim_time = 0.0
-        for k in range(cfg.events):
-            sim_time += clock.exponential(cfg.p * cfg.rate_per_node)
-            i = clock.uniform_index(cfg.p)
-            alpha = step_size_at(cfg.hyper, tn[i])
-            j = partner[i].uniform_index(cfg.p)
-            if use_noise:
-                g.set_vector(i, N.BUF_NOISE, noise[i].fill_normal(cfg.noise.sigma, d))
-            g.async_pull_event(cfg.hyper, i, j, grad=_grad_kind(obj), noise=use_noise)
-            tn[i] += 1
-            if (k + 1) % cfg.trace_every == 0 or k + 1 == cfg.events:
-                trace.append(_record(g, cfg, obj, k + 1, sim_time, alpha))
+        trace, sim_time = _run_events(g, cfg, obj, N.ASYNC_PULL, use_noise)
         th = np.zeros((cfg.p, d))
         dp = np.zeros((cfg.p, d))
         t = np.zeros(cfg.p, dtype=np.uint64)

@@ -391,6 +391,19 @@ class Group:
         rd._keep = (gs, pool)
         N.check(self.lib.dsgd_run_rounds(self._ctx, C.byref(rd)))
 
+    def run_events(self, protocol: int, h: Hyperparams, events: int, rate_per_node: float,
+                   grad=None, host_noise_sigma: float = 0.0, sim_time: float = 0.0,
+                   alpha: float = 0.0):
+        """run_async's event loop (simulator.cpp:380-449) on this context:
+        returns (accumulated sim_time, alpha of the last event)."""
+        gs = self._grad(grad, False, False)
+        rd = N.RunDesc(protocol, h.to_c(), N.SCOPE_AGGREGATE, gs, 0, None, host_noise_sigma, 0)
+        rd._keep = gs
+        st, al = C.c_double(sim_time), C.c_double(alpha)
+        N.check(self.lib.dsgd_run_events(self._ctx, C.byref(rd), events, rate_per_node,
+                                         C.byref(st), C.byref(al)))
+        return st.value, al.value
+
     def rounds_done(self) -> int:
         r = C.c_uint64()
         N.check(self.lib.dsgd_ctx_round(self._ctx, C.byref(r)))
