@@ -906,10 +906,9 @@ __global__ void __launch_bounds__(kBlock) k_ar_oneshot_tma(const __grid_constant
 
 // One-shot round with EVERY stream staged through shared memory (every
 // rank's exchange tile + this rank's theta, delta, gradient / s+opt, noise):
-// 3 stages of up to P + 5 8-KB tiles per CTA, registers hold no loads.
-constexpr int kOs2Stages = 3;
-
-template <typename T, int P>
+// S stages of up to P + 5 8-KB tiles per CTA, registers hold no loads.
+// kOs2Stages stages (DSGD_OS_STAGES, default 2).
+template <typename T, int P, int kOs2Stages>
 __global__ void __launch_bounds__(kBlock) k_ar_oneshot_tma2(const __grid_constant__ ArOneShotArgs<T> a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr uint64_t TILE = os_tile<T>();
@@ -1013,6 +1012,31 @@ __global__ void __launch_bounds__(kBlock) k_ar_oneshot_tma2(const __grid_constan
   block_signal(a.signal);
 }
 
+template <typename T, int P, int S>
+cudaError_t launch_os2(const ArOneShotArgs<T>& a, int max_ctas, cudaStream_t s) {
+  const int nsl = P + 1 + (a.agg ? 0 : 1) + (a.quad ? 2 : 1) + (a.node.noise ? 1 : 0);
+  const size_t smem = 128 + (size_t)S * nsl * os_tile<T>() * sizeof(T);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  static size_t attr = 0;
+  if (attr < smem) {
+    cudaFuncSetAttribute(k_ar_oneshot_tma2<T, P, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = smem;
+  }
+  int resident = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_ar_oneshot_tma2<T, P, S>, kBlock, smem);
+  if (resident < 1) resident = 1;
+  if (max_ctas > 0 && resident > max_ctas) resident = max_ctas;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t tiles = a.d / os_tile<T>();
+  uint32_t g = (uint32_t)sms * (uint32_t)resident;
+  if (tiles < g) g = (uint32_t)(tiles ? tiles : 1);
+  k_ar_oneshot_tma2<T, P, S><<<g, kBlock, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
 template <typename T, int P>
 cudaError_t launch_ar_oneshot_p(const ArOneShotArgs<T>& a, int vec, uint32_t grid, cudaStream_t s) {
   static const bool all_staged = [] {  // DSGD_OS_STAGE_ALL=0: stage only the exchange tiles
@@ -1020,25 +1044,24 @@ cudaError_t launch_ar_oneshot_p(const ArOneShotArgs<T>& a, int vec, uint32_t gri
     return !(e && e[0] == '0');
   }();
   if (vec && a.pending && !a.apply_only && a.tma_rank >= 0 && all_staged) {
-    const int nsl = P + 1 + (a.agg ? 0 : 1) + (a.quad ? 2 : 1) + (a.node.noise ? 1 : 0);
-    const size_t smem = 128 + (size_t)kOs2Stages * nsl * os_tile<T>() * sizeof(T);
-    static size_t attr = 0;
-    if (attr < smem) {
-      cudaFuncSetAttribute(k_ar_oneshot_tma2<T, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
-      attr = smem;
+    static const int stages = [] {
+      // 2 stages at 3 CTAs/SM measured best at p = 2, d = 25M (182.5 vs
+      // 192-203 us/round for 3 stages at 2 CTAs/SM, profiles/r1_os_stages_n2.md)
+      const char* e = getenv("DSGD_OS_STAGES");
+      const int v = e ? atoi(e) : 2;
+      return v < 2 ? 2 : (v > 6 ? 6 : v);
+    }();
+    static const int max_ctas = [] {  // DSGD_OS_CTAS: cap on CTAs per SM (0: occupancy)
+      const char* e = getenv("DSGD_OS_CTAS");
+      return e ? atoi(e) : 0;
+    }();
+    switch (stages) {
+      case 2: return launch_os2<T, P, 2>(a, max_ctas, s);
+      case 4: return launch_os2<T, P, 4>(a, max_ctas, s);
+      case 5: return launch_os2<T, P, 5>(a, max_ctas, s);
+      case 6: return launch_os2<T, P, 6>(a, max_ctas, s);
+      default: return launch_os2<T, P, 3>(a, max_ctas, s);
     }
-    int resident = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_ar_oneshot_tma2<T, P>, kBlock, smem);
-    if (resident < 1) resident = 1;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const uint64_t tiles = a.d / os_tile<T>();
-    uint32_t g = (uint32_t)sms * (uint32_t)resident;
-    if (tiles < g) g = (uint32_t)(tiles ? tiles : 1);
-    k_ar_oneshot_tma2<T, P><<<g, kBlock, smem, s>>>(a);
-    return cudaGetLastError();
   }
   if (vec && a.pending && !a.apply_only && a.tma_rank >= 0) {
     const size_t smem = 128 + (size_t)kOsStages * P * os_tile<T>() * sizeof(T);
