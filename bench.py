@@ -504,6 +504,41 @@ def run_extras(args, local, h):
             torch.cuda.empty_cache()
         except Exception as e:  # pragma: no cover
             out[name] = {"error": str(e)}
+    # F4: the asynchronous event loop in the library (dsgd_run_events): one
+    # async_pull_event kernel per Poisson tick, 8 nodes x 10M on one GPU
+    name = "async-pull p=8 x 10M (1 GPU, events)"
+    try:
+        from paper_1611_04581_b200.engine import Hyperparams
+        p, d = 8, 10_000_000
+        grp = Group(d, p, dtype="f32", device=local, grad=True)
+        gen = torch.Generator(device=f"cuda:{local}")
+        gen.manual_seed(9)
+        for i in range(p):
+            t = torch.randn(d, generator=gen, device=f"cuda:{local}")
+            grp.copy_in_async(i, N.BUF_THETA, t.data_ptr(), d)
+            grp.copy_in_async(i, N.BUF_GRAD, t.data_ptr(), d)
+            grp.sync()
+        grp.seed_streams(2, "c4/trial0")
+        ha = Hyperparams(alpha0=0.05, anneal_at=(), mu=0.0, weight_decay=1e-4, beta_gossip=0.5)
+        grp.run_events(N.ASYNC_PULL, ha, 10, 1.0, grad="buffer")
+        grp.sync()
+        stream = torch.cuda.ExternalStream(grp.stream(), device=f"cuda:{local}")
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        k = 200
+        e0.record(stream)
+        grp.run_events(N.ASYNC_PULL, ha, k, 1.0, grad="buffer")
+        e1.record(stream)
+        grp.sync()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / k
+        out[name] = {"ms_per_event": ms, "events_per_s": 1e3 / ms,
+                     "param_updates_per_s": d / (ms * 1e-3),
+                     "hbm_gbs": 16 * d / (ms * 1e-3) / 1e9, "bytes_per_param": 16}
+        grp.close()
+        torch.cuda.empty_cache()
+    except Exception as e:  # pragma: no cover
+        out[name] = {"error": str(e)}
     return out
 
 
