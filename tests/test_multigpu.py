@@ -103,3 +103,23 @@ def test_multi_gpu_missing_peer_times_out():
         assert res[proto]["timed_out"], res
         assert "timed out" in res[proto]["message"]
         assert res[proto]["seconds"] < 20.0, res
+
+
+@pytest.mark.skipif("n_gpus() < 3")
+def test_multi_gpu_three_ranks_match_oracle():
+    """p = 3 (uneven reference ring chunks, odd slice split): every protocol
+    with the default backends against the oracle, fp64."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=3",
+           "--master-addr", "127.0.0.1", "--master-port", "29741",
+           os.path.join(ROOT, "tests", "mgpu_worker.py"), "f64"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    line = [l for l in out.stdout.splitlines() if l.startswith("RESULT ")][0]
+    res = json.loads(line[7:])
+    for proto, r in res.items():
+        if proto.startswith("all-reduce") and r["nvls"]:
+            assert r["max_rel"] <= 1e-12, (proto, r)
+        else:
+            assert r["bit_exact"], (proto, r)
+        if r["center_exact"] is not None:
+            assert r["center_exact"], (proto, r)
