@@ -405,8 +405,9 @@ __global__ void __launch_bounds__(kBlock) k_step_tma2(const __grid_constant__ St
   src[q++] = n.partner;   // slot 0: the peer snapshot (NVLink)
   src[q++] = n.theta_in;  // slot 1
   const bool mix_only = MODE == kModeMix;
+  const bool uses_dp = !mix_only && MODE != kModeAsync;  // async: no momentum term
   const int s_dp = q;
-  if (!mix_only) src[q++] = n.delta;
+  if (uses_dp) src[q++] = n.delta;
   const int s_g = q;
   if (!mix_only) {
     if (a.quad) {
@@ -454,7 +455,7 @@ __global__ void __launch_bounds__(kBlock) k_step_tma2(const __grid_constant__ St
       rd(0, in[u].xj);
       rd(1, in[u].x);
       if (!mix_only) {
-        rd(s_dp, in[u].dp);
+        if (uses_dp) rd(s_dp, in[u].dp);
         if (a.quad) {
           rd(s_g, in[u].s);
           rd(s_g + 1, in[u].o);
@@ -542,6 +543,29 @@ cudaError_t launch_step_tma(const StepArgs<T>& a, cudaStream_t s) {
 
 template <typename T>
 cudaError_t launch_step(int mode, const StepArgs<T>& a, int vec, uint32_t grid, cudaStream_t s) {
+  // one async event (single context): every stream staged, in place on node i
+  if (mode == kModeAsync && a.tma_partner && vec && a.n_local == 1) {
+    const int nsl = 2 + (a.quad ? 2 : 1) + (a.node[0].noise ? 1 : 0);
+    const size_t smem = 128 + (size_t)3 * nsl * st_tile<T>() * sizeof(T);
+    static size_t attr = 0;
+    if (attr < smem) {
+      cudaFuncSetAttribute(k_step_tma2<T, kModeAsync>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      attr = smem;
+    }
+    int resident = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_step_tma2<T, kModeAsync>, kBlock,
+                                                  smem);
+    if (resident < 1) resident = 1;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t tiles = a.d / st_tile<T>();
+    uint32_t g = (uint32_t)sms * (uint32_t)resident;
+    if (tiles < g) g = (uint32_t)(tiles ? tiles : 1);
+    k_step_tma2<T, kModeAsync><<<g, kBlock, smem, s>>>(a);
+    return cudaGetLastError();
+  }
   // one node whose partner is a peer GPU: stage the NVLink stream in smem
   if (a.tma_partner && vec && a.n_local == 1 && a.blocks_per_node == grid) {
     if (mode == kModePull) return launch_step_tma<T, kModePull>(a, s);

@@ -1747,6 +1747,7 @@ dsgd_status dsgd_async_pull_event(dsgd_ctx* c, const dsgd_hyperparams* h,
     if (gs.noise) a.node[0].noise = as<T>(c->noise[i]);
     const uint64_t W = vec ? 16 / sizeof(T) : 1;
     a.blocks_per_node = blocks_for(c, (c->d / W + 1) / 2, 1);
+    a.tma_partner = c->ar_tma;  // every stream staged through smem (k_step_tma2<Async>)
     {
       LaunchScope ls(c, DSGD_K_STEP);
       DSGD_CUDA(dsgd::launch_step<T>(dsgd::kModeAsync, a, vec, a.blocks_per_node, c->stream));
