@@ -292,8 +292,9 @@ def main():
                  "through smem by cp.async.bulk), 12 B read + 8 B write per param")
     elif backend == "oneshot":
         kname, bpp = "allreduce_comm", (5 + (world - 1)) * es
-        kdesc = ("k_ar_oneshot_tma: one kernel per round; every rank's previous exchange tile staged "
-                 "in smem by cp.async.bulk (P-1 over NVLink), ring-order average fused with theta += "
+        kdesc = ("k_ar_oneshot_tma2: one kernel per round; every rank's previous exchange tile and "
+                 "this rank's theta/g staged in smem by cp.async.bulk (2 stages x 3 CTAs/SM; P-1 "
+                 "tiles over NVLink), ring-order average fused with theta += "
                  "avg and the next delta; HBM: theta, g, own x read + theta', x' write + x served "
                  f"to {world - 1} peer(s); NVLink {nv_bytes / d:.0f} B/param each direction")
     elif backend == "nvls":
