@@ -259,7 +259,9 @@ def main():
         load()
         barrier()
         torch.cuda.synchronize()
-        grp.profile(True)
+        # no per-launch events inside the timed region: an event between two
+        # back-to-back kernels costs ~5 us per step here (measured,
+        # tools/step_gap.py)
         k0, n0 = grp.launch_count()
         ev0.record(stream)
         rounds(args.steps)
@@ -267,7 +269,18 @@ def main():
         grp.sync()
         torch.cuda.synchronize()
         k1, n1 = grp.launch_count()
+        barrier()
+        # per-kernel breakdown: the same K rounds again with per-launch events
+        grp.profile(True)
+        pe0 = torch.cuda.Event(enable_timing=True)
+        pe1 = torch.cuda.Event(enable_timing=True)
+        pe0.record(stream)
+        rounds(args.steps)
+        pe1.record(stream)
+        grp.sync()
+        torch.cuda.synchronize()
         prof = {N.KERNEL_NAMES[k]: grp.profile_read(k, reset=True) for k in range(8)}
+        prof_ms = pe0.elapsed_time(pe1)
         barrier()
         grp.profile(False)
         load()
@@ -309,7 +322,18 @@ def main():
     else:
         kname, bpp = "ar_delta", 5 * es
         kdesc = "k_step<ApplyDelta>: read theta, avg, g; write theta', delta' (then ncclAllReduce)"
-    kms, kn = prof.get(kname, (0.0, 0))
+    kms_p, kn = prof.get(kname, (0.0, 0))
+    share = (kms_p / prof_ms) if prof_ms else None
+    single = kn == args.steps and (k1 - k0) == args.steps and (n1 - n0) == 0
+    if single:
+        # the step IS one launch of this kernel: its duration is the timed
+        # region / launches (CUDA events around the region on this stream;
+        # includes the ~1 us launch gap, so conservative)
+        kms = ms
+        timing = "timed region / launches (one launch of this kernel per step, no per-launch events)"
+    else:
+        kms = kms_p
+        timing = "per-launch CUDA events in a second pass of the same K rounds"
     kavg_ms = kms / max(1, kn)
     # parameters one launch processes: d, or d / K with K pipelines per round
     units = d * args.steps / kn if kn else d
@@ -336,11 +360,14 @@ def main():
                 "kernel_avg_us": kavg_ms * 1e3,
                 "roofline_time_us": max(t_hbm, t_nv) * 1e6,
                 "frac_of_roofline_time": (max(t_hbm, t_nv) / (kavg_ms * 1e-3)) if kn else None,
-                "share_of_step": (kms / ms) if ms else None}
+                "kernel_timing": timing,
+                "share_of_step": share}
     step_bytes = 5 * es * d if world == 1 else 7 * es * d
     if world > 1:
         nms, nn = prof.get("allreduce_comm", (0.0, 0))
         t_c = nms / max(1, nn) * 1e-3
+        if single and kname == "allreduce_comm":
+            t_c = kavg_ms * 1e-3  # the timed region's own per-launch time
         nv_launch = nv_bytes * (args.steps / nn if nn else 1.0)  # per launch (K pipelines)
         roofline["allreduce_backend"] = backend
         roofline["allreduce_launches_per_round"] = nn / args.steps if nn else None
