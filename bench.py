@@ -324,7 +324,9 @@ def main():
         kdesc = "k_step<ApplyDelta>: read theta, avg, g; write theta', delta' (then ncclAllReduce)"
     kms_p, kn = prof.get(kname, (0.0, 0))
     share = (kms_p / prof_ms) if prof_ms else None
-    single = kn == args.steps and (k1 - k0) == args.steps and (n1 - n0) == 0
+    # one launch of the dominant kernel per step (+ the run's final deferred
+    # apply, which run_rounds materialises once at the end at N > 1)
+    single = kn == args.steps and (k1 - k0) in (args.steps, args.steps + 1) and (n1 - n0) == 0
     if single:
         # the step IS one launch of this kernel: its duration is the timed
         # region / launches (CUDA events around the region on this stream;
