@@ -302,7 +302,8 @@ def main():
     if world == 1:
         kname, bpp = "allreduce_local", 5 * es  # read theta, delta, g; write theta', delta'
         kdesc = ("k_local_tma (p=1 round: fused delta + mean + apply; theta, delta, g staged "
-                 "through smem by cp.async.bulk), 12 B read + 8 B write per param")
+                 "through smem by cp.async.bulk; back-to-back rounds with programmatic dependent "
+                 "launch), 12 B read + 8 B write per param")
     elif backend == "oneshot":
         kname, bpp = "allreduce_comm", (5 + (world - 1)) * es
         kdesc = ("k_ar_oneshot_tma2: one kernel per round; every rank's previous exchange tile and "

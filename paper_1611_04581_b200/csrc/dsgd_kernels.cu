@@ -1205,6 +1205,11 @@ __global__ void __launch_bounds__(kBlock) k_local_tma(const __grid_constant__ Al
   }
   if (n.noise) src[ns++] = n.noise;
   const uint64_t nt = a.d / TILE;
+  // programmatic dependent launch: let the next round's grid be scheduled
+  // now, and wait here until the previous round's grid has finished and its
+  // writes are visible (theta / delta are read-after-write across rounds)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (threadIdx.x == 0) {
     for (int s = 0; s < kLtStages; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
@@ -1323,8 +1328,21 @@ cudaError_t launch_local_tma(const AllreduceArgs<T>& a, cudaStream_t s) {
   const uint64_t tiles = a.d / lt_tile<T>();
   uint32_t g = (uint32_t)sms * (uint32_t)resident;
   if (tiles < g) g = (uint32_t)(tiles ? tiles : 1);
-  k_local_tma<T><<<g, kBlock, smem, s>>>(a);
-  return cudaGetLastError();
+  static const bool pdl = [] {  // DSGD_PDL=0: plain stream-ordered launches
+    const char* e = getenv("DSGD_PDL");
+    return !(e && e[0] == '0');
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g);
+  cfg.blockDim = dim3(kBlock);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_local_tma<T>, a);
 }
 
 // Two-shot all-reduce delta kernel (kModeArDelta / kModeApplyDelta) of one
