@@ -256,16 +256,17 @@ struct LaunchScope {
   dsgd_ctx* c;
   int id;
   cudaStream_t st;
+  bool nccl;  // an NCCL call (counted apart from this library's kernels)
   cudaEvent_t a = nullptr;
-  LaunchScope(dsgd_ctx* ctx, int kid, cudaStream_t on = nullptr)
-      : c(ctx), id(kid), st(on ? on : ctx->stream) {
+  LaunchScope(dsgd_ctx* ctx, int kid, cudaStream_t on = nullptr, bool is_nccl = false)
+      : c(ctx), id(kid), st(on ? on : ctx->stream), nccl(is_nccl) {
     if (c->profile) {
       a = take_event(c);
       cudaEventRecord(a, st);
     }
   }
   ~LaunchScope() {
-    if (id == DSGD_K_NCCL)
+    if (nccl)
       c->nccl_calls++;
     else
       c->kernels++;
@@ -1013,7 +1014,7 @@ dsgd_status do_allreduce(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& 
   }
   if (fused) c->cur ^= 1;  // theta_{t} + avg_{t-1} now materialised in the other buffer
   {
-    LaunchScope ls(c, DSGD_K_NCCL);
+    LaunchScope ls(c, DSGD_K_NCCL, nullptr, true);
     DSGD_NCCL(ncclAllReduce(xbuf, xbuf, c->d, sizeof(T) == 4 ? ncclFloat : ncclDouble, ncclAvg,
                             c->comm, c->stream));
   }
@@ -1946,7 +1947,7 @@ dsgd_status dsgd_ea_init_center(dsgd_ctx* c) {
     // ranks' c_in are written by their chain predecessor only.)
     if (!c->aux[0]) DSGD_CUDA(cudaMalloc(&c->aux[0], c->d * c->es));
     {
-      LaunchScope ls(c, DSGD_K_NCCL);
+      LaunchScope ls(c, DSGD_K_NCCL, nullptr, true);
       DSGD_NCCL(ncclAllReduce(c->theta_ptr(0, c->cur), c->aux[0], c->d,
                               sizeof(T) == 4 ? ncclFloat : ncclDouble, ncclAvg, c->comm,
                               c->stream));
