@@ -692,7 +692,7 @@ __device__ __forceinline__ void nvls_scalar(const double* x, double* y, double d
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kBlock) k_ar_nvls(const __grid_constant__ ArNvlsArgs<T> a) {
+__global__ void __launch_bounds__(1024) k_ar_nvls(const __grid_constant__ ArNvlsArgs<T> a) {
   if (!block_wait(a.wait)) return;
   fence_proxy_alias();  // peers wrote x through their unicast mappings
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -717,7 +717,22 @@ __global__ void __launch_bounds__(kBlock) k_ar_nvls(const __grid_constant__ ArNv
 
 template <typename T>
 cudaError_t launch_ar_nvls(const ArNvlsArgs<T>& a, uint32_t grid, cudaStream_t s) {
-  k_ar_nvls<T><<<grid, kBlock, 0, s>>>(a);
+  // DSGD_AR_COMM_SMEM=<KB>: reserve (unused) shared memory per CTA so that a
+  // reduce CTA cannot share an SM with a (144 KB) delta CTA: SM-issued NVLink
+  // traffic starves when co-resident with an HBM stream, not when the two
+  // run on disjoint SMs (profiles/r1_nvlink_probe.txt, "split" rows)
+  static const int pad = [] {
+    const char* e = getenv("DSGD_AR_COMM_SMEM");
+    const int kb = e ? atoi(e) : 120;  // measured best at p = 4 (r1_tune_allreduce_n4/split/)
+    return kb < 0 ? 0 : (kb > 200 ? 200 : kb) * 1024;
+  }();
+  static bool attr = false;
+  if (pad && !attr) {
+    cudaFuncSetAttribute(k_ar_nvls<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad);
+    attr = true;
+  }
+  // one padded CTA per SM: 1024 threads keep enough switch reductions in flight
+  k_ar_nvls<T><<<grid, pad ? 1024 : kBlock, pad, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -2212,6 +2212,11 @@ dsgd_status dsgd_ctx_attach_multicast(dsgd_ctx* c, void* x, void* x_mc, void* av
   c->p2p_allreduce = true;
   c->ar_oneshot = false;
   c->ar_nvls = true;
+  // reduce CTAs on SMs of their own (1024 threads, padded smem) and a wider
+  // delta grid: 271.5 vs 328.7 us/round at p = 4, d = 25M
+  // (profiles/r1_tune_allreduce_n4/split/); the environment still overrides
+  if (!std::getenv("DSGD_AR_DELTA_FRAC")) c->ar_delta_frac = 1.5;
+  if (!std::getenv("DSGD_AR_COMM_FRAC")) c->ar_comm_frac = 0.5;
   return DSGD_OK;
 }
 

@@ -194,6 +194,52 @@ int main() {
         if (both) printf("  gpu1 %.1f GB/s\n", bytes / (best[1] * 1e6));
       }
   if (interference(buf, sink)) return 1;
+  // spatial split: local stream on L SMs, peer loads on the other 148 - L
+  // (one CTA per SM each, forced by a large dynamic smem reservation)
+  {
+    CK(cudaSetDevice(0));
+    const uint64_t lb = 400ull << 20;
+    void *a, *b, *c;
+    CK(cudaMalloc(&a, lb)); CK(cudaMalloc(&b, lb)); CK(cudaMalloc(&c, lb));
+    cudaStream_t s0, s1; CK(cudaStreamCreate(&s0)); CK(cudaStreamCreate(&s1));
+    cudaEvent_t ev[4]; for (auto& x : ev) CK(cudaEventCreate(&x));
+    const int big = 160 * 1024;
+    CK(cudaFuncSetAttribute(k_local, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(k_read, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    for (int L : {148, 120, 100, 74}) {
+      float bl = 1e9f, bp = 1e9f;
+      for (int rep = 0; rep < 5; ++rep) {
+        CK(cudaDeviceSynchronize());
+        CK(cudaEventRecord(ev[0], s0));
+        k_local<<<L, 1024, big, s0>>>((const uint4*)a, (const uint4*)b, (uint4*)c, lb / 16);
+        CK(cudaEventRecord(ev[1], s0));
+        if (L < 148) {
+          CK(cudaEventRecord(ev[2], s1));
+          k_read<<<148 - L, 1024, big, s1>>>((const uint4*)buf[1], (100ull << 20) / 16, sink[0]);
+          CK(cudaEventRecord(ev[3], s1));
+        }
+        CK(cudaDeviceSynchronize());
+        float ms;
+        CK(cudaEventElapsedTime(&ms, ev[0], ev[1])); if (ms < bl) bl = ms;
+        if (L < 148) { CK(cudaEventElapsedTime(&ms, ev[2], ev[3])); if (ms < bp) bp = ms; }
+      }
+      printf("split: local on %3d SMs %.1f us (%.0f GB/s)", L, bl * 1e3, 3.0 * lb / (bl * 1e6));
+      if (L < 148) printf("  peer ld on %3d SMs %.1f us (%.0f GB/s)", 148 - L, bp * 1e3, (100ull << 20) / (bp * 1e6));
+      printf("\n");
+    }
+    // peer loads alone on the small SM sets
+    for (int P : {28, 48, 74}) {
+      float bp = 1e9f;
+      for (int rep = 0; rep < 5; ++rep) {
+        CK(cudaEventRecord(ev[2], s1));
+        k_read<<<P, 1024, big, s1>>>((const uint4*)buf[1], (100ull << 20) / 16, sink[0]);
+        CK(cudaEventRecord(ev[3], s1));
+        CK(cudaDeviceSynchronize());
+        float ms; CK(cudaEventElapsedTime(&ms, ev[2], ev[3])); if (ms < bp) bp = ms;
+      }
+      printf("peer ld alone on %3d SMs: %.0f GB/s\n", P, (100ull << 20) / (bp * 1e6));
+    }
+  }
   // both GPUs at once: each streams its own HBM and pulls 100 MB from the
   // other with a copy engine (the shape of a CE-exchange all-reduce round)
   {
