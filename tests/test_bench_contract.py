@@ -28,3 +28,33 @@ def test_reference_arm_json_line():
         assert k in j, k
     assert j["value"] > 0 and j["cpu_baseline"]["kind"] == "reference"
     assert j["e2e"]["h2d_bytes_per_step"] == 0 and j["e2e"]["value"] == j["value"]
+
+
+@pytest.mark.gpu
+def test_bench_json_line_on_gpu():
+    """One N = 1 bench line carries every key of the driver contract and the
+    round-1 additions (roofline with traffic, e2e with copy bytes, clocks,
+    gpu_launches) with sane values."""
+    out = subprocess.run([sys.executable, "bench.py", "--steps", "5", "--warmup", "3",
+                          "--no-extras", "--no-cpu"], capture_output=True, text=True,
+                         cwd=ROOT, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    j = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "roofline", "e2e", "clocks", "gpu_launches"):
+        assert k in j, k
+    assert j["n_gpus"] == 1 and j["steps"] == 5 and j["warmup"] == 3
+    assert j["value"] > 1e10 and j["higher_is_better"] is True
+    assert "workload" in j["config"]
+    r = j["roofline"]
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in r, k
+    assert r["bound"] == "hbm" and 0.3 < r["frac"] <= 1.05
+    e = j["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] == 4 * 25_000_000
+    assert e["d2h_bytes_per_step"] > 0
+    assert j["gpu_launches"] >= 5
+    assert j["clocks"]["sm_mhz"] is not None
