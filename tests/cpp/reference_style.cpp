@@ -113,6 +113,33 @@ int main() {
       CHECK(approx(th[0], want[i]));
     }
   }
+  // LogisticObjective (test_objectives.cpp tiny_logistic): at theta = 0 every
+  // z = 0, sigmoid = 1/2, so the one-row minibatch gradient is (1/2 - y) x;
+  // a plain step theta -= alpha * g
+  {
+    Context ctx(2, 1, DSGD_F64, 0, 0);
+    ctx.set_logistic({{1.0, 0.0}, {0.0, 1.0}, {1.0, 1.0}, {-1.0, 0.5}}, {1, 0, 1, 0}, 0.1);
+    const double y[4] = {1, 0, 1, 0};
+    const double X[4][2] = {{1.0, 0.0}, {0.0, 1.0}, {1.0, 1.0}, {-1.0, 0.5}};
+    for (uint64_t r = 0; r < 4; ++r) {
+      ctx.set_state(0, {0.0, 0.0}, {0.0, 0.0}, 0);
+      Gradient g;
+      g.source = DSGD_GRAD_LOGISTIC;
+      g.rows = {r};
+      ctx.local_sgd_step(plain(0.5), g);
+      std::vector<double> th(2);
+      ctx.get_state(0, &th, nullptr, nullptr);
+      for (int k = 0; k < 2; ++k) CHECK(approx(th[k], -0.5 * ((0.5 - y[r]) * X[r][k]), 1e-15));
+    }
+    // the constructor's checks surface as std::invalid_argument
+    bool threw = false;
+    try {
+      ctx.set_logistic({{1.0, 0.0}}, {2}, 0.1);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
   if (failures == 0) std::printf("reference-style C++ caller: all checks passed\n");
   return failures == 0 ? 0 : 1;
 }
