@@ -510,3 +510,21 @@ def test_golden_trace_jsonl_schema_round_trips():
                                    '"sim_time":null,"sq_err_consensus":0,"sq_err_opt":null,"t":0}')
     with pytest.raises(RuntimeError, match="missing or mistyped"):
         TraceRecord.from_json_line('{"alpha":1}')
+
+
+def test_golden_trace_metrics_restatement():
+    """make_trace_record (simulator.cpp:92-123) restated (dsgdo_trace, the
+    GPU trace test's checker) on the oracle's final state equals the
+    reference's last trace record for the golden runs."""
+    from tests.golden.make_golden import RUN_CASES, TRACE_CASES
+    g = _golden("traces.npz")
+    for name in ("c1_allreduce", "pull8", "push5", "ea8", "stale4", "fresh4"):
+        cfg = RUN_CASES[name]
+        th, _, _, _ = O.run(cfg)
+        last = g[f"{name}_rec"][-1]
+        assert int(last[0]) == cfg.rounds
+        opt = np.zeros(cfg.d) if cfg.opt is None else np.asarray(cfg.opt)
+        m = O.trace(th, cfg.spectrum, opt)
+        assert m["sq_err_opt"] == pytest.approx(last[2], rel=1e-12), name
+        assert m["sq_err_consensus"] == pytest.approx(last[3], rel=1e-12, abs=1e-300), name
+        assert m["loss_mean"] == pytest.approx(last[4], rel=1e-12), name
