@@ -528,3 +528,18 @@ def test_golden_trace_metrics_restatement():
         assert m["sq_err_opt"] == pytest.approx(last[2], rel=1e-12), name
         assert m["sq_err_consensus"] == pytest.approx(last[3], rel=1e-12, abs=1e-300), name
         assert m["loss_mean"] == pytest.approx(last[4], rel=1e-12), name
+
+
+def test_golden_logistic_value_restatement():
+    """LogisticObjective::value restated (the GPU logistic trace test's
+    checker) on the reference's final lg_pull state equals the loss of the
+    reference's last trace record of the same run."""
+    from tests.golden.make_golden import LOGISTIC_CASES
+    lg = _golden("logistic.npz")
+    tr = _golden("traces.npz")
+    th = lg["lg_pull_theta"]
+    want = tr["lg_pull_rec"][-1]
+    assert int(want[0]) == LOGISTIC_CASES["lg_pull"].rounds
+    got = np.mean([O.logistic_value(lg["X"], lg["y"], float(lg["l2"]), th[i])
+                   for i in range(th.shape[0])])
+    assert got == pytest.approx(want[4], rel=1e-13)
