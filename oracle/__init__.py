@@ -627,3 +627,68 @@ def run_transport_allreduce(cfg: SimConfig, dtype=np.float64) -> "Nodes":
         n.dprev = deltas.copy() if cfg.per_node_scope else avg.copy()
         n.t += 1
     return n
+
+
+# --------------------------------------------------------------------------
+# LogisticObjective run_sync restated (pull-gossip and all-reduce), composed
+# from the primitives above exactly as simulator.cpp:234-369 drives them:
+# per round, every node draws its minibatch rows from its sample stream and
+# its noise from its noise stream; pull rounds mix first and take the
+# gradient at the mixed point (protocols.cpp:173-185).
+def logistic_run(cfg: SimConfig, X, y, l2: float, ranges, dtype=np.float64):
+    """Returns (theta[p,d], dprev[p,d], t[p]) for cfg.protocol in {PULL,
+    ALLREDUCE} with the gaussian-spread or zeros init."""
+    p, d = cfg.p, X.shape[1]
+    f = np.dtype(dtype).type
+    Xf = np.ascontiguousarray(X, dtype=dtype)
+    y = np.ascontiguousarray(y, dtype=np.int32)
+    base = np.zeros(d)
+    th = np.tile(base, (p, 1))
+    if cfg.init_kind == INIT_GAUSSIAN:  # simulator.cpp:196-205
+        for i in range(p):
+            s = Stream.make(cfg.seed, cfg.run_id, i, "init")
+            th[i] = base + cfg.init_scale * s.normals(d)
+    elif cfg.init_kind != INIT_ZEROS:
+        raise ValueError("gaussian-spread or zeros init only")
+    n = Nodes(th.astype(dtype), dtype=dtype)
+    sample = [Stream.make(cfg.seed, cfg.run_id, i, "sample") for i in range(p)]
+    noise_s = [Stream.make(cfg.seed, cfg.run_id, i, "gradient-noise") for i in range(p)]
+    partner_s = [Stream.make(cfg.seed, cfg.run_id, i, "partner-choice") for i in range(p)]
+    h = cfg.hyper
+    mu = f(h.mu)
+
+    def point(theta, dprev):
+        if h.mu == 0.0:
+            return theta.copy()
+        return (theta + (mu * dprev).astype(dtype)).astype(dtype)
+
+    def grads(theta, dprev):
+        pts = point(theta, dprev)
+        return np.stack([logistic_grad(Xf, y, l2, pts[i],
+                                       sample[i].draw_rows(int(ranges[i][0]), int(ranges[i][1]),
+                                                           h.batch)) for i in range(p)])
+
+    for r in range(cfg.rounds):
+        gated = r > 0 and r % h.tau == 0
+        noise = None  # NoiseModel::sample per node, after its rows (own stream)
+        if cfg.protocol == PULL and gated:
+            partners = np.array([partner_s[i].uniform_index(p) for i in range(p)], dtype=np.uint32)
+            mixed = pull_mix(n.theta, partners)
+            G = grads(mixed, n.dprev)
+            if cfg.sigma is not None:
+                noise = np.stack([cfg.sigma * noise_s[i].normals(d) for i in range(p)]).astype(dtype)
+            n = Nodes(mixed, n.dprev, n.t, dtype=dtype)
+            local_sgd_step(n, h, gfixed=G, noise=noise)
+        elif cfg.protocol == ALLREDUCE:
+            G = grads(n.theta, n.dprev)
+            if cfg.sigma is not None:
+                noise = np.stack([cfg.sigma * noise_s[i].normals(d) for i in range(p)]).astype(dtype)
+            allreduce_round(n, h, gfixed=G, noise=noise, per_node=cfg.per_node_scope)
+        elif cfg.protocol == PULL:
+            G = grads(n.theta, n.dprev)
+            if cfg.sigma is not None:
+                noise = np.stack([cfg.sigma * noise_s[i].normals(d) for i in range(p)]).astype(dtype)
+            local_sgd_step(n, h, gfixed=G, noise=noise)
+        else:
+            raise ValueError("pull-gossip or all-reduce only")
+    return n.theta, n.dprev, n.t

@@ -346,3 +346,17 @@ def test_p_nodes_batch_b_match_one_node_batch_pb():
         O.local_sgd_step(single, hs, gfixed=acc[None])
         assert np.abs(nodes[0].theta - single.theta[0]).max() <= 1e-10
         assert nodes[0].theta.tobytes() == nodes[1].theta.tobytes()
+
+
+@pytest.mark.parametrize("name", ["lg_pull", "lg_allreduce"])
+def test_logistic_trajectory_fp32_matches_fp32_restatement(name):
+    """fp32 contexts over 40 rounds against the oracle's fp32 logistic run
+    (same rows, noise and partners; the device's tree-summed dot product is
+    the only difference): within 1e-5."""
+    cfg, dc, obj, shards = _driver_case(name)
+    r = D.run_sync(dc, obj, dtype="f32", node_objs=shards)
+    gd = golden()
+    th, dp, t = O.logistic_run(cfg, gd["X"], gd["y"], float(gd["l2"]), gd["ranges"],
+                               dtype=np.float32)
+    assert r.t.tolist() == t.tolist()
+    assert close(r.theta.astype(np.float32), th, 1e-5)

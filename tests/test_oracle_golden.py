@@ -543,3 +543,17 @@ def test_golden_logistic_value_restatement():
     got = np.mean([O.logistic_value(lg["X"], lg["y"], float(lg["l2"]), th[i])
                    for i in range(th.shape[0])])
     assert got == pytest.approx(want[4], rel=1e-13)
+
+
+@pytest.mark.parametrize("name", ["lg_pull", "lg_allreduce", "lg_allreduce_agg"])
+def test_golden_logistic_trajectories_restated_bit_exact(name):
+    """The oracle's LogisticObjective run_sync (rows from the sample streams,
+    host noise, pull mix / ring-free pivot mean) reproduces the reference's
+    40-round trajectories byte for byte."""
+    from tests.golden.make_golden import LOGISTIC_CASES
+    g = _golden("logistic.npz")
+    th, dp, t = O.logistic_run(LOGISTIC_CASES[name], g["X"], g["y"], float(g["l2"]),
+                               g["ranges"])
+    assert th.tobytes() == g[f"{name}_theta"].tobytes()
+    assert dp.tobytes() == g[f"{name}_dprev"].tobytes()
+    assert t.tolist() == g[f"{name}_t"].tolist()
