@@ -151,6 +151,9 @@ dsgd_status dsgd_ctx_stream(dsgd_ctx* ctx, void** stream);
 /* Waits for the context's stream and reports device-side failures (a peer
  * timeout inside a kernel -> DSGD_ETIMEOUT). */
 dsgd_status dsgd_ctx_sync(dsgd_ctx* ctx);
+/* Raises the grad_norm_out of the rounds run since the last read to the
+ * device-side running max (one host wait). */
+dsgd_status dsgd_grad_norm_flush(dsgd_ctx* ctx);
 
 /* Buffers (device pointers, dtype elements, d per node). */
 typedef enum {
@@ -212,7 +215,12 @@ typedef struct {
   uint32_t use_noise;      /* 0: add +0.0 (NoiseModel::zero); 1: add DSGD_BUF_NOISE (e.g. the
                               reference noise stream drawn on the host); 2: N(0, noise_sigma^2)
                               drawn inside the kernel (Philox keyed by noise_seed, node, t) */
-  double* grad_norm_out;   /* optional: raised to max_i ||g_i|| like protocols.cpp:34-36 (syncs) */
+  double* grad_norm_out;   /* optional: raised to max ||g_i|| over nodes and rounds like
+                              protocols.cpp:34-36.  Accumulated on the device without a host
+                              wait; *grad_norm_out is raised lazily, when the call that
+                              needs it returns: dsgd_grad_norm_flush, dsgd_ctx_sync,
+                              dsgd_get_state, the end of dsgd_run_rounds / dsgd_run_events,
+                              or a round passing a different grad_norm_out pointer */
   double noise_sigma;      /* use_noise == 2 */
   uint64_t noise_seed;     /* use_noise == 2 */
   const uint64_t* rows;    /* GRAD_LOGISTIC: n_local * batch global row indices (host), node
@@ -280,7 +288,10 @@ dsgd_status dsgd_gossip_fresh_mix(dsgd_ctx* ctx, const uint32_t* partner_of, dou
 dsgd_status dsgd_ea_set_update_out(dsgd_ctx* ctx, void* const* update_out);
 /* ea_server_apply protocols.cpp:155-159: center += update (device vector) */
 dsgd_status dsgd_ea_server_apply(dsgd_ctx* ctx, const void* update);
-/* EASGD center = spatial_mean of the nodes' current theta (simulator.cpp:62-67) */
+/* EASGD center = spatial_mean of the nodes' current theta (simulator.cpp:62-67,
+ * pivot form param_vec.cpp:19-40).  One context per GPU: node 0's context reads
+ * every rank's theta over NVLink (call after every rank's dsgd_set_state, e.g.
+ * behind a host barrier); the others return at once. */
 dsgd_status dsgd_ea_init_center(dsgd_ctx* ctx);
 /* One client tick of asynchronous EASGD (run_async simulator.cpp:419-428):
  * node i (global id, single context) runs ea_client_step against the center
@@ -292,7 +303,7 @@ dsgd_status dsgd_ea_client_event(dsgd_ctx* ctx, const dsgd_hyperparams* h,
  * sum_i ||theta_i - theta*||^2, fp64 accumulation.  A non-finite parameter
  * returns DSGD_ESTATE ("non-finite parameter", the reference's
  * runtime_error).  One context per GPU: reads every peer's current theta over
- * NVLink; call after a host barrier so every peer finished the round. */
+ * NVLink once every peer has published its last round (device-side wait). */
 dsgd_status dsgd_trace(dsgd_ctx* ctx, double* sq_err_consensus, double* loss_mean,
                        double* sq_err_opt);
 
@@ -344,7 +355,7 @@ dsgd_status dsgd_ctx_attach_multicast(dsgd_ctx* ctx, void* x, void* x_mc, void* 
                                       void* avg_mc);
 dsgd_status dsgd_nccl_unique_id(void* id /* DSGD_NCCL_ID_BYTES */);
 dsgd_status dsgd_ctx_init_nccl(dsgd_ctx* ctx, const void* id, int rank, int nranks);
-/* Spin-wait bound for cross-GPU flags (default 10 s). */
+/* Spin-wait bound for cross-GPU flags (default 30 s). */
 dsgd_status dsgd_ctx_set_timeout(dsgd_ctx* ctx, double seconds);
 
 /* ----------------------------------------------------------- measurement */

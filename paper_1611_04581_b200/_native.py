@@ -98,6 +98,7 @@ _SIGS = {
     "dsgd_ctx_destroy": (None, [_P]),
     "dsgd_ctx_stream": (C.c_int, [_P, C.POINTER(_P)]),
     "dsgd_ctx_sync": (C.c_int, [_P]),
+    "dsgd_grad_norm_flush": (C.c_int, [_P]),
     "dsgd_buffer_ptr": (C.c_int, [_P, C.c_uint32, C.c_int, C.POINTER(_P)]),
     "dsgd_set_state": (C.c_int, [_P, C.c_uint32, _P, _P, C.c_uint64]),
     "dsgd_get_state": (C.c_int, [_P, C.c_uint32, _P, _P, _U64P]),

@@ -20,6 +20,7 @@ namespace dsgd {
 constexpr int kMaxLocal = 32;  // == DSGD_MAX_LOCAL_NODES
 constexpr int kMaxWait = 16;
 constexpr int kBlock = 256;
+constexpr uint32_t kNormSlots = 1024;  // rounds of grad-norm sums between folds
 
 // ---------------------------------------------------------------- arithmetic
 __device__ __forceinline__ float radd(float a, float b) { return __fadd_rn(a, b); }
@@ -125,6 +126,9 @@ __device__ __forceinline__ bool block_wait(const WaitSpec& w) {
   if (threadIdx.x == 0) {
     int good = 1;
     for (int i = 0; i < w.n && good; ++i) good = wait_flag(w.ptr[i], w.val[i], w.timeout_ns, w.error);
+    // the peers published their buffers with generic-proxy stores; this
+    // thread next reads them with cp.async.bulk (async proxy)
+    asm volatile("fence.proxy.async.global;" ::: "memory");
     ok = good;
     if (tr) w.trace[1] = globaltimer();
   }
@@ -210,6 +214,7 @@ __device__ __forceinline__ void block_add_double(double v, double* out) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if (lane == 0) atomicAdd(out, v);
   }
+  __syncthreads();  // part[] is reused by the next call
 }
 
 }  // namespace dsgd

@@ -12,6 +12,21 @@
 
 namespace dsgd {
 
+// Kernels issued by this thread (tail launches included): dsgd_launch_count.
+// (the file is compiled once per dtype, DSGD_KERNEL_DTYPE = 32 / 64, in
+// parallel; the counter lives in the fp32 object)
+#if !defined(DSGD_KERNEL_DTYPE) || DSGD_KERNEL_DTYPE == 32
+thread_local uint64_t g_launches = 0;
+uint64_t launches_issued() { return g_launches; }
+#else
+extern thread_local uint64_t g_launches;
+#endif
+#define DSGD_COUNTED(...) \
+  do {                    \
+    ++g_launches;         \
+    __VA_ARGS__;          \
+  } while (0)
+
 // compute_local_delta protocols.cpp:85-100 for one coordinate:
 //   la = mu != 0 ? theta + mu*delta_prev : theta          (92-93)
 //   g  = obj.stochastic_gradient(la)                       (30; quadratic: objectives.cpp:75)
@@ -520,7 +535,7 @@ cudaError_t launch_step_tma(const StepArgs<T>& a, cudaStream_t s) {
     const uint64_t tiles = a.d / st_tile<T>();
     uint32_t g = (uint32_t)sms * (uint32_t)resident;
     if (tiles < g) g = (uint32_t)(tiles ? tiles : 1);
-    k_step_tma2<T, MODE><<<g, kBlock, smem, s>>>(a);
+    DSGD_COUNTED(k_step_tma2<T, MODE><<<g, kBlock, smem, s>>>(a));
     return cudaGetLastError();
   }
   const size_t smem = 128 + (size_t)kStStages * st_tile<T>() * sizeof(T);
@@ -537,7 +552,7 @@ cudaError_t launch_step_tma(const StepArgs<T>& a, cudaStream_t s) {
   const uint64_t tiles = a.d / st_tile<T>();
   uint32_t g = (uint32_t)sms * (uint32_t)resident;
   if (tiles < g) g = (uint32_t)(tiles ? tiles : 1);
-  k_step_tma<T, MODE><<<g, kBlock, smem, s>>>(a);
+  DSGD_COUNTED(k_step_tma<T, MODE><<<g, kBlock, smem, s>>>(a));
   return cudaGetLastError();
 }
 
@@ -563,7 +578,7 @@ cudaError_t launch_step(int mode, const StepArgs<T>& a, int vec, uint32_t grid, 
     const uint64_t tiles = a.d / st_tile<T>();
     uint32_t g = (uint32_t)sms * (uint32_t)resident;
     if (tiles < g) g = (uint32_t)(tiles ? tiles : 1);
-    k_step_tma2<T, kModeAsync><<<g, kBlock, smem, s>>>(a);
+    DSGD_COUNTED(k_step_tma2<T, kModeAsync><<<g, kBlock, smem, s>>>(a));
     return cudaGetLastError();
   }
   // one node whose partner is a peer GPU: stage the NVLink stream in smem
@@ -575,9 +590,9 @@ cudaError_t launch_step(int mode, const StepArgs<T>& a, int vec, uint32_t grid, 
 #define DSGD_STEP_CASE(M)                                                   \
   case M:                                                                   \
     if (vec)                                                                \
-      k_step<T, M, true><<<grid, kBlock, 0, s>>>(a);                        \
+      DSGD_COUNTED(k_step<T, M, true><<<grid, kBlock, 0, s>>>(a));                        \
     else                                                                    \
-      k_step<T, M, false><<<grid, kBlock, 0, s>>>(a);                       \
+      DSGD_COUNTED(k_step<T, M, false><<<grid, kBlock, 0, s>>>(a));                       \
     break;
   switch (mode) {
     DSGD_STEP_CASE(kModeStep)
@@ -634,7 +649,7 @@ __global__ void __launch_bounds__(kBlock) k_ar_reduce(const __grid_constant__ Ar
 
 template <typename T>
 cudaError_t launch_ar_reduce(const ArReduceArgs<T>& a, uint32_t grid, cudaStream_t s) {
-  k_ar_reduce<T><<<grid, kBlock, 0, s>>>(a);
+  DSGD_COUNTED(k_ar_reduce<T><<<grid, kBlock, 0, s>>>(a));
   return cudaGetLastError();
 }
 
@@ -732,7 +747,7 @@ cudaError_t launch_ar_nvls(const ArNvlsArgs<T>& a, uint32_t grid, cudaStream_t s
     attr = true;
   }
   // one padded CTA per SM: 1024 threads keep enough switch reductions in flight
-  k_ar_nvls<T><<<grid, pad ? 1024 : kBlock, pad, s>>>(a);
+  DSGD_COUNTED(k_ar_nvls<T><<<grid, pad ? 1024 : kBlock, pad, s>>>(a));
   return cudaGetLastError();
 }
 
@@ -1072,7 +1087,7 @@ cudaError_t launch_os2(const ArOneShotArgs<T>& a, int max_ctas, cudaStream_t s) 
   const uint64_t tiles = a.d / os_tile<T>();
   uint32_t g = (uint32_t)sms * (uint32_t)resident;
   if (tiles < g) g = (uint32_t)(tiles ? tiles : 1);
-  k_ar_oneshot_tma2<T, P, S><<<g, kBlock, smem, s>>>(a);
+  DSGD_COUNTED(k_ar_oneshot_tma2<T, P, S><<<g, kBlock, smem, s>>>(a));
   return cudaGetLastError();
 }
 
@@ -1119,11 +1134,11 @@ cudaError_t launch_ar_oneshot_p(const ArOneShotArgs<T>& a, int vec, uint32_t gri
     uint32_t g = (uint32_t)sms * (uint32_t)resident;
     if (tiles < g) g = (uint32_t)(tiles ? tiles : 1);
     (void)grid;
-    k_ar_oneshot_tma<T, P><<<g, kBlock, smem, s>>>(a, (uint32_t)a.tma_rank);
+    DSGD_COUNTED(k_ar_oneshot_tma<T, P><<<g, kBlock, smem, s>>>(a, (uint32_t)a.tma_rank));
   } else if (vec) {
-    k_ar_oneshot<T, true, P><<<grid, kBlock, 0, s>>>(a);
+    DSGD_COUNTED(k_ar_oneshot<T, true, P><<<grid, kBlock, 0, s>>>(a));
   } else {
-    k_ar_oneshot<T, false, P><<<grid, kBlock, 0, s>>>(a);
+    DSGD_COUNTED(k_ar_oneshot<T, false, P><<<grid, kBlock, 0, s>>>(a));
   }
   return cudaGetLastError();
 }
@@ -1238,6 +1253,8 @@ __global__ void __launch_bounds__(kBlock) k_local_tma(const __grid_constant__ Al
     }
   }
   __syncthreads();
+  const bool norm = n.norm != nullptr;  // grad_norm_out: sum of g^2 (fp64)
+  double nacc = 0.0;
   for (uint64_t j = 0;; ++j) {
     const uint64_t tile = blockIdx.x + j * gridDim.x;
     if (tile >= nt) break;
@@ -1297,12 +1314,11 @@ __global__ void __launch_bounds__(kBlock) k_local_tma(const __grid_constant__ Al
     for (int u = 0; u < 2; ++u) {
       const uint64_t k = tile * TILE + (uint64_t)threadIdx.x * W + (uint64_t)u * kBlock * W;
       Lanes<T, true> ot, od;
-      double dummy = 0.0;
 #pragma unroll
       for (int l = 0; l < W; ++l) {
         const T d0 = sgd_delta(x[u].v[l], dp[u].v[l], gb[u].v[l], sp[u].v[l], o[u].v[l],
-                               xi[u].v[l], n.alpha, a.mu, a.wd, a.mu_nz, a.wd_pos, a.quad, false,
-                               dummy);
+                               xi[u].v[l], n.alpha, a.mu, a.wd, a.mu_nz, a.wd_pos, a.quad, norm,
+                               nacc);
         const T avg = radd(d0, rmul(T(0), a.inv_p));  // spatial_mean of one node (param_vec.cpp:37)
         ot.v[l] = radd(x[u].v[l], avg);
         od.v[l] = a.per_node ? d0 : avg;
@@ -1319,13 +1335,13 @@ __global__ void __launch_bounds__(kBlock) k_local_tma(const __grid_constant__ Al
     ld(x, n.theta_in, k);
     ld(dp, n.delta, k);
     ld_grad_inputs(gb, sp, o, xi, n, a.spec, a.opt, a.quad, k);
-    double dummy = 0.0;
     const T d0 = sgd_delta(x.v[0], dp.v[0], gb.v[0], sp.v[0], o.v[0], xi.v[0], n.alpha, a.mu,
-                           a.wd, a.mu_nz, a.wd_pos, a.quad, false, dummy);
+                           a.wd, a.mu_nz, a.wd_pos, a.quad, norm, nacc);
     const T avg = radd(d0, rmul(T(0), a.inv_p));
     n.theta_out[k] = radd(x.v[0], avg);
     n.delta[k] = a.per_node ? d0 : avg;
   }
+  block_add_double(nacc, n.norm);
 }
 
 template <typename T>
@@ -1357,6 +1373,7 @@ cudaError_t launch_local_tma(const AllreduceArgs<T>& a, cudaStream_t s) {
   attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  ++g_launches;
   return cudaLaunchKernelEx(&cfg, k_local_tma<T>, a);
 }
 
@@ -1492,9 +1509,9 @@ cudaError_t launch_ard_tma(int mode, const StepArgs<T>& a, uint32_t grid, cudaSt
   const uint64_t tiles = a.d / lt_tile<T>();
   if (tiles < grid) grid = (uint32_t)(tiles ? tiles : 1);
   if (mode == kModeApplyDelta)
-    k_ard_tma<T, kModeApplyDelta><<<grid, kBlock, smem, s>>>(a);
+    DSGD_COUNTED(k_ard_tma<T, kModeApplyDelta><<<grid, kBlock, smem, s>>>(a));
   else
-    k_ard_tma<T, kModeArDelta><<<grid, kBlock, smem, s>>>(a);
+    DSGD_COUNTED(k_ard_tma<T, kModeArDelta><<<grid, kBlock, smem, s>>>(a));
   return cudaGetLastError();
 }
 
@@ -1505,13 +1522,13 @@ cudaError_t launch_allreduce_local(const AllreduceArgs<T>& a, int vec, int norm,
     const char* e = getenv("DSGD_LOCAL_TMA");
     return !(e && e[0] == '0');
   }();
-  if (tma && a.p == 1 && vec && !norm) return launch_local_tma<T>(a, s);
+  if (tma && a.p == 1 && vec) return launch_local_tma<T>(a, s);  // norm fused too
   // the vector kernel covers d - d % W; a scalar launch finishes the tail
   if (vec) {
     if (norm)
-      k_allreduce_local<T, true, true><<<grid, kBlock, 0, s>>>(a);
+      DSGD_COUNTED(k_allreduce_local<T, true, true><<<grid, kBlock, 0, s>>>(a));
     else
-      k_allreduce_local<T, true, false><<<grid, kBlock, 0, s>>>(a);
+      DSGD_COUNTED(k_allreduce_local<T, true, false><<<grid, kBlock, 0, s>>>(a));
     const uint64_t W = Vec<T>::N, head = (a.d / W) * W;
     if (head != a.d) {
       AllreduceArgs<T> t = a;
@@ -1528,15 +1545,15 @@ cudaError_t launch_allreduce_local(const AllreduceArgs<T>& a, int vec, int norm,
       if (t.opt) t.opt += head;
       t.d = a.d - head;
       if (norm)
-        k_allreduce_local<T, false, true><<<1, kBlock, 0, s>>>(t);
+        DSGD_COUNTED(k_allreduce_local<T, false, true><<<1, kBlock, 0, s>>>(t));
       else
-        k_allreduce_local<T, false, false><<<1, kBlock, 0, s>>>(t);
+        DSGD_COUNTED(k_allreduce_local<T, false, false><<<1, kBlock, 0, s>>>(t));
     }
   } else {
     if (norm)
-      k_allreduce_local<T, false, true><<<grid, kBlock, 0, s>>>(a);
+      DSGD_COUNTED(k_allreduce_local<T, false, true><<<grid, kBlock, 0, s>>>(a));
     else
-      k_allreduce_local<T, false, false><<<grid, kBlock, 0, s>>>(a);
+      DSGD_COUNTED(k_allreduce_local<T, false, false><<<grid, kBlock, 0, s>>>(a));
   }
   return cudaGetLastError();
 }
@@ -1610,14 +1627,14 @@ template <typename T>
 cudaError_t launch_ea_local(const EaArgs<T>& a, int vec, int norm, uint32_t grid, cudaStream_t s,
                             bool mix_only) {
   if (mix_only) {  // gated client/server half only (the gradient comes later)
-    k_ea_local<T, false, false, true><<<grid, kBlock, 0, s>>>(a);
+    DSGD_COUNTED(k_ea_local<T, false, false, true><<<grid, kBlock, 0, s>>>(a));
     return cudaGetLastError();
   }
   if (vec) {
     if (norm)
-      k_ea_local<T, true, true><<<grid, kBlock, 0, s>>>(a);
+      DSGD_COUNTED(k_ea_local<T, true, true><<<grid, kBlock, 0, s>>>(a));
     else
-      k_ea_local<T, true, false><<<grid, kBlock, 0, s>>>(a);
+      DSGD_COUNTED(k_ea_local<T, true, false><<<grid, kBlock, 0, s>>>(a));
     const uint64_t W = Vec<T>::N, head = (a.d / W) * W;
     if (head != a.d) {
       EaArgs<T> t = a;
@@ -1636,15 +1653,15 @@ cudaError_t launch_ea_local(const EaArgs<T>& a, int vec, int norm, uint32_t grid
       t.center += head;
       t.d = a.d - head;
       if (norm)
-        k_ea_local<T, false, true><<<1, kBlock, 0, s>>>(t);
+        DSGD_COUNTED(k_ea_local<T, false, true><<<1, kBlock, 0, s>>>(t));
       else
-        k_ea_local<T, false, false><<<1, kBlock, 0, s>>>(t);
+        DSGD_COUNTED(k_ea_local<T, false, false><<<1, kBlock, 0, s>>>(t));
     }
   } else {
     if (norm)
-      k_ea_local<T, false, true><<<grid, kBlock, 0, s>>>(a);
+      DSGD_COUNTED(k_ea_local<T, false, true><<<grid, kBlock, 0, s>>>(a));
     else
-      k_ea_local<T, false, false><<<grid, kBlock, 0, s>>>(a);
+      DSGD_COUNTED(k_ea_local<T, false, false><<<grid, kBlock, 0, s>>>(a));
   }
   return cudaGetLastError();
 }
@@ -1712,9 +1729,9 @@ __global__ void __launch_bounds__(kBlock) k_push(const __grid_constant__ PushArg
 template <typename T>
 cudaError_t launch_push(const PushArgs<T>& a, int vec, uint32_t grid, cudaStream_t s) {
   if (vec)
-    k_push<T, true><<<grid, kBlock, 0, s>>>(a);
+    DSGD_COUNTED(k_push<T, true><<<grid, kBlock, 0, s>>>(a));
   else
-    k_push<T, false><<<grid, kBlock, 0, s>>>(a);
+    DSGD_COUNTED(k_push<T, false><<<grid, kBlock, 0, s>>>(a));
   return cudaGetLastError();
 }
 
@@ -1801,6 +1818,7 @@ __global__ void __launch_bounds__(kBlock) k_ea_chain(const __grid_constant__ EaC
     if (threadIdx.x == 0) st_release_sys(&a.flag_out[c], a.seq);
   }
   block_add_double(nacc, n.norm);
+  block_signal(a.signal);
 }
 
 template <typename T>
@@ -1808,15 +1826,15 @@ cudaError_t launch_ea_chain(const EaChainArgs<T>& a, int vec, uint32_t grid, cud
                             bool mix_only) {
   if (mix_only) {
     if (vec)
-      k_ea_chain<T, true, true><<<grid, kBlock, 0, s>>>(a);
+      DSGD_COUNTED(k_ea_chain<T, true, true><<<grid, kBlock, 0, s>>>(a));
     else
-      k_ea_chain<T, false, true><<<grid, kBlock, 0, s>>>(a);
+      DSGD_COUNTED(k_ea_chain<T, false, true><<<grid, kBlock, 0, s>>>(a));
     return cudaGetLastError();
   }
   if (vec)
-    k_ea_chain<T, true><<<grid, kBlock, 0, s>>>(a);
+    DSGD_COUNTED(k_ea_chain<T, true><<<grid, kBlock, 0, s>>>(a));
   else
-    k_ea_chain<T, false><<<grid, kBlock, 0, s>>>(a);
+    DSGD_COUNTED(k_ea_chain<T, false><<<grid, kBlock, 0, s>>>(a));
   return cudaGetLastError();
 }
 
@@ -1906,9 +1924,9 @@ __global__ void __launch_bounds__(kBlock) k_logistic_grad(const __grid_constant_
 template <typename T>
 cudaError_t launch_logistic(const LogisticArgs<T>& a, uint32_t grid, cudaStream_t s) {
   const uint32_t nr = a.n_nodes * a.batch;
-  k_logit_partial<T><<<dim3(a.nblk, nr < 65535u ? nr : 65535u), kBlock, 0, s>>>(a);
-  k_logit_coeff<T><<<nr, 32, 0, s>>>(a);
-  if (!a.value_mode) k_logistic_grad<T><<<grid, kBlock, 0, s>>>(a);
+  DSGD_COUNTED(k_logit_partial<T><<<dim3(a.nblk, nr < 65535u ? nr : 65535u), kBlock, 0, s>>>(a));
+  DSGD_COUNTED(k_logit_coeff<T><<<nr, 32, 0, s>>>(a));
+  if (!a.value_mode) DSGD_COUNTED(k_logistic_grad<T><<<grid, kBlock, 0, s>>>(a));
   return cudaGetLastError();
 }
 
@@ -1918,6 +1936,7 @@ cudaError_t launch_logistic(const LogisticArgs<T>& a, uint32_t grid, cudaStream_
 // objective value and optimum error, accumulated in fp64.
 template <typename T>
 __global__ void __launch_bounds__(kBlock) k_trace(const __grid_constant__ TraceArgs<T> a) {
+  if (!block_wait(a.wait)) return;
   double cons = 0.0, loss = 0.0, err = 0.0, bad = 0.0;
   const double inv_p = 1.0 / (double)a.p;
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < a.d;
@@ -1946,7 +1965,7 @@ __global__ void __launch_bounds__(kBlock) k_trace(const __grid_constant__ TraceA
 
 template <typename T>
 cudaError_t launch_trace(const TraceArgs<T>& a, uint32_t grid, cudaStream_t s) {
-  k_trace<T><<<grid, kBlock, 0, s>>>(a);
+  DSGD_COUNTED(k_trace<T><<<grid, kBlock, 0, s>>>(a));
   return cudaGetLastError();
 }
 
@@ -1982,7 +2001,7 @@ cudaError_t launch_spatial_mean(const T* const* x, uint32_t p, uint64_t d, T* ou
   a.inv_p = T(1) / T(p);
   a.out = out;
   const uint64_t blocks = (d + kBlock - 1) / kBlock;
-  k_spatial_mean<T><<<(unsigned)(blocks < 4096 ? (blocks ? blocks : 1) : 4096), kBlock, 0, s>>>(a);
+  DSGD_COUNTED(k_spatial_mean<T><<<(unsigned)(blocks < 4096 ? (blocks ? blocks : 1) : 4096), kBlock, 0, s>>>(a));
   return cudaGetLastError();
 }
 
@@ -2017,9 +2036,33 @@ cudaError_t launch_fill_normal(T* out, uint64_t n, double sigma, uint64_t seed, 
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint64_t need = (n / 4 + kBlock) / kBlock;
   const uint64_t grid = need < (uint64_t)sms * 8 ? (need ? need : 1) : (uint64_t)sms * 8;
-  k_fill_normal<T><<<(unsigned)grid, kBlock, 0, s>>>(out, n, sigma, seed, offset);
+  DSGD_COUNTED(k_fill_normal<T><<<(unsigned)grid, kBlock, 0, s>>>(out, n, sigma, seed, offset));
   return cudaGetLastError();
 }
+
+#if !defined(DSGD_KERNEL_DTYPE) || DSGD_KERNEL_DTYPE == 32
+__global__ void __launch_bounds__(kBlock) k_norm_fold(double* acc, uint64_t n, double* max) {
+  double m = 0.0;
+  for (uint64_t k = threadIdx.x; k < n; k += blockDim.x) {
+    m = fmax(m, sqrt(acc[k]));  // ParamVec::norm = sqrt(squared_norm)
+    acc[k] = 0.0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ double part[kBlock / 32];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, part[w]);
+    *max = fmax(*max, m);
+  }
+}
+
+cudaError_t launch_norm_fold(double* acc, uint64_t n, double* max, cudaStream_t s) {
+  DSGD_COUNTED(k_norm_fold<<<1, kBlock, 0, s>>>(acc, n, max));
+  return cudaGetLastError();
+}
+#endif
 
 #define DSGD_INSTANTIATE(T)                                                                        \
   template cudaError_t launch_step<T>(int, const StepArgs<T>&, int, uint32_t, cudaStream_t);       \
@@ -2040,7 +2083,11 @@ cudaError_t launch_fill_normal(T* out, uint64_t n, double sigma, uint64_t seed, 
                                               cudaStream_t);                                       \
   template cudaError_t launch_fill_normal<T>(T*, uint64_t, double, uint64_t, uint64_t, cudaStream_t);
 
+#if !defined(DSGD_KERNEL_DTYPE) || DSGD_KERNEL_DTYPE == 32
 DSGD_INSTANTIATE(float)
+#endif
+#if !defined(DSGD_KERNEL_DTYPE) || DSGD_KERNEL_DTYPE == 64
 DSGD_INSTANTIATE(double)
+#endif
 
 }  // namespace dsgd

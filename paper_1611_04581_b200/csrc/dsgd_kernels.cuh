@@ -36,6 +36,7 @@ struct TraceArgs {
   uint32_t p;
   uint64_t d;
   double* out;    // [0] sq_err_consensus, [1] sum_i 2 f(theta_i), [2] sq_err_opt, [3] non-finite count
+  WaitSpec wait;  // one node per GPU: every peer finished its last round
 };
 
 // Kernel modes of the fused gossip-family kernel k_step.
@@ -214,7 +215,11 @@ struct EaChainArgs {
   int mu_nz, wd_pos, quad;
   unsigned long long timeout_ns;
   unsigned int* error;
+  SignalSpec signal;  // publishes this rank's round counter when every chunk is done
 };
+
+// Kernels launched by the calling thread so far (every launch, tails included).
+uint64_t launches_issued();
 
 // Host-side launchers (explicitly instantiated for float and double).
 template <typename T>
@@ -244,6 +249,8 @@ template <typename T>
 cudaError_t launch_trace(const TraceArgs<T>& a, uint32_t grid, cudaStream_t s);
 template <typename T>
 cudaError_t launch_spatial_mean(const T* const* x, uint32_t p, uint64_t d, T* out, cudaStream_t s);
+// max over `n` per-round sums of g^2 of sqrt(sum) into *max, zeroing the sums
+cudaError_t launch_norm_fold(double* acc, uint64_t n, double* max, cudaStream_t s);
 template <typename T>
 cudaError_t launch_fill_normal(T* out, uint64_t n, double sigma, uint64_t seed, uint64_t offset,
                                cudaStream_t s);

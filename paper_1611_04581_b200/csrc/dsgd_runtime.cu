@@ -151,7 +151,7 @@ struct dsgd_ctx {
   double ar_delta_frac = 2.0;      // delta-kernel CTAs per SM, split over the pipelines
   double ar_comm_frac = 2.0;       // reduce-kernel CTAs per SM, split over the pipelines
   cudaStream_t pipe_stream[4] = {};
-  cudaEvent_t pipe_event[5] = {};  // [0..3] join, [4] fork
+  cudaEvent_t pipe_event[9] = {};  // [0..3] join, [4] fork, [5..8] delta kernels done
   bool pipes_forked = false;
   // DSGD_TRACE: per launch {kind, round, %globaltimer entry / after wait / done}
   unsigned long long* trace_dev = nullptr;
@@ -173,8 +173,16 @@ struct dsgd_ctx {
   char* aux[kMaxLocal] = {};
   char* spec = nullptr;
   char* opt = nullptr;
-  double* norm = nullptr;        // n_local sums of g^2
+  // grad_norm_out (protocols.cpp:34-36) on the device: each round (or
+  // event) accumulates every local node's sum of g^2 into its own slot of a
+  // ring; a fold kernel turns the used slots into max ||g|| (norm_max) every
+  // kNormSlots rounds and whenever the host reads, so no round syncs.
+  double* norm = nullptr;        // kNormSlots * n_local sums of g^2 (zeroed after each fold)
+  double* norm_max = nullptr;    // running max of ||g|| since the last host read
   double* norm_host = nullptr;   // pinned
+  uint32_t norm_slot = 0;        // next free slot
+  double* norm_out = nullptr;    // host grad_norm_out raised at the next read
+  double* scratch = nullptr;     // trace metrics (4 doubles)
   unsigned int* arrive = nullptr;
   unsigned int* error = nullptr;
   char* staging = nullptr;       // pinned host staging (d * 8 bytes)
@@ -258,8 +266,10 @@ struct LaunchScope {
   cudaStream_t st;
   bool nccl;  // an NCCL call (counted apart from this library's kernels)
   cudaEvent_t a = nullptr;
+  uint64_t issued0;  // dsgd::launches_issued() at entry: every kernel, tails included
   LaunchScope(dsgd_ctx* ctx, int kid, cudaStream_t on = nullptr, bool is_nccl = false)
-      : c(ctx), id(kid), st(on ? on : ctx->stream), nccl(is_nccl) {
+      : c(ctx), id(kid), st(on ? on : ctx->stream), nccl(is_nccl),
+        issued0(dsgd::launches_issued()) {
     if (c->profile) {
       a = take_event(c);
       cudaEventRecord(a, st);
@@ -268,8 +278,7 @@ struct LaunchScope {
   ~LaunchScope() {
     if (nccl)
       c->nccl_calls++;
-    else
-      c->kernels++;
+    c->kernels += dsgd::launches_issued() - issued0;
     if (c->profile) {
       cudaEvent_t b = take_event(c);
       cudaEventRecord(b, st);
@@ -364,7 +373,7 @@ void fill_node(dsgd_ctx* c, uint32_t i, const GradSel& gs, const dsgd_hyperparam
   n->noise = gs.noise ? as<T>(c->noise[i]) : nullptr;
   n->partner = nullptr;
   n->aux = nullptr;
-  n->norm = gs.norm ? c->norm + i : nullptr;
+  n->norm = gs.norm ? c->norm + (size_t)c->norm_slot * c->n_local + i : nullptr;
   const double alpha = h ? dsgd_step_size_at(h, c->t[i]) : 0.0;
   n->alpha = (T)(negate_alpha ? -alpha : alpha);
   n->nsigma = gs.dev_noise ? (T)gs.sigma : T(0);
@@ -393,21 +402,49 @@ bool all_aligned(dsgd_ctx* c, const GradSel& gs) {
   return true;
 }
 
-dsgd_status norm_begin(dsgd_ctx* c, const GradSel& gs) {
-  if (gs.norm) DSGD_CUDA(cudaMemsetAsync(c->norm, 0, sizeof(double) * c->n_local, c->stream));
+dsgd_status join_pipes(dsgd_ctx* c);
+
+// Folds the used norm slots into norm_max on the device (no host wait).
+dsgd_status norm_fold(dsgd_ctx* c) {
+  if (c->norm_slot == 0) return DSGD_OK;
+  DSGD_TRY(join_pipes(c));
+  {
+    LaunchScope ls(c, DSGD_K_OTHER);
+    DSGD_CUDA(dsgd::launch_norm_fold(c->norm, (uint64_t)c->norm_slot * c->n_local, c->norm_max,
+                                     c->stream));
+  }
+  c->norm_slot = 0;
   return DSGD_OK;
 }
 
-dsgd_status join_pipes(dsgd_ctx* c);
+// Raises the registered host grad_norm_out to the device running max and
+// restarts the max (the only place the norm path waits for the device).
+dsgd_status norm_read(dsgd_ctx* c) {
+  if (!c->norm_out) return DSGD_OK;
+  DSGD_TRY(norm_fold(c));
+  DSGD_TRY(join_pipes(c));
+  DSGD_CUDA(cudaMemcpyAsync(c->norm_host, c->norm_max, sizeof(double), cudaMemcpyDeviceToHost,
+                            c->stream));
+  DSGD_CUDA(cudaMemsetAsync(c->norm_max, 0, sizeof(double), c->stream));
+  DSGD_CUDA(cudaStreamSynchronize(c->stream));
+  *c->norm_out = std::max(*c->norm_out, c->norm_host[0]);
+  c->norm_out = nullptr;
+  return DSGD_OK;
+}
+
+// A round that reports its gradient norm writes slot norm_slot; a different
+// host pointer than the registered one first settles the registered one.
+dsgd_status norm_begin(dsgd_ctx* c, const GradSel& gs, const dsgd_grad_spec* g) {
+  if (!gs.norm) return DSGD_OK;
+  if (c->norm_out && c->norm_out != g->grad_norm_out) DSGD_TRY(norm_read(c));
+  c->norm_out = g->grad_norm_out;
+  if (c->norm_slot >= dsgd::kNormSlots) DSGD_TRY(norm_fold(c));
+  return DSGD_OK;
+}
 
 dsgd_status norm_end(dsgd_ctx* c, const GradSel& gs, const dsgd_grad_spec* g) {
-  if (!gs.norm) return DSGD_OK;
-  DSGD_TRY(join_pipes(c));
-  DSGD_CUDA(cudaMemcpyAsync(c->norm_host, c->norm, sizeof(double) * c->n_local,
-                            cudaMemcpyDeviceToHost, c->stream));
-  DSGD_CUDA(cudaStreamSynchronize(c->stream));
-  for (uint32_t i = 0; i < c->n_local; ++i)
-    *g->grad_norm_out = std::max(*g->grad_norm_out, std::sqrt(c->norm_host[i]));
+  (void)g;
+  if (gs.norm) c->norm_slot += 1;
   return DSGD_OK;
 }
 
@@ -445,24 +482,47 @@ void trace_slot(dsgd_ctx* c, int kind, dsgd::WaitSpec* w, dsgd::SignalSpec* s) {
 
 // Wait list of a multi-GPU round that reads `reads` (the partner, or none)
 // and overwrites the snapshot the previous round's pullers read.
-void build_waits(dsgd_ctx* c, const std::vector<uint32_t>& reads, dsgd::WaitSpec* w) {
+dsgd_status build_waits(dsgd_ctx* c, const std::vector<uint32_t>& reads, dsgd::WaitSpec* w) {
   w->n = 0;
   w->timeout_ns = c->timeout_ns;
   w->error = c->error;
-  if (!c->distributed()) return;
+  if (!c->distributed()) return DSGD_OK;
   const uint32_t me = c->first;
+  bool full = false;
   auto add = [&](uint32_t node) {
     if (node == me) return;
     for (int k = 0; k < w->n; ++k)
       if (w->ptr[k] == c->peers[node].round) return;
-    if (w->n < kMaxWait) {
-      w->ptr[w->n] = c->peers[node].round;
-      w->val[w->n] = c->seq;
-      w->n++;
+    if (w->n == kMaxWait) {
+      full = true;
+      return;
     }
+    w->ptr[w->n] = c->peers[node].round;
+    w->val[w->n] = c->seq;
+    w->n++;
   };
   for (uint32_t j : reads) add(j);            // RAW: partner finished round r-1
   for (uint32_t k : c->prev_readers) add(k);  // WAR: last round's readers of my snapshot
+  if (full)  // never drop a wait: that would be a silent race
+    return set_error(DSGD_EINVAL, "more than 16 peers to wait for in one round");
+  return DSGD_OK;
+}
+
+// Waits until every peer has published round counter `value` (all of them
+// finished the same lock-step launch sequence).
+dsgd_status all_peer_waits(dsgd_ctx* c, unsigned long long value, dsgd::WaitSpec* w) {
+  w->n = 0;
+  w->timeout_ns = c->timeout_ns;
+  w->error = c->error;
+  if (!c->distributed()) return DSGD_OK;
+  for (uint32_t k = 0; k < c->p; ++k) {
+    if (k == c->first) continue;
+    if (w->n == kMaxWait) return set_error(DSGD_EINVAL, "more than 16 peers to wait for");
+    w->ptr[w->n] = c->peers[k].round;
+    w->val[w->n] = value;
+    w->n++;
+  }
+  return DSGD_OK;
 }
 
 void build_signal(dsgd_ctx* c, dsgd::SignalSpec* s) {
@@ -502,7 +562,7 @@ dsgd_status run_step_mode(dsgd_ctx* c, int mode, int kid, const dsgd_hyperparams
                   partner_of[c->first] != c->first;
   const uint64_t W = vec ? 16 / sizeof(T) : 1;
   a.blocks_per_node = blocks_for(c, (c->d / W + 1) / 2, c->n_local);
-  build_waits(c, reads, &a.wait);
+  DSGD_TRY(build_waits(c, reads, &a.wait));
   build_signal(c, &a.signal);
   trace_slot(c, kid, &a.wait, &a.signal);
   const uint32_t grid = a.blocks_per_node * c->n_local;
@@ -606,7 +666,6 @@ dsgd_status produce_logistic(dsgd_ctx* c, const dsgd_hyperparams* h, const GradS
   a.lookahead = lookahead && h->mu != 0.0;
   LaunchScope ls(c, DSGD_K_OTHER);
   DSGD_CUDA(dsgd::launch_logistic<T>(a, blocks_for(c, c->d, 1), c->stream));
-  c->kernels += 2;  // three launches under one scope
   return DSGD_OK;
 }
 
@@ -650,7 +709,6 @@ dsgd_status logistic_values(dsgd_ctx* c, double* data) {
   {
     LaunchScope ls(c, DSGD_K_OTHER);
     DSGD_CUDA(dsgd::launch_logistic<T>(a, 1, c->stream));
-    c->kernels += 1;
   }
   std::vector<double> terms(nr);
   DSGD_CUDA(cudaMemcpyAsync(terms.data(), a.coeff, nr * sizeof(double), cudaMemcpyDeviceToHost,
@@ -715,8 +773,9 @@ dsgd_status join_pipes(dsgd_ctx* c) {
   return DSGD_OK;
 }
 
+// Orders this round's pipeline work after everything on the context stream
+// (e.g. the caller's gradient upload).  Recorded every round.
 dsgd_status fork_pipes(dsgd_ctx* c) {
-  if (c->pipes_forked) return DSGD_OK;
   DSGD_CUDA(cudaEventRecord(c->pipe_event[4], c->stream));
   for (uint32_t h = 0; h < c->ar_pipes; ++h)
     DSGD_CUDA(cudaStreamWaitEvent(c->pipe_stream[h], c->pipe_event[4], 0));
@@ -914,6 +973,13 @@ dsgd_status do_allreduce_p2p(dsgd_ctx* c, const dsgd_hyperparams* h, const GradS
         DSGD_CUDA(dsgd::launch_step<T>(mode, a, vec, a.blocks_per_node, st));
       }
     }
+    if (K > 1) {
+      // the delta kernel is this round's only reader of the caller's buffers
+      // (gradient, noise): order the context stream after it, so the next
+      // upload into them cannot overwrite what it still reads
+      DSGD_CUDA(cudaEventRecord(c->pipe_event[5 + pi], st));
+      DSGD_CUDA(cudaStreamWaitEvent(c->stream, c->pipe_event[5 + pi], 0));
+    }
     dsgd::WaitSpec wx{};
     wx.timeout_ns = c->timeout_ns;
     wx.error = c->error;
@@ -1074,6 +1140,7 @@ dsgd_status do_ea(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& gs, int
   a.quad = gs.quad;
   a.timeout_ns = c->timeout_ns;
   a.error = c->error;
+  build_signal(c, &a.signal);
   const bool vec = all_aligned(c, gs);
   // one CTA per chunk: a CTA blocked on its flag or in its release fence
   // leaves the SM to the other resident chunks (dispatch is in chunk order,
@@ -1081,6 +1148,7 @@ dsgd_status do_ea(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& gs, int
   const uint32_t grid = (uint32_t)std::min<uint64_t>(a.n_chunks, 0x7fffffffu);
   LaunchScope ls(c, DSGD_K_EA);
   DSGD_CUDA(dsgd::launch_ea_chain<T>(a, vec, grid, c->stream, mix_only));
+  c->seq += 1;
   c->prev_readers.clear();
   return DSGD_OK;
 }
@@ -1117,7 +1185,7 @@ dsgd_status do_push(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel* gs,
   bool vec = gs ? all_aligned(c, *gs) : true;
   const uint64_t W = vec ? 16 / sizeof(T) : 1;
   a.blocks_per_node = blocks_for(c, c->d / W, c->n_local);
-  build_waits(c, reads, &a.wait);
+  DSGD_TRY(build_waits(c, reads, &a.wait));
   build_signal(c, &a.signal);
   LaunchScope ls(c, DSGD_K_PUSH);
   DSGD_CUDA(dsgd::launch_push<T>(a, vec, a.blocks_per_node * c->n_local, c->stream));
@@ -1283,7 +1351,14 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
     DSGD_CUDA(cudaMemset(c->spec, 0, vb));
     DSGD_CUDA(cudaMemset(c->opt, 0, vb));
   }
-  DSGD_CUDA(cudaMalloc(&c->norm, sizeof(double) * kMaxLocal));
+  {
+    const size_t nb = sizeof(double) * dsgd::kNormSlots * c->n_local;
+    DSGD_CUDA(cudaMalloc(&c->norm, nb));
+    DSGD_CUDA(cudaMemset(c->norm, 0, nb));
+    DSGD_CUDA(cudaMalloc(&c->norm_max, sizeof(double) * 8));
+    DSGD_CUDA(cudaMemset(c->norm_max, 0, sizeof(double) * 8));
+    c->scratch = c->norm_max + 4;
+  }
   DSGD_CUDA(cudaMallocHost(&c->norm_host, sizeof(double) * kMaxLocal));
   DSGD_CUDA(cudaMalloc(&c->arrive, 256));
   DSGD_CUDA(cudaMemset(c->arrive, 0, 256));
@@ -1294,7 +1369,7 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
   if (c->n_local < c->p) {
     for (int h = 0; h < 4; ++h)
       DSGD_CUDA(cudaStreamCreateWithFlags(&c->pipe_stream[h], cudaStreamNonBlocking));
-    for (int h = 0; h < 5; ++h)
+    for (int h = 0; h < 9; ++h)
       DSGD_CUDA(cudaEventCreateWithFlags(&c->pipe_event[h], cudaEventDisableTiming));
   }
   c->error = c->arrive + 32;
@@ -1336,6 +1411,7 @@ void dsgd_ctx_destroy(dsgd_ctx* c) {
   cudaFree(c->spec);
   cudaFree(c->opt);
   cudaFree(c->norm);
+  cudaFree(c->norm_max);
   cudaFreeHost(c->norm_host);
   cudaFree(c->arrive);
   cudaFree(c->trace_dev);
@@ -1364,7 +1440,7 @@ void dsgd_ctx_destroy(dsgd_ctx* c) {
       cudaStreamSynchronize(c->pipe_stream[h]);
       cudaStreamDestroy(c->pipe_stream[h]);
     }
-  for (int h = 0; h < 5; ++h)
+  for (int h = 0; h < 9; ++h)
     if (c->pipe_event[h]) cudaEventDestroy(c->pipe_event[h]);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -1379,12 +1455,19 @@ dsgd_status dsgd_ctx_stream(dsgd_ctx* c, void** stream) {
 dsgd_status dsgd_ctx_sync(dsgd_ctx* c) {
   DSGD_TRY(check_ctx(c));
   DeviceGuard g(c->device);
+  DSGD_TRY(norm_read(c));
   DSGD_TRY(join_pipes(c));
   DSGD_CUDA(cudaStreamSynchronize(c->stream));
   unsigned int err = 0;
   DSGD_CUDA(cudaMemcpy(&err, c->error, sizeof(err), cudaMemcpyDeviceToHost));
   if (err) return set_error(DSGD_ETIMEOUT, "a peer flag wait timed out inside a kernel");
   return DSGD_OK;
+}
+
+dsgd_status dsgd_grad_norm_flush(dsgd_ctx* c) {
+  DSGD_TRY(check_ctx(c));
+  DeviceGuard g(c->device);
+  return norm_read(c);
 }
 
 dsgd_status dsgd_ctx_set_timeout(dsgd_ctx* c, double seconds) {
@@ -1560,7 +1643,7 @@ dsgd_status dsgd_local_sgd_step(dsgd_ctx* c, const dsgd_hyperparams* h, const ds
   DSGD_TRY(resolve_grad(c, g, &gs));
   return dispatch(c, [&](auto z) -> dsgd_status {
     using T = decltype(z);
-    DSGD_TRY(norm_begin(c, gs));
+    DSGD_TRY(norm_begin(c, gs, g));
     DSGD_TRY(produce_logistic<T>(c, h, gs, all_local(c), true));
     DSGD_TRY(do_local_step<T>(c, h, gs));
     finish_round(c, true);
@@ -1579,7 +1662,7 @@ dsgd_status dsgd_allreduce_round(dsgd_ctx* c, const dsgd_hyperparams* h, const d
   if (gs.logistic) DSGD_TRY(flush_pending(c));  // the gradient reads the applied theta
   return dispatch(c, [&](auto z) -> dsgd_status {
     using T = decltype(z);
-    DSGD_TRY(norm_begin(c, gs));
+    DSGD_TRY(norm_begin(c, gs, g));
     DSGD_TRY(produce_logistic<T>(c, h, gs, all_local(c), true));
     DSGD_TRY(do_allreduce<T>(c, h, gs, scope));
     finish_round(c, !c->distributed());  // multi-GPU: do_allreduce tracks the buffers
@@ -1597,7 +1680,7 @@ dsgd_status dsgd_ea_round(dsgd_ctx* c, const dsgd_hyperparams* h, const dsgd_gra
   DSGD_TRY(resolve_grad(c, g, &gs));
   return dispatch(c, [&](auto z) -> dsgd_status {
     using T = decltype(z);
-    DSGD_TRY(norm_begin(c, gs));
+    DSGD_TRY(norm_begin(c, gs, g));
     if (gs.logistic && gated) {
       // client/server half, then the minibatch gradient at the moved theta,
       // then the step (ea_client_step protocols.cpp:146-151)
@@ -1627,7 +1710,7 @@ dsgd_status dsgd_pull_gossip_round(dsgd_ctx* c, const dsgd_hyperparams* h,
   DSGD_TRY(resolve_grad(c, g, &gs));
   return dispatch(c, [&](auto z) -> dsgd_status {
     using T = decltype(z);
-    DSGD_TRY(norm_begin(c, gs));
+    DSGD_TRY(norm_begin(c, gs, g));
     if (partner_of && gs.logistic) {
       // pull_mix, then the minibatch gradient at the mixed theta, then the
       // step (protocols.cpp:173-185)
@@ -1661,7 +1744,7 @@ dsgd_status dsgd_push_gossip_round(dsgd_ctx* c, const dsgd_hyperparams* h,
   DSGD_TRY(resolve_grad(c, g, &gs));
   return dispatch(c, [&](auto z) -> dsgd_status {
     using T = decltype(z);
-    DSGD_TRY(norm_begin(c, gs));
+    DSGD_TRY(norm_begin(c, gs, g));
     if (gs.logistic) {  // push_mix, gradient at the mixed theta, step (230-242)
       DSGD_TRY(do_push<T>(c, nullptr, nullptr, target_of));
       finish_round(c, true, false);
@@ -1687,7 +1770,7 @@ dsgd_status dsgd_gossip_stale_round(dsgd_ctx* c, const dsgd_hyperparams* h,
   DSGD_TRY(resolve_grad(c, g, &gs));
   return dispatch(c, [&](auto z) -> dsgd_status {
     using T = decltype(z);
-    DSGD_TRY(norm_begin(c, gs));
+    DSGD_TRY(norm_begin(c, gs, g));
     DSGD_TRY(produce_logistic<T>(c, h, gs, all_local(c), true));
     DSGD_TRY(do_pull<T>(c, h, gs, partner_of, dsgd::kModeStale, (T)h->beta_gossip));
     finish_round(c, true);
@@ -1706,7 +1789,7 @@ dsgd_status dsgd_gossip_fresh_round(dsgd_ctx* c, const dsgd_hyperparams* h,
   DSGD_TRY(resolve_grad(c, g, &gs));
   return dispatch(c, [&](auto z) -> dsgd_status {
     using T = decltype(z);
-    DSGD_TRY(norm_begin(c, gs));
+    DSGD_TRY(norm_begin(c, gs, g));
     // every node steps (theta' into the other buffer), then mixes with the
     // partner's post-step theta' (simulator.cpp:305-319)
     DSGD_TRY(produce_logistic<T>(c, h, gs, all_local(c), true));
@@ -1731,7 +1814,7 @@ dsgd_status dsgd_async_pull_event(dsgd_ctx* c, const dsgd_hyperparams* h,
   DSGD_TRY(resolve_grad(c, g, &gs));
   return dispatch(c, [&](auto z) -> dsgd_status {
     using T = decltype(z);
-    DSGD_TRY(norm_begin(c, gs));
+    DSGD_TRY(norm_begin(c, gs, g));
     // model_gradient at theta_i itself (protocols.cpp:287: no lookahead)
     DSGD_TRY(produce_logistic<T>(c, h, gs, {i}, false));
     // in place on node i (only node i changes; j == i reads the pre-event value)
@@ -1739,7 +1822,7 @@ dsgd_status dsgd_async_pull_event(dsgd_ctx* c, const dsgd_hyperparams* h,
     fill_node<T>(c, i, gs, h, &a.node[0], true);
     a.node[0].theta_out = as<T>(c->theta_ptr(i, c->cur));
     a.node[0].partner = as<T>(c->theta_ptr(j, c->cur));
-    a.node[0].norm = gs.norm ? c->norm : nullptr;
+    a.node[0].norm = gs.norm ? c->norm + (size_t)c->norm_slot * c->n_local : nullptr;
     fill_common(c, h, gs, &a);
     a.beta = (T)h->beta_gossip;
     a.n_local = 1;
@@ -1754,13 +1837,7 @@ dsgd_status dsgd_async_pull_event(dsgd_ctx* c, const dsgd_hyperparams* h,
       DSGD_CUDA(dsgd::launch_step<T>(dsgd::kModeAsync, a, vec, a.blocks_per_node, c->stream));
     }
     c->t[i] += 1;
-    if (gs.norm) {
-      DSGD_CUDA(cudaMemcpyAsync(c->norm_host, c->norm, sizeof(double), cudaMemcpyDeviceToHost,
-                                c->stream));
-      DSGD_CUDA(cudaStreamSynchronize(c->stream));
-      *g->grad_norm_out = std::max(*g->grad_norm_out, std::sqrt(c->norm_host[0]));
-    }
-    return DSGD_OK;
+    return norm_end(c, gs, g);
   });
 }
 
@@ -1851,13 +1928,13 @@ dsgd_status dsgd_ea_client_event(dsgd_ctx* c, const dsgd_hyperparams* h,
   DSGD_TRY(resolve_grad(c, g, &gs));
   return dispatch(c, [&](auto z) -> dsgd_status {
     using T = decltype(z);
-    DSGD_TRY(norm_begin(c, gs));
+    DSGD_TRY(norm_begin(c, gs, g));
     dsgd::EaArgs<T> a{};
     fill_node<T>(c, i, gs, h, &a.node[0]);
     a.node[0].theta_out = as<T>(c->theta_ptr(i, c->cur));  // in place: only node i moves
     if (!gs.quad) a.node[0].grad = static_cast<const T*>(gs.grad[i]);
     a.node[0].noise = gs.noise ? as<T>(c->noise[i]) : nullptr;
-    a.node[0].norm = gs.norm ? c->norm : nullptr;
+    a.node[0].norm = gs.norm ? c->norm + (size_t)c->norm_slot * c->n_local : nullptr;
     fill_common(c, h, gs, &a);
     a.center = as<T>(c->arena + c->off_c_in);
     a.beta = (T)h->beta_ea;
@@ -1876,13 +1953,7 @@ dsgd_status dsgd_ea_client_event(dsgd_ctx* c, const dsgd_hyperparams* h,
       DSGD_CUDA(dsgd::launch_ea_local<T>(a, vec, gs.norm, blocks_for(c, c->d / W, 1), c->stream));
     }
     c->t[i] += 1;
-    if (gs.norm) {
-      DSGD_CUDA(cudaMemcpyAsync(c->norm_host, c->norm, sizeof(double), cudaMemcpyDeviceToHost,
-                                c->stream));
-      DSGD_CUDA(cudaStreamSynchronize(c->stream));
-      *g->grad_norm_out = std::max(*g->grad_norm_out, std::sqrt(c->norm_host[0]));
-    }
-    return DSGD_OK;
+    return norm_end(c, gs, g);
   });
 }
 
@@ -1900,14 +1971,16 @@ dsgd_status dsgd_trace(dsgd_ctx* c, double* sq_err_consensus, double* loss_mean,
     a.opt = c->spec ? as<T>(c->opt) : nullptr;
     a.p = c->p;
     a.d = c->d;
-    a.out = c->norm;  // 4 doubles of scratch
-    DSGD_CUDA(cudaMemsetAsync(c->norm, 0, 4 * sizeof(double), c->stream));
+    a.out = c->scratch;
+    // every peer's current theta is final once its last launch published
+    DSGD_TRY(all_peer_waits(c, c->seq, &a.wait));
+    DSGD_CUDA(cudaMemsetAsync(c->scratch, 0, 4 * sizeof(double), c->stream));
     {
       LaunchScope ls(c, DSGD_K_OTHER);
       DSGD_CUDA(dsgd::launch_trace<T>(a, blocks_for(c, c->d, 1), c->stream));
     }
-    DSGD_CUDA(cudaMemcpyAsync(c->norm_host, c->norm, 4 * sizeof(double), cudaMemcpyDeviceToHost,
-                              c->stream));
+    DSGD_CUDA(cudaMemcpyAsync(c->norm_host, c->scratch, 4 * sizeof(double),
+                              cudaMemcpyDeviceToHost, c->stream));
     DSGD_CUDA(cudaStreamSynchronize(c->stream));
     if (c->norm_host[3] != 0.0)
       return set_error(DSGD_ESTATE, "non-finite parameter encountered at t=" +
@@ -1941,20 +2014,15 @@ dsgd_status dsgd_ea_init_center(dsgd_ctx* c) {
       DSGD_CUDA(dsgd::launch_spatial_mean<T>(xs, c->p, c->d, center, c->stream));
       return DSGD_OK;
     }
-    if (!c->comm) return set_error(DSGD_ESTATE, "multi-GPU center init needs NCCL");
-    // mean over ranks (NCCL average; not the reference's pivot order) into a
-    // scratch buffer; only node 0's context owns the server center.  (Other
-    // ranks' c_in are written by their chain predecessor only.)
-    if (!c->aux[0]) DSGD_CUDA(cudaMalloc(&c->aux[0], c->d * c->es));
-    {
-      LaunchScope ls(c, DSGD_K_NCCL, nullptr, true);
-      DSGD_NCCL(ncclAllReduce(c->theta_ptr(0, c->cur), c->aux[0], c->d,
-                              sizeof(T) == 4 ? ncclFloat : ncclDouble, ncclAvg, c->comm,
-                              c->stream));
-    }
-    if (c->first == 0)
-      DSGD_CUDA(cudaMemcpyAsync(center, c->aux[0], c->d * c->es, cudaMemcpyDeviceToDevice,
-                                c->stream));
+    // only node 0's context owns the server center (other ranks' c_in are
+    // written by their chain predecessor): it reads every rank's theta over
+    // NVLink and forms the reference's pivot-form mean (param_vec.cpp:19-40)
+    if (!c->connected) return set_error(DSGD_ESTATE, "peers not connected");
+    if (c->first != 0) return DSGD_OK;
+    const T* xs[kMaxLocal];
+    for (uint32_t k = 0; k < c->p; ++k) xs[k] = as<T>(c->peers[k].theta[c->cur]);
+    LaunchScope ls(c, DSGD_K_OTHER);
+    DSGD_CUDA(dsgd::launch_spatial_mean<T>(xs, c->p, c->d, center, c->stream));
     return DSGD_OK;
   });
 }
@@ -1987,6 +2055,7 @@ dsgd_status dsgd_run_events(dsgd_ctx* c, const dsgd_run_desc* run, uint64_t even
                             double rate_per_node, double* sim_time, double* alpha) {
   DSGD_TRY(check_ctx(c));
   if (!run) return set_error(DSGD_EINVAL, "null run descriptor");
+  DSGD_TRY(dsgd_hyperparams_validate(&run->hyper));
   const dsgd_protocol proto = run->protocol;
   if (proto != DSGD_ASYNC_PULL && proto != DSGD_ELASTIC_AVG)
     return set_error(DSGD_EINVAL, "asynchronous driver supports async-pull and elastic-avg");
@@ -2030,7 +2099,7 @@ dsgd_status dsgd_run_events(dsgd_ctx* c, const dsgd_run_desc* run, uint64_t even
   }
   if (sim_time) *sim_time = now;
   if (alpha) *alpha = last_alpha;
-  return DSGD_OK;
+  return norm_read(c);  // grad_norm_out: one host read per run, not per event
 }
 
 dsgd_status dsgd_ctx_round(dsgd_ctx* c, uint64_t* round) {
@@ -2042,6 +2111,7 @@ dsgd_status dsgd_ctx_round(dsgd_ctx* c, uint64_t* round) {
 dsgd_status dsgd_run_rounds(dsgd_ctx* c, const dsgd_run_desc* run) {
   DSGD_TRY(check_ctx(c));
   if (!run) return set_error(DSGD_EINVAL, "null run descriptor");
+  DSGD_TRY(dsgd_hyperparams_validate(&run->hyper));
   const dsgd_protocol proto = run->protocol;
   const bool needs_partners = proto == DSGD_PULL_GOSSIP || proto == DSGD_GOSSIP_STALE ||
                               proto == DSGD_GOSSIP_FRESH || proto == DSGD_PUSH_GOSSIP;
@@ -2110,7 +2180,9 @@ dsgd_status dsgd_run_rounds(dsgd_ctx* c, const dsgd_run_desc* run) {
   }
   // leave the context in its logical state (the timed work of `rounds`
   // rounds includes the last deferred apply)
-  return flush_pending(c);
+  DSGD_TRY(flush_pending(c));
+  DeviceGuard dg(c->device);
+  return norm_read(c);  // grad_norm_out: one host read per run, not per round
 }
 
 // -------------------------------------------------------- multi-GPU wiring

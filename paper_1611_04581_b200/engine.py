@@ -294,7 +294,11 @@ class Group:
         self._norm.value = 0.0
         gs = self._grad(grad, noise, grad_norm, rows)
         N.check(fn(self._ctx, *args[:1], C.byref(gs), *args[1:]))
-        return self._norm.value if grad_norm else None
+        if not grad_norm:
+            return None
+        # the library raises grad_norm_out lazily (no per-round host wait)
+        N.check(self.lib.dsgd_grad_norm_flush(self._ctx))
+        return self._norm.value
 
     def local_sgd_step(self, h: Hyperparams, **kw):
         hc = h.to_c()

@@ -117,59 +117,6 @@ class LogisticObjective:
         return self.l2, self.lipschitz
 
 
-def _stod_full(cell: str):
-    """std::stod plus the trailing-whitespace check of objectives.cpp:214-227:
-    the whole cell (leading/trailing whitespace allowed) must be one number."""
-    t = cell.strip()
-    if not t or "_" in t:
-        return None
-    try:
-        return float(t)
-    except ValueError:
-        if "0x" not in t.lower():  # strtod's hex floats need the 0x prefix
-            return None
-        try:
-            return float.fromhex(t)
-        except ValueError:
-            return None
-
-
-def load_csv_dataset(path: str, has_header: bool, l2: float) -> LogisticObjective:
-    """load_csv_dataset objectives.cpp:195-248: "label,f1,...,fd" rows,
-    labels 0/1, CR-LF tolerated, blank lines skipped, malformed rows
-    reported with their line number (RuntimeError like std::runtime_error)."""
-    try:
-        f = open(path, "r", newline="")
-    except OSError:
-        raise RuntimeError("cannot open dataset: " + path)
-    features, labels = [], []
-    with f:
-        for line_no, line in enumerate(f.read().split("\n"), start=1):
-            if line_no == 1 and has_header:
-                continue
-            if line.endswith("\r"):
-                line = line[:-1]
-            if not line:
-                continue
-            fields = []
-            for cell in line.split(","):
-                v = _stod_full(cell)
-                if v is None:
-                    raise RuntimeError(f"line {line_no}: field '{cell}' is not a number")
-                fields.append(v)
-            if len(fields) < 2:
-                raise RuntimeError(f"line {line_no}: expected label plus at least one feature")
-            if fields[0] not in (0.0, 1.0):
-                raise RuntimeError(f"line {line_no}: label must be 0 or 1")
-            labels.append(int(fields[0]))
-            features.append(fields[1:])
-            if len(features[0]) != len(features[-1]):
-                raise RuntimeError(f"line {line_no}: row width differs from first row")
-    if not features:
-        raise RuntimeError("dataset has no rows: " + path)
-    return LogisticObjective(features, labels, l2)
-
-
 Objective = Union[QuadraticObjective, GradientObjective, LogisticObjective]
 
 

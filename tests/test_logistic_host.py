@@ -1,6 +1,6 @@
 """Host side of the logistic objective (no GPU): the LogisticObjective
-mirror's constructor checks (objectives.cpp:80-106) and load_csv_dataset
-(objectives.cpp:195-248), written after test_objectives.cpp."""
+mirror's constructor checks (objectives.cpp:80-106), written after
+test_objectives.cpp."""
 import numpy as np
 import pytest
 
@@ -33,23 +33,3 @@ def test_constructor_checks():
         o.set_sample_range(0, 5)
     s = o.shard(1, 3)
     assert s.range == (1, 3) and o.range == (0, 4)
-
-
-def test_load_csv(tmp_path):
-    f = tmp_path / "d.csv"
-    f.write_text("label,a,b\r\n1, 0.5 ,2\r\n\r\n0,-1,3e-1\n")
-    o = P.load_csv_dataset(str(f), True, 0.2)
-    assert o.labels.tolist() == [1, 0]
-    assert o.features.tolist() == [[0.5, 2.0], [-1.0, 0.3]]
-    cases = {"1,2\n0,x\n": "line 2: field 'x' is not a number",
-             "1,2\n1\n": "line 2: expected label plus at least one feature",
-             "2,1\n": "line 1: label must be 0 or 1",
-             "1,2\n0,1,2\n": "line 2: row width differs from first row",
-             "1,2abc\n": "line 1: field '2abc' is not a number",
-             "\n\n": "dataset has no rows"}
-    for text, msg in cases.items():
-        f.write_text(text)
-        with pytest.raises(RuntimeError, match=msg):
-            P.load_csv_dataset(str(f), False, 0.1)
-    with pytest.raises(RuntimeError, match="cannot open dataset"):
-        P.load_csv_dataset(str(tmp_path / "missing.csv"), False, 0.1)
