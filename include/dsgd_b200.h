@@ -345,6 +345,24 @@ dsgd_status dsgd_run_events(dsgd_ctx* ctx, const dsgd_run_desc* run, uint64_t ev
  * blobs out of band (e.g. torch.distributed all_gather) and connects. */
 dsgd_status dsgd_ctx_export_handle(dsgd_ctx* ctx, void* blob /* DSGD_HANDLE_BYTES */);
 dsgd_status dsgd_ctx_connect_peers(dsgd_ctx* ctx, const void* blobs /* p blobs */);
+/* In-process group: p one-node contexts (rank r on devices[r], or all on
+ * base->device when devices == NULL) created and wired to each other by raw
+ * device pointers in this process -- no IPC, no second process.  The host
+ * issues every round in node order (rank 0..p-1; the two-shot all-reduce's
+ * reduce kernels after every rank's exchange kernel), so every cross-rank
+ * flag wait is already satisfied when a kernel starts.  Ranks on one GPU
+ * share one stream: the multi-GPU kernels (ring-order all-reduce, EASGD
+ * chain, peer-read gossip) then run -- and can be checked -- on a single
+ * GPU; ranks on distinct GPUs run over NVLink exactly as with one process
+ * per GPU (the shape a single-process profiler capture needs).  out: p
+ * contexts in node order (destroy each).  Same-GPU ranks use a 5 s flag
+ * timeout. */
+dsgd_status dsgd_group_create_inproc(const dsgd_ctx_desc* base, uint32_t p, const int* devices,
+                                     dsgd_ctx** out);
+/* dsgd_run_rounds over an in-process group: round r of every rank, in node
+ * order, then round r+1 (runs: one descriptor per rank, same protocol and
+ * round count). */
+dsgd_status dsgd_group_run_rounds(dsgd_ctx* const* ctxs, uint32_t n, const dsgd_run_desc* runs);
 /* NVLS (in-switch) all-reduce: `x` and `avg` are this context's d-element
  * slices of a multicast-mapped (NVSwitch multicast object) allocation and
  * `x_mc` / `avg_mc` their multicast addresses (e.g. from

@@ -242,8 +242,11 @@ class Stream:
     def normal(self) -> float:
         return lib().dsgdo_normal(self._buf)
 
-    def normals(self, n: int) -> np.ndarray:
-        return np.array([self.normal() for _ in range(n)], dtype=np.float64)
+    def normals(self, n: int, sigma: float = 1.0) -> np.ndarray:
+        """sigma * normal(), n draws (NoiseModel::sample objectives.cpp:175-183)."""
+        out = np.empty(n, dtype=np.float64)
+        lib().dsgdo_fill_normal(self._buf, C.c_double(sigma), _ptr(out), C.c_uint64(n))
+        return out
 
     def exponential(self, rate: float) -> float:
         return lib().dsgdo_exponential(self._buf, rate)
@@ -615,7 +618,7 @@ def run_transport_allreduce(cfg: SimConfig, dtype=np.float64) -> "Nodes":
     for _ in range(cfg.rounds):
         noise = None
         if cfg.sigma is not None:
-            noise = np.array([[cfg.sigma * s.normal() for _ in range(d)] for s in streams]).astype(dtype)
+            noise = np.array([s.normals(d, cfg.sigma) for s in streams]).astype(dtype)
         deltas = np.zeros((p, d), dtype=dtype)
         for i in range(p):
             m = Nodes(n.theta[i:i + 1], n.dprev[i:i + 1], n.t[i:i + 1], dtype=dtype)

@@ -63,6 +63,11 @@ double dsgdo_normal(dsgdo_rng* r) {
   return rad * cos(2.0 * kPi * u2);
 }
 
+/* NoiseModel::sample objectives.cpp:175-183: out[k] = sigma * normal(), k = 0..n-1 */
+void dsgdo_fill_normal(dsgdo_rng* r, double sigma, double* out, uint64_t n) {
+  for (uint64_t k = 0; k < n; ++k) out[k] = sigma * dsgdo_normal(r);
+}
+
 /* rng.cpp:64-70 */
 double dsgdo_exponential(dsgdo_rng* r, double rate) { return -log(dsgdo_uniform01(r)) / rate; }
 

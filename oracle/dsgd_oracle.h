@@ -46,6 +46,7 @@ uint64_t dsgdo_rng_next(dsgdo_rng* r);
 double dsgdo_uniform01(dsgdo_rng* r);
 double dsgdo_normal(dsgdo_rng* r);
 double dsgdo_exponential(dsgdo_rng* r, double rate);
+void dsgdo_fill_normal(dsgdo_rng* r, double sigma, double* out, uint64_t n);
 uint32_t dsgdo_uniform_index(dsgdo_rng* r, uint32_t n);
 uint64_t dsgdo_derive_stream_seed(uint64_t root_seed, const char* run_id,
                                   uint32_t node_id, int purpose);

@@ -136,6 +136,9 @@ _SIGS = {
     "dsgd_ctx_round": (C.c_int, [_P, _U64P]),
     "dsgd_ctx_export_handle": (C.c_int, [_P, _P]),
     "dsgd_ctx_connect_peers": (C.c_int, [_P, _P]),
+    "dsgd_group_create_inproc": (C.c_int, [C.POINTER(CtxDesc), C.c_uint32, C.POINTER(C.c_int),
+                                           C.POINTER(_P)]),
+    "dsgd_group_run_rounds": (C.c_int, [C.POINTER(_P), C.c_uint32, C.POINTER(RunDesc)]),
     "dsgd_nccl_unique_id": (C.c_int, [_P]),
     "dsgd_ctx_attach_multicast": (C.c_int, [_P, _P, _P, _P, _P]),
     "dsgd_ctx_init_nccl": (C.c_int, [_P, _P, C.c_int, C.c_int]),

@@ -60,7 +60,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
         failed = [cmd for cmd, p in procs if p.wait() != 0]
         if failed:
             raise subprocess.CalledProcessError(1, failed[0])
-        link = [NVCC, *ARCH, "-shared", *objs, "-o", SO + ".tmp", "-lnccl", "-lcuda"]
+        # host linker: no device-link step (no relocatable device code), so
+        # each object's cubin is embedded once
+        cuda = os.path.dirname(os.path.dirname(os.path.realpath(NVCC)))
+        link = ["g++", "-shared", *objs, "-o", SO + ".tmp", "-L" + os.path.join(cuda, "lib64"),
+                "-lcudart_static", "-lnccl", "-lcuda", "-ldl", "-lrt", "-lpthread"]
         subprocess.run(link, check=True)
     os.replace(SO + ".tmp", SO)
     return SO

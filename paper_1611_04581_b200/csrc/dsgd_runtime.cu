@@ -126,6 +126,24 @@ struct DeviceGuard {
   }
 };
 
+// One-node contexts of one process wired to each other by raw device
+// pointers (dsgd_group_create_inproc): the ranks' launches are issued in host
+// order (rank 0..p-1 per round, two-shot reduces after every rank's
+// exchange), so every cross-rank wait is already satisfied when a kernel
+// starts.  Ranks on one GPU share one stream, which makes the multi-GPU
+// kernels executable -- and checkable -- on a single GPU.
+struct InprocGroup {
+  std::vector<dsgd_ctx*> ctx;                         // node order
+  std::vector<std::pair<int, cudaStream_t>> streams;  // one per device, owned
+  ~InprocGroup() {
+    for (auto& s : streams) {
+      DeviceGuard g(s.first);
+      cudaStreamSynchronize(s.second);
+      cudaStreamDestroy(s.second);
+    }
+  }
+};
+
 }  // namespace
 
 struct dsgd_ctx {
@@ -199,6 +217,8 @@ struct dsgd_ctx {
   unsigned long long timeout_ns = 30ull * 1000 * 1000 * 1000;
 
   // multi-GPU
+  std::shared_ptr<InprocGroup> grp;  // in-process group (null: one process per GPU)
+  unsigned long long reduce_t = 0;   // in-process two-shot: round of the deferred reduces
   bool connected = false;
   std::vector<PeerNode> peers;   // all p nodes
   std::vector<void*> ipc_opened;
@@ -868,6 +888,64 @@ dsgd_status flush_pending(dsgd_ctx* c) {
   return c->dtype == DSGD_F32 ? flush_pending_t<float>(c) : flush_pending_t<double>(c);
 }
 
+// Second kernel of pipeline `pi` of a two-shot round t: reduce this rank's
+// slice of every rank's exchange buffer and write the average to every rank
+// (NVLS multimem, or peer memory in the reference ring order).
+template <typename T>
+dsgd_status launch_reduce_pipe(dsgd_ctx* c, uint32_t pi, uint32_t K, unsigned long long t) {
+  const uint32_t me = c->first;
+  cudaStream_t st = K > 1 ? c->pipe_stream[pi] : c->stream;
+  const uint64_t b0 = (c->d * pi / K) / 64 * 64;
+  const uint64_t b1 = pi + 1 == K ? c->d : (c->d * (pi + 1) / K) / 64 * 64;
+  const uint64_t len = b1 - b0;
+  unsigned int* arrive = c->arrive + 40 + pi;
+  dsgd::WaitSpec wx{};
+  wx.timeout_ns = c->timeout_ns;
+  wx.error = c->error;
+  for (uint32_t k = 0; k < c->p; ++k) {  // every rank's exchange of this pipeline is written
+    wx.ptr[wx.n] = c->peers[k].ar + 2 * pi;
+    wx.val[wx.n] = t + 1;
+    wx.n++;
+  }
+  dsgd::SignalSpec sx{c->peers[me].ar + 2 * pi + 1, t + 1, arrive, nullptr};
+  trace_slot(c, DSGD_K_NCCL + 16 * pi, &wx, &sx);
+  if (c->ar_nvls) {
+    dsgd::ArNvlsArgs<T> a{};
+    a.x_mc = as<T>(c->nvls_x_mc);
+    a.avg_mc = as<T>(c->nvls_avg_mc);
+    const uint64_t per = ((len + c->p - 1) / c->p + 3) / 4 * 4;
+    a.lo = std::min<uint64_t>(b1, b0 + (uint64_t)me * per);
+    a.hi = std::min<uint64_t>(b1, a.lo + per);
+    a.p = c->p;
+    a.wait = wx;
+    a.signal = sx;
+    const uint32_t cap = std::max<uint32_t>(1, (uint32_t)(c->sm_count * c->ar_comm_frac / K));
+    const uint32_t grid = std::min<uint32_t>(cap, std::max<uint32_t>(1, (uint32_t)((a.hi - a.lo) / 4 / kBlockU + 1)));
+    LaunchScope ls(c, DSGD_K_NCCL, st);
+    DSGD_CUDA(dsgd::launch_ar_nvls<T>(a, grid, st));
+  } else {
+    dsgd::ArReduceArgs<T> a{};
+    for (uint32_t k = 0; k < c->p; ++k) {
+      a.x[k] = as<T>(c->peers[k].x);
+      a.avg[k] = as<T>(c->peers[k].avg);
+    }
+    a.p = c->p;
+    a.slice = me;
+    const uint64_t base = c->d / c->p, rem = c->d % c->p;  // transport.cpp:193-198
+    const uint64_t clo = (uint64_t)me * base + std::min<uint64_t>(me, rem);
+    const uint64_t chi = clo + base + (me < rem ? 1 : 0);
+    a.lo = std::max(clo, b0);  // my ring chunk within this pipeline's range
+    a.hi = std::max(a.lo, std::min(chi, b1));
+    a.wait = wx;
+    a.signal = sx;
+    const uint32_t grid =
+        std::max<uint32_t>(1, blocks_for(c, (a.hi - a.lo) / (16 / sizeof(T)) + 1, 1) / K);
+    LaunchScope ls(c, DSGD_K_NCCL, st);
+    DSGD_CUDA(dsgd::launch_ar_reduce<T>(a, grid, st));
+  }
+  return DSGD_OK;
+}
+
 // Multi-GPU all-reduce round over NVLink peer memory, two kernels:
 //  1. fused (previous apply +) delta kernel -> own exchange buffer x
 //     [waits: every rank's averages of the previous round are written]
@@ -980,50 +1058,18 @@ dsgd_status do_allreduce_p2p(dsgd_ctx* c, const dsgd_hyperparams* h, const GradS
       DSGD_CUDA(cudaEventRecord(c->pipe_event[5 + pi], st));
       DSGD_CUDA(cudaStreamWaitEvent(c->stream, c->pipe_event[5 + pi], 0));
     }
-    dsgd::WaitSpec wx{};
-    wx.timeout_ns = c->timeout_ns;
-    wx.error = c->error;
-    for (uint32_t k = 0; k < c->p; ++k) {  // every rank's exchange of this pipeline is written
-      wx.ptr[wx.n] = c->peers[k].ar + 2 * pi;
-      wx.val[wx.n] = t + 1;
-      wx.n++;
-    }
-    dsgd::SignalSpec sx{c->peers[me].ar + 2 * pi + 1, t + 1, arrive, nullptr};
-    trace_slot(c, DSGD_K_NCCL + 16 * pi, &wx, &sx);
-    if (c->ar_nvls) {
-      dsgd::ArNvlsArgs<T> a{};
-      a.x_mc = as<T>(c->nvls_x_mc);
-      a.avg_mc = as<T>(c->nvls_avg_mc);
-      const uint64_t per = ((len + c->p - 1) / c->p + 3) / 4 * 4;
-      a.lo = std::min<uint64_t>(b1, b0 + (uint64_t)me * per);
-      a.hi = std::min<uint64_t>(b1, a.lo + per);
-      a.p = c->p;
-      a.wait = wx;
-      a.signal = sx;
-      const uint32_t cap = std::max<uint32_t>(1, (uint32_t)(c->sm_count * c->ar_comm_frac / K));
-      const uint32_t grid = std::min<uint32_t>(cap, std::max<uint32_t>(1, (uint32_t)((a.hi - a.lo) / 4 / kBlockU + 1)));
-      LaunchScope ls(c, DSGD_K_NCCL, st);
-      DSGD_CUDA(dsgd::launch_ar_nvls<T>(a, grid, st));
-    } else {
-      dsgd::ArReduceArgs<T> a{};
-      for (uint32_t k = 0; k < c->p; ++k) {
-        a.x[k] = as<T>(c->peers[k].x);
-        a.avg[k] = as<T>(c->peers[k].avg);
+    if (!c->grp) DSGD_TRY(launch_reduce_pipe<T>(c, pi, K, t));
+  }
+  if (c->grp) {
+    // in-process group: every rank's exchange kernels are issued before any
+    // reduce (host order satisfies every cross-rank wait: the ranks of one
+    // GPU share a stream); the last rank issues the reduces of all ranks
+    c->reduce_t = t;
+    if (c->first + 1 == c->p)
+      for (dsgd_ctx* r : c->grp->ctx) {
+        DeviceGuard dg(r->device);
+        for (uint32_t q = 0; q < K; ++q) DSGD_TRY(launch_reduce_pipe<T>(r, q, K, r->reduce_t));
       }
-      a.p = c->p;
-      a.slice = me;
-      const uint64_t base = c->d / c->p, rem = c->d % c->p;  // transport.cpp:193-198
-      const uint64_t clo = (uint64_t)me * base + std::min<uint64_t>(me, rem);
-      const uint64_t chi = clo + base + (me < rem ? 1 : 0);
-      a.lo = std::max(clo, b0);  // my ring chunk within this pipeline's range
-      a.hi = std::max(a.lo, std::min(chi, b1));
-      a.wait = wx;
-      a.signal = sx;
-      const uint32_t grid =
-          std::max<uint32_t>(1, blocks_for(c, (a.hi - a.lo) / (16 / sizeof(T)) + 1, 1) / K);
-      LaunchScope ls(c, DSGD_K_NCCL, st);
-      DSGD_CUDA(dsgd::launch_ar_reduce<T>(a, grid, st));
-    }
   }
   if (fused) c->cur ^= 1;
   c->ar_rounds = t + 1;
@@ -1264,6 +1310,8 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
     return set_error(DSGD_EINVAL, "bad node layout (p, first_node, n_local)");
   if (desc->n_local != desc->p && desc->n_local != 1)
     return set_error(DSGD_EINVAL, "a context hosts all p nodes or exactly one");
+  if (desc->n_local < desc->p && desc->p > (uint32_t)kMaxWait)
+    return set_error(DSGD_EINVAL, "one node per context supports p <= 16");
   if (desc->dtype != DSGD_F32 && desc->dtype != DSGD_F64) return set_error(DSGD_EINVAL, "dtype");
   auto c = std::make_unique<dsgd_ctx>();
   c->device = desc->device;
@@ -1436,7 +1484,7 @@ void dsgd_ctx_destroy(dsgd_ctx* c) {
   }
   for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
   for (int h = 0; h < 4; ++h)
-    if (c->pipe_stream[h]) {
+    if (c->pipe_stream[h] && c->pipe_stream[h] != c->stream) {
       cudaStreamSynchronize(c->pipe_stream[h]);
       cudaStreamDestroy(c->pipe_stream[h]);
     }
@@ -2108,7 +2156,9 @@ dsgd_status dsgd_ctx_round(dsgd_ctx* c, uint64_t* round) {
   return DSGD_OK;
 }
 
-dsgd_status dsgd_run_rounds(dsgd_ctx* c, const dsgd_run_desc* run) {
+namespace {
+
+dsgd_status run_check(dsgd_ctx* c, const dsgd_run_desc* run) {
   DSGD_TRY(check_ctx(c));
   if (!run) return set_error(DSGD_EINVAL, "null run descriptor");
   DSGD_TRY(dsgd_hyperparams_validate(&run->hyper));
@@ -2118,71 +2168,96 @@ dsgd_status dsgd_run_rounds(dsgd_ctx* c, const dsgd_run_desc* run) {
   if (needs_partners && c->partner_streams.size() != c->p)
     return set_error(DSGD_ESTATE, "dsgd_ctx_seed_streams first");
   if (proto == DSGD_ASYNC_PULL) return set_error(DSGD_EINVAL, "async-pull is event-driven");
+  if (proto > DSGD_ASYNC_PULL) return set_error(DSGD_EINVAL, "unknown protocol");
   if (run->host_noise_sigma > 0.0) {
     if (!c->noise[0]) return set_error(DSGD_ESTATE, "host noise needs DSGD_CTX_NOISE");
     if (c->noise_streams.size() != c->n_local)
       return set_error(DSGD_ESTATE, "dsgd_ctx_seed_streams first");
     if (!c->noise_host) c->noise_host = new double[c->d];
   }
+  return DSGD_OK;
+}
+
+// One round of run_sync's loop (simulator.cpp:234-369) on one context.
+dsgd_status run_one_round(dsgd_ctx* c, const dsgd_run_desc* run) {
+  const dsgd_protocol proto = run->protocol;
   const dsgd_hyperparams* h = &run->hyper;
   std::vector<uint32_t> map(c->p);
-  std::vector<const void*> grads(c->n_local);
-  for (uint64_t r = 0; r < run->rounds; ++r) {
-    const uint64_t t = c->t[0];
-    const bool gated = t > 0 && t % h->tau == 0;  // simulator.cpp:25
-    dsgd_grad_spec g = run->grad;
-    if (run->n_grad_pool > 0) {
-      const uint64_t slot = c->rounds_done % run->n_grad_pool;
-      for (uint32_t i = 0; i < c->n_local; ++i) grads[i] = run->grad_pool[slot * c->n_local + i];
-      g.source = DSGD_GRAD_BUFFER;
-      g.grad = grads.data();
-    }
-    if (run->host_noise_sigma > 0.0) {
-      // NoiseModel::sample on each local node's reference noise stream
-      for (uint32_t i = 0; i < c->n_local; ++i) {
-        dsgd_stream_fill_normal(c->noise_streams[i], run->host_noise_sigma, c->noise_host, c->d);
-        DSGD_TRY(dsgd_set_vector(c, i, DSGD_BUF_NOISE, c->noise_host));
-      }
-      g.use_noise = 1;
-    }
-    dsgd_status st = DSGD_OK;
-    switch (proto) {
-      case DSGD_ALLREDUCE:
-        st = dsgd_allreduce_round(c, h, &g, run->scope);
-        break;
-      case DSGD_ELASTIC_AVG:
-        st = dsgd_ea_round(c, h, &g, gated ? 1 : 0);
-        break;
-      case DSGD_PULL_GOSSIP:
-      case DSGD_GOSSIP_STALE:
-      case DSGD_GOSSIP_FRESH:
-        if (gated) {
-          DSGD_TRY(dsgd_draw_pull_partners(c->partner_streams.data(), c->p, map.data()));
-          st = proto == DSGD_PULL_GOSSIP    ? dsgd_pull_gossip_round(c, h, &g, map.data())
-               : proto == DSGD_GOSSIP_STALE ? dsgd_gossip_stale_round(c, h, &g, map.data())
-                                            : dsgd_gossip_fresh_round(c, h, &g, map.data());
-        } else {
-          st = dsgd_pull_gossip_round(c, h, &g, nullptr);
-        }
-        break;
-      case DSGD_PUSH_GOSSIP:
-        if (gated && c->p > 1) {
-          DSGD_TRY(dsgd_draw_push_targets(c->partner_streams.data(), c->p, map.data()));
-          st = dsgd_push_gossip_round(c, h, &g, map.data());
-        } else {
-          st = dsgd_pull_gossip_round(c, h, &g, nullptr);
-        }
-        break;
-      default:
-        return set_error(DSGD_EINVAL, "unknown protocol");
-    }
-    if (st != DSGD_OK) return st;
+  const void* grads[kMaxLocal];
+  const uint64_t t = c->t[0];
+  const bool gated = t > 0 && t % h->tau == 0;  // simulator.cpp:25
+  dsgd_grad_spec g = run->grad;
+  if (run->n_grad_pool > 0) {
+    const uint64_t slot = c->rounds_done % run->n_grad_pool;
+    for (uint32_t i = 0; i < c->n_local; ++i) grads[i] = run->grad_pool[slot * c->n_local + i];
+    g.source = DSGD_GRAD_BUFFER;
+    g.grad = grads;
   }
-  // leave the context in its logical state (the timed work of `rounds`
-  // rounds includes the last deferred apply)
+  if (run->host_noise_sigma > 0.0) {
+    // NoiseModel::sample on each local node's reference noise stream
+    for (uint32_t i = 0; i < c->n_local; ++i) {
+      dsgd_stream_fill_normal(c->noise_streams[i], run->host_noise_sigma, c->noise_host, c->d);
+      DSGD_TRY(dsgd_set_vector(c, i, DSGD_BUF_NOISE, c->noise_host));
+    }
+    g.use_noise = 1;
+  }
+  switch (proto) {
+    case DSGD_ALLREDUCE:
+      return dsgd_allreduce_round(c, h, &g, run->scope);
+    case DSGD_ELASTIC_AVG:
+      return dsgd_ea_round(c, h, &g, gated ? 1 : 0);
+    case DSGD_PULL_GOSSIP:
+    case DSGD_GOSSIP_STALE:
+    case DSGD_GOSSIP_FRESH:
+      if (!gated) return dsgd_pull_gossip_round(c, h, &g, nullptr);
+      DSGD_TRY(dsgd_draw_pull_partners(c->partner_streams.data(), c->p, map.data()));
+      return proto == DSGD_PULL_GOSSIP    ? dsgd_pull_gossip_round(c, h, &g, map.data())
+             : proto == DSGD_GOSSIP_STALE ? dsgd_gossip_stale_round(c, h, &g, map.data())
+                                          : dsgd_gossip_fresh_round(c, h, &g, map.data());
+    case DSGD_PUSH_GOSSIP:
+      if (!(gated && c->p > 1)) return dsgd_pull_gossip_round(c, h, &g, nullptr);
+      DSGD_TRY(dsgd_draw_push_targets(c->partner_streams.data(), c->p, map.data()));
+      return dsgd_push_gossip_round(c, h, &g, map.data());
+    default:
+      return set_error(DSGD_EINVAL, "unknown protocol");
+  }
+}
+
+// Leaves the context in its logical state (the timed work of `rounds`
+// rounds includes the last deferred apply) and settles grad_norm_out: one
+// host read per run, not per round.
+dsgd_status run_finish(dsgd_ctx* c) {
   DSGD_TRY(flush_pending(c));
   DeviceGuard dg(c->device);
-  return norm_read(c);  // grad_norm_out: one host read per run, not per round
+  return norm_read(c);
+}
+
+}  // namespace
+
+dsgd_status dsgd_run_rounds(dsgd_ctx* c, const dsgd_run_desc* run) {
+  DSGD_TRY(run_check(c, run));
+  if (c->grp && c->p > 1)
+    return set_error(DSGD_EINVAL, "in-process group: use dsgd_group_run_rounds");
+  for (uint64_t r = 0; r < run->rounds; ++r) DSGD_TRY(run_one_round(c, run));
+  return run_finish(c);
+}
+
+dsgd_status dsgd_group_run_rounds(dsgd_ctx* const* ctxs, uint32_t n, const dsgd_run_desc* runs) {
+  if (!ctxs || !runs || n == 0) return set_error(DSGD_EINVAL, "null group");
+  for (uint32_t k = 0; k < n; ++k) {
+    DSGD_TRY(run_check(ctxs[k], &runs[k]));
+    if (!ctxs[k]->grp || ctxs[k]->grp->ctx.size() != n || ctxs[k]->grp->ctx[k] != ctxs[k])
+      return set_error(DSGD_EINVAL, "contexts must be one in-process group in node order");
+    if (runs[k].rounds != runs[0].rounds || runs[k].protocol != runs[0].protocol)
+      return set_error(DSGD_EINVAL, "every rank runs the same rounds and protocol");
+  }
+  for (uint64_t r = 0; r < runs[0].rounds; ++r)
+    for (uint32_t k = 0; k < n; ++k) {  // host order = rank order inside every round
+      DeviceGuard dg(ctxs[k]->device);
+      DSGD_TRY(run_one_round(ctxs[k], &runs[k]));
+    }
+  for (uint32_t k = 0; k < n; ++k) DSGD_TRY(run_finish(ctxs[k]));
+  return DSGD_OK;
 }
 
 // -------------------------------------------------------- multi-GPU wiring
@@ -2266,6 +2341,83 @@ dsgd_status dsgd_ctx_connect_peers(dsgd_ctx* c, const void* blobs) {
     }
   }
   c->connected = true;
+  return DSGD_OK;
+}
+
+dsgd_status dsgd_group_create_inproc(const dsgd_ctx_desc* base, uint32_t p, const int* devices,
+                                     dsgd_ctx** out) {
+  if (!base || !out) return set_error(DSGD_EINVAL, "null argument");
+  if (p == 0 || p > (uint32_t)kMaxWait) return set_error(DSGD_EINVAL, "in-process group: 1 <= p <= 16");
+  auto grp = std::make_shared<InprocGroup>();
+  std::vector<int> dev(p);
+  for (uint32_t r = 0; r < p; ++r) dev[r] = devices ? devices[r] : base->device;
+  auto stream_of = [&](int d, cudaStream_t* s) -> dsgd_status {
+    for (auto& e : grp->streams)
+      if (e.first == d) {
+        *s = e.second;
+        return DSGD_OK;
+      }
+    DeviceGuard g(d);
+    DSGD_CUDA(cudaSetDevice(d));
+    cudaStream_t ns = nullptr;
+    DSGD_CUDA(cudaStreamCreateWithFlags(&ns, cudaStreamNonBlocking));
+    grp->streams.emplace_back(d, ns);
+    *s = ns;
+    return DSGD_OK;
+  };
+  auto fail = [&](dsgd_status st) {
+    const std::string msg = dsgd::g_error;
+    for (dsgd_ctx* c : grp->ctx) dsgd_ctx_destroy(c);
+    grp->ctx.clear();
+    return set_error(st, msg);
+  };
+  for (uint32_t r = 0; r < p; ++r) {
+    dsgd_ctx_desc d = *base;
+    d.device = dev[r];
+    d.p = p;
+    d.first_node = r;
+    d.n_local = 1;
+    cudaStream_t s = nullptr;
+    dsgd_status st = stream_of(dev[r], &s);
+    if (st != DSGD_OK) return fail(st);
+    d.stream = s;
+    dsgd_ctx* c = nullptr;
+    st = dsgd_ctx_create(&d, &c);
+    if (st != DSGD_OK) return fail(st);
+    grp->ctx.push_back(c);
+  }
+  for (uint32_t r = 0; r < p; ++r) {
+    dsgd_ctx* c = grp->ctx[r];
+    DeviceGuard g(c->device);
+    const bool shared = std::count(dev.begin(), dev.end(), c->device) > 1;
+    if (shared) {
+      // ranks of one GPU: one stream, no pipeline streams (nothing of two
+      // ranks may run concurrently on one device), and a short flag timeout
+      // (a wait host order cannot satisfy never will be)
+      for (int h = 0; h < 4; ++h) {
+        if (c->pipe_stream[h] && c->pipe_stream[h] != c->stream) cudaStreamDestroy(c->pipe_stream[h]);
+        c->pipe_stream[h] = c->stream;
+      }
+      c->timeout_ns = 5ull * 1000 * 1000 * 1000;
+    }
+    for (uint32_t k = 0; k < p; ++k) {
+      if (k == r) continue;
+      dsgd_ctx* o = grp->ctx[k];
+      if (o->device != c->device) {
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, c->device, o->device);
+        if (!can) return fail(set_error(DSGD_ECUDA, "no peer access between the group's GPUs"));
+        cudaError_t e = cudaDeviceEnablePeerAccess(o->device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+          return fail(set_error(DSGD_ECUDA, std::string("enable peer access: ") + cudaGetErrorString(e)));
+        cudaGetLastError();
+      }
+      c->peers[k] = o->peers[k];  // the owner's own view of its arena
+    }
+    c->connected = true;
+    c->grp = grp;
+  }
+  for (uint32_t r = 0; r < p; ++r) out[r] = grp->ctx[r];
   return DSGD_OK;
 }
 

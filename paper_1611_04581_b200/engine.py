@@ -157,6 +157,34 @@ class Group:
         self.device = device
         self._norm = C.c_double(0.0)
 
+    @classmethod
+    def inproc(cls, d: int, p: int, dtype="f32", devices: Optional[Sequence[int]] = None,
+               device: int = 0, quadratic: bool = False, grad: bool = False,
+               noise: bool = False, center: bool = False) -> list:
+        """dsgd_group_create_inproc: p one-node contexts of this process wired
+        by raw device pointers (rank r on devices[r], or all on `device`).
+        Drive them in node order every round (``run_rounds_inproc`` does)."""
+        lib = N.load()
+        flags = ((N.CTX_QUADRATIC if quadratic else 0) | (N.CTX_GRAD if grad else 0) |
+                 (N.CTX_NOISE if noise else 0) | (N.CTX_CENTER if center else 0))
+        desc = N.CtxDesc(device, int(d), DTYPES[dtype], p, 0, 1, flags, None)
+        out = (C.c_void_p * p)()
+        devs = (C.c_int * p)(*(devices if devices is not None else [device] * p))
+        N.check(lib.dsgd_group_create_inproc(C.byref(desc), p, devs, out))
+        groups = []
+        for r in range(p):
+            g = cls.__new__(cls)
+            g.lib = lib
+            g.d, g.p = int(d), int(p)
+            g.dtype = DTYPES[dtype]
+            g.np_dtype = NP_OF[g.dtype]
+            g.first, g.n_local, g.flags = r, 1, flags
+            g.device = devs[r]
+            g._ctx = C.c_void_p(out[r])
+            g._norm = C.c_double(0.0)
+            groups.append(g)
+        return groups
+
     # ------------------------------------------------------------ lifetime
     def close(self) -> None:
         if self._ctx:
@@ -395,6 +423,20 @@ class Group:
         rd._keep = (gs, pool)
         N.check(self.lib.dsgd_run_rounds(self._ctx, C.byref(rd)))
 
+    def _run_desc(self, protocol: int, h: Hyperparams, rounds: int, scope: str, grad,
+                  grad_pool, host_noise_sigma: float, noise: bool):
+        gs = self._grad(grad, noise, False)
+        pool = None
+        if grad_pool:
+            pool = (C.c_void_p * len(grad_pool))(*grad_pool)
+        rd = N.RunDesc(protocol, h.to_c(), N.SCOPE_PER_NODE if scope == "per-node"
+                       else N.SCOPE_AGGREGATE, gs,
+                       (len(grad_pool) // self.n_local) if grad_pool else 0,
+                       C.cast(pool, C.POINTER(C.c_void_p)) if pool else None,
+                       host_noise_sigma, rounds)
+        rd._keep = (gs, pool)
+        return rd
+
     def run_events(self, protocol: int, h: Hyperparams, events: int, rate_per_node: float,
                    grad=None, host_noise_sigma: float = 0.0, sim_time: float = 0.0,
                    alpha: float = 0.0):
@@ -535,3 +577,17 @@ def broadcast_nccl_id(rank: int, world: int, make=None) -> bytes:
     if world > 1:
         dist.broadcast_object_list(uid, src=0)
     return uid[0]
+
+
+def run_rounds_inproc(groups: Sequence[Group], protocol: int, h: Hyperparams, rounds: int,
+                      scope: str = "aggregate", grad=None, grad_pools=None,
+                      host_noise_sigma: float = 0.0, noise: bool = False) -> None:
+    """dsgd_group_run_rounds: run_sync's round loop over an in-process group
+    (every rank's round r in node order, then round r+1)."""
+    n = len(groups)
+    descs = [g._run_desc(protocol, h, rounds, scope, grad,
+                         grad_pools[i] if grad_pools else None, host_noise_sigma, noise)
+             for i, g in enumerate(groups)]
+    arr = (N.RunDesc * n)(*descs)
+    ctxs = (C.c_void_p * n)(*[g._ctx.value for g in groups])
+    N.check(N.load().dsgd_group_run_rounds(ctxs, n, arr))
