@@ -277,14 +277,24 @@ dsgd_status dsgd_gossip_fresh_round(dsgd_ctx* ctx, const dsgd_hyperparams* h,
 /* async_pull_event protocols.cpp:278-297 (nodes i, j global ids; one context) */
 dsgd_status dsgd_async_pull_event(dsgd_ctx* ctx, const dsgd_hyperparams* h,
                                   const dsgd_grad_spec* g, uint32_t i, uint32_t j);
+/* gossip_stale_step protocols.cpp:252-263 for ONE local node of a single
+ * context against an arbitrary device vector `partner` (dtype elements, d):
+ * delta' = compute_local_delta(theta_i); theta_i = mix_toward(theta_i,
+ * partner, beta_gossip) + delta'; in place, t_i += 1.  (The reference's
+ * single-node signature; simulator.cpp:283-292 calls it per node.) */
+dsgd_status dsgd_gossip_stale_step(dsgd_ctx* ctx, const dsgd_hyperparams* h,
+                                   const dsgd_grad_spec* g, uint32_t local, const void* partner);
+/* mix_toward protocols.cpp:42-51 for ONE local node, in place:
+ * theta_i += beta * (partner - theta_i) (gossip_fresh_mix 265-269). */
+dsgd_status dsgd_mix_toward(dsgd_ctx* ctx, uint32_t local, const void* partner, double beta);
 /* pull_mix 161-171 / push_mix 195-228 without the SGD step */
 dsgd_status dsgd_pull_mix(dsgd_ctx* ctx, const uint32_t* partner_of);
 dsgd_status dsgd_push_mix(dsgd_ctx* ctx, const uint32_t* target_of);
 /* gossip_fresh_mix protocols.cpp:265-269 (mix_toward with beta, no step) */
 dsgd_status dsgd_gossip_fresh_mix(dsgd_ctx* ctx, const uint32_t* partner_of, double beta);
 /* ea_client_step's update output: when update_out != NULL (n_local device
- * pointers), the next dsgd_ea_round on a single context also writes each
- * client's update u_i = beta*(theta_i - c) there. */
+ * pointers), dsgd_ea_round / dsgd_ea_client_event on a single context also
+ * write each client's update u_i = beta*(theta_i - c) there. */
 dsgd_status dsgd_ea_set_update_out(dsgd_ctx* ctx, void* const* update_out);
 /* ea_server_apply protocols.cpp:155-159: center += update (device vector) */
 dsgd_status dsgd_ea_server_apply(dsgd_ctx* ctx, const void* update);

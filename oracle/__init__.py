@@ -13,6 +13,7 @@ Only tests/, ``__graft_entry__.smoke()`` and bench.py's ``cpu_baseline`` /
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import os
 import subprocess
@@ -188,33 +189,51 @@ def ref():
     if _ref is None:
         if not ref_available():
             raise RuntimeError("oracle/_ref/libdsgd_ref.so not built (needs /root/reference)")
-        _ref = C.CDLL(REF_SO)
-        _ref.ref_last_error.restype = C.c_char_p
-        _ref.ref_derive_stream_seed.restype = C.c_uint64
-        _ref.ref_derive_stream_seed.argtypes = [C.c_uint64, C.c_char_p, C.c_uint32, C.c_int]
-        _ref.ref_stream_draws.argtypes = [C.c_uint64, C.c_int, C.c_uint32, C.c_uint64, C.c_void_p]
-        _ref.ref_run.argtypes = [C.POINTER(Sim), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
-        _ref.ref_run_transport.argtypes = [C.POINTER(Sim), C.c_void_p, C.c_void_p, C.c_void_p,
-                                           C.c_void_p, C.c_uint64]
-        _ref.ref_round.argtypes = [C.c_int, C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p,
-                                   C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
-                                   C.c_void_p, C.c_int, C.c_double, C.c_uint64, C.c_char_p,
-                                   C.POINTER(Hyper), C.c_int, C.c_void_p, C.c_int,
-                                   C.c_uint32, C.c_uint32]
-        _ref.ref_ring_allreduce.argtypes = [C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p,
-                                            C.c_uint64]
-        _ref.ref_set_logistic.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64,
-                                          C.c_double, C.c_void_p, C.c_uint32]
-        _ref.ref_logistic_grad.argtypes = [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint64,
-                                           C.c_uint64, C.c_uint64, C.c_void_p]
-        _ref.ref_logistic_value.restype = C.c_double
-        _ref.ref_logistic_value.argtypes = [C.c_void_p, C.c_uint64]
-        _ref.ref_run_traced.restype = C.c_long
-        _ref.ref_run_traced.argtypes = [C.POINTER(Sim), C.c_uint64, C.c_void_p, C.c_uint64,
-                                        C.c_char_p, C.c_uint64]
-        _ref.ref_time_rounds.restype = C.c_double
-        _ref.ref_time_rounds.argtypes = [C.c_int, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int,
-                                         C.POINTER(Hyper)]
+        _ref = _configure_ref(C.CDLL(REF_SO))
+    return _ref
+
+
+@contextlib.contextmanager
+def ref_library(path: str):
+    """Temporarily route every ref_* helper to another build of the same
+    shim, e.g. integration/_build/libdsgd_ref_b200_harness.so: the UNMODIFIED
+    reference drivers with protocols.cpp replaced by the B200 binding."""
+    global _ref
+    old = _ref
+    _ref = _configure_ref(C.CDLL(path))
+    try:
+        yield _ref
+    finally:
+        _ref = old
+
+
+def _configure_ref(_ref):
+    _ref.ref_last_error.restype = C.c_char_p
+    _ref.ref_derive_stream_seed.restype = C.c_uint64
+    _ref.ref_derive_stream_seed.argtypes = [C.c_uint64, C.c_char_p, C.c_uint32, C.c_int]
+    _ref.ref_stream_draws.argtypes = [C.c_uint64, C.c_int, C.c_uint32, C.c_uint64, C.c_void_p]
+    _ref.ref_run.argtypes = [C.POINTER(Sim), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    _ref.ref_run_transport.argtypes = [C.POINTER(Sim), C.c_void_p, C.c_void_p, C.c_void_p,
+                                       C.c_void_p, C.c_uint64]
+    _ref.ref_round.argtypes = [C.c_int, C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p,
+                               C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                               C.c_void_p, C.c_int, C.c_double, C.c_uint64, C.c_char_p,
+                               C.POINTER(Hyper), C.c_int, C.c_void_p, C.c_int,
+                               C.c_uint32, C.c_uint32]
+    _ref.ref_ring_allreduce.argtypes = [C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p,
+                                        C.c_uint64]
+    _ref.ref_set_logistic.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64,
+                                      C.c_double, C.c_void_p, C.c_uint32]
+    _ref.ref_logistic_grad.argtypes = [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint64,
+                                       C.c_uint64, C.c_uint64, C.c_void_p]
+    _ref.ref_logistic_value.restype = C.c_double
+    _ref.ref_logistic_value.argtypes = [C.c_void_p, C.c_uint64]
+    _ref.ref_run_traced.restype = C.c_long
+    _ref.ref_run_traced.argtypes = [C.POINTER(Sim), C.c_uint64, C.c_void_p, C.c_uint64,
+                                    C.c_char_p, C.c_uint64]
+    _ref.ref_time_rounds.restype = C.c_double
+    _ref.ref_time_rounds.argtypes = [C.c_int, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int,
+                                     C.POINTER(Hyper)]
     return _ref
 
 

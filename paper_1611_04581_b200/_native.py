@@ -120,6 +120,9 @@ _SIGS = {
     "dsgd_gossip_fresh_round": (C.c_int, [_P, C.POINTER(Hyper), C.POINTER(GradSpec), _U32P]),
     "dsgd_async_pull_event": (C.c_int, [_P, C.POINTER(Hyper), C.POINTER(GradSpec), C.c_uint32,
                                         C.c_uint32]),
+    "dsgd_gossip_stale_step": (C.c_int, [_P, C.POINTER(Hyper), C.POINTER(GradSpec), C.c_uint32,
+                                         _P]),
+    "dsgd_mix_toward": (C.c_int, [_P, C.c_uint32, _P, C.c_double]),
     "dsgd_pull_mix": (C.c_int, [_P, _U32P]),
     "dsgd_push_mix": (C.c_int, [_P, _U32P]),
     "dsgd_ea_init_center": (C.c_int, [_P]),

@@ -1295,6 +1295,36 @@ char* buffer_of(dsgd_ctx* c, uint32_t local, dsgd_buffer which) {
   return nullptr;
 }
 
+// One local node, in place, against an arbitrary device vector: the
+// reference's single-node gossip rules (protocols.hpp:124-139).
+template <typename T>
+dsgd_status node_step(dsgd_ctx* c, int mode, const dsgd_hyperparams* h, const GradSel* gs,
+                      uint32_t i, const void* partner, T beta) {
+  dsgd::StepArgs<T> a{};
+  GradSel none;
+  none.quad = 1;
+  const GradSel& g = gs ? *gs : none;
+  fill_node<T>(c, i, g, h, &a.node[0]);
+  a.node[0].theta_out = as<T>(c->theta_ptr(i, c->cur));  // each element read, then written
+  a.node[0].partner = static_cast<const T*>(partner);
+  if (gs) {
+    if (!gs->quad) a.node[0].grad = static_cast<const T*>(gs->grad[i]);
+    if (gs->noise) a.node[0].noise = as<T>(c->noise[i]);
+    a.node[0].norm = gs->norm ? c->norm + (size_t)c->norm_slot * c->n_local : nullptr;
+    fill_common(c, h, *gs, &a);
+  } else {
+    a.d = c->d;
+  }
+  a.beta = beta;
+  a.n_local = 1;
+  const bool vec = aligned16(partner) && (g.quad || aligned16(g.grad[i]));
+  const uint64_t W = vec ? 16 / sizeof(T) : 1;
+  a.blocks_per_node = blocks_for(c, (c->d / W + 1) / 2, 1);
+  LaunchScope ls(c, DSGD_K_STEP);
+  DSGD_CUDA(dsgd::launch_step<T>(mode, a, vec, a.blocks_per_node, c->stream));
+  return DSGD_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1889,6 +1919,38 @@ dsgd_status dsgd_async_pull_event(dsgd_ctx* c, const dsgd_hyperparams* h,
   });
 }
 
+dsgd_status dsgd_gossip_stale_step(dsgd_ctx* c, const dsgd_hyperparams* h,
+                                   const dsgd_grad_spec* g, uint32_t local, const void* partner) {
+  DSGD_TRY(check_ctx(c));
+  DSGD_TRY(flush_pending(c));
+  if (!h) return set_error(DSGD_EINVAL, "null hyperparams");
+  if (c->distributed()) return set_error(DSGD_EINVAL, "single-node rules run on a single context");
+  if (local >= c->n_local) return set_error(DSGD_EINVAL, "local node out of range");
+  if (!partner) return set_error(DSGD_EINVAL, "null partner vector");
+  GradSel gs;
+  DSGD_TRY(resolve_grad(c, g, &gs));
+  if (gs.logistic) return set_error(DSGD_EINVAL, "single-node rules take a quadratic or buffer gradient");
+  return dispatch(c, [&](auto z) -> dsgd_status {
+    using T = decltype(z);
+    DSGD_TRY(norm_begin(c, gs, g));
+    DSGD_TRY(node_step<T>(c, dsgd::kModeStale, h, &gs, local, partner, (T)h->beta_gossip));
+    c->t[local] += 1;
+    return norm_end(c, gs, g);
+  });
+}
+
+dsgd_status dsgd_mix_toward(dsgd_ctx* c, uint32_t local, const void* partner, double beta) {
+  DSGD_TRY(check_ctx(c));
+  DSGD_TRY(flush_pending(c));
+  if (c->distributed()) return set_error(DSGD_EINVAL, "single-node rules run on a single context");
+  if (local >= c->n_local) return set_error(DSGD_EINVAL, "local node out of range");
+  if (!partner) return set_error(DSGD_EINVAL, "null partner vector");
+  return dispatch(c, [&](auto z) -> dsgd_status {
+    using T = decltype(z);
+    return node_step<T>(c, dsgd::kModeMix, nullptr, nullptr, local, partner, (T)beta);
+  });
+}
+
 dsgd_status dsgd_pull_mix(dsgd_ctx* c, const uint32_t* partner_of) {
   DSGD_TRY(check_ctx(c));
   DSGD_TRY(flush_pending(c));
@@ -1980,6 +2042,7 @@ dsgd_status dsgd_ea_client_event(dsgd_ctx* c, const dsgd_hyperparams* h,
     dsgd::EaArgs<T> a{};
     fill_node<T>(c, i, gs, h, &a.node[0]);
     a.node[0].theta_out = as<T>(c->theta_ptr(i, c->cur));  // in place: only node i moves
+    a.node[0].aux = static_cast<T*>(c->ea_update_out[i]);  // ea_client_step's update
     if (!gs.quad) a.node[0].grad = static_cast<const T*>(gs.grad[i]);
     a.node[0].noise = gs.noise ? as<T>(c->noise[i]) : nullptr;
     a.node[0].norm = gs.norm ? c->norm + (size_t)c->norm_slot * c->n_local : nullptr;
