@@ -374,8 +374,9 @@ def main():
         nv_launch = nv_bytes * (args.steps / nn if nn else 1.0)  # per launch (K pipelines)
         roofline["allreduce_backend"] = backend
         roofline["allreduce_launches_per_round"] = nn / args.steps if nn else None
-        if getattr(grp, "nvls_unavailable", None):
-            roofline["nvls_unavailable"] = grp.nvls_unavailable
+        note = grp.allreduce_info()[1]
+        if note:
+            roofline["nvls_unavailable"] = note
         roofline["allreduce_comm_us"] = t_c * 1e6
         roofline["nvlink_bytes_per_direction_per_round"] = nv_bytes
         roofline["nvlink_achieved_gbs"] = nv_launch / t_c / 1e9 if nn else None
@@ -585,7 +586,7 @@ def run_extras_dist(args, world, rank, local, h, max_over_ranks, barrier):
         try:
             grp = Group.distributed(d, rank, world, local, dtype="f32",
                                     nccl=(proto == N.ELASTIC_AVG),  # center init = mean
-                                    allreduce=False, center=(proto == N.ELASTIC_AVG))
+                                    center=(proto == N.ELASTIC_AVG))
             gen = torch.Generator(device=f"cuda:{local}")
             gen.manual_seed(7 + rank)
             pool = [torch.randn(d, generator=gen, device=f"cuda:{local}") for _ in range(2)]

@@ -39,9 +39,9 @@
 extern "C" {
 #endif
 
-#define DSGD_B200_ABI_VERSION 1
+#define DSGD_B200_ABI_VERSION 2
 #define DSGD_MAX_LOCAL_NODES 32
-#define DSGD_HANDLE_BYTES 256 /* size of one dsgd_ctx_export_handle blob */
+#define DSGD_HANDLE_BYTES 512 /* size of one dsgd_ctx_export_handle blob */
 #define DSGD_NCCL_ID_BYTES 128
 
 typedef enum {
@@ -351,8 +351,14 @@ dsgd_status dsgd_run_events(dsgd_ctx* ctx, const dsgd_run_desc* run, uint64_t ev
 
 /* ---------------------------------------------- multi-GPU group wiring
  * One context per GPU (n_local == 1).  Each context exports a fixed-size
- * blob (CUDA IPC handle of its state arena + layout); the host exchanges
- * blobs out of band (e.g. torch.distributed all_gather) and connects. */
+ * blob (CUDA IPC handle of its state arena + layout; on node 0, when the
+ * all-reduce backend is NVLS, the NVSwitch multicast object it created, as
+ * its pid + POSIX fd); the host exchanges blobs out of band (e.g.
+ * torch.distributed all_gather, a shared mapping) and connects.  Connecting
+ * maps every peer's arena and -- for NVLS -- makes every rank join the
+ * multicast object (pidfd_getfd, cuMulticastAddDevice, cuMulticastBindMem),
+ * agreeing over the mapped peer memory; when any GPU cannot join, every rank
+ * stays on the peer-memory two-shot ("p2p").  All ranks call it together. */
 dsgd_status dsgd_ctx_export_handle(dsgd_ctx* ctx, void* blob /* DSGD_HANDLE_BYTES */);
 dsgd_status dsgd_ctx_connect_peers(dsgd_ctx* ctx, const void* blobs /* p blobs */);
 /* In-process group: p one-node contexts (rank r on devices[r], or all on
@@ -373,14 +379,18 @@ dsgd_status dsgd_group_create_inproc(const dsgd_ctx_desc* base, uint32_t p, cons
  * order, then round r+1 (runs: one descriptor per rank, same protocol and
  * round count). */
 dsgd_status dsgd_group_run_rounds(dsgd_ctx* const* ctxs, uint32_t n, const dsgd_run_desc* runs);
-/* NVLS (in-switch) all-reduce: `x` and `avg` are this context's d-element
- * slices of a multicast-mapped (NVSwitch multicast object) allocation and
- * `x_mc` / `avg_mc` their multicast addresses (e.g. from
- * torch.distributed._symmetric_memory).  After this call the multi-GPU
- * all-reduce reduces with multimem.ld_reduce and broadcasts with
- * multimem.st (summation order: the switch's). */
+/* NVLS (in-switch) all-reduce with CALLER-provided buffers (the library sets
+ * up its own in dsgd_ctx_connect_peers): `x` and `avg` are this context's
+ * d-element slices of a multicast-mapped allocation and `x_mc` / `avg_mc`
+ * their multicast addresses.  The multi-GPU all-reduce then reduces with
+ * multimem.ld_reduce and broadcasts with multimem.st (summation order: the
+ * switch's). */
 dsgd_status dsgd_ctx_attach_multicast(dsgd_ctx* ctx, void* x, void* x_mc, void* avg,
                                       void* avg_mc);
+/* The multi-GPU all-reduce this context runs: "local" (one context),
+ * "oneshot", "nvls", "p2p" or "nccl"; *note says why NVLS is not in use when
+ * it was requested (empty otherwise).  Strings owned by the context. */
+dsgd_status dsgd_ctx_allreduce_backend(dsgd_ctx* ctx, const char** name, const char** note);
 dsgd_status dsgd_nccl_unique_id(void* id /* DSGD_NCCL_ID_BYTES */);
 dsgd_status dsgd_ctx_init_nccl(dsgd_ctx* ctx, const void* id, int rank, int nranks);
 /* Spin-wait bound for cross-GPU flags (default 30 s). */

@@ -25,7 +25,7 @@ GRAD_QUADRATIC, GRAD_BUFFER, GRAD_LOGISTIC = 0, 1, 2
 K_STEP, K_ALLREDUCE, K_AR_DELTA, K_AR_APPLY, K_NCCL, K_EA, K_PUSH, K_OTHER = range(8)
 KERNEL_NAMES = ["step", "allreduce_local", "ar_delta", "ar_apply", "allreduce_comm",
                 "ea", "push", "other"]
-HANDLE_BYTES = 256
+HANDLE_BYTES = 512
 NCCL_ID_BYTES = 128
 MAX_LOCAL = 32
 
@@ -142,6 +142,7 @@ _SIGS = {
     "dsgd_group_create_inproc": (C.c_int, [C.POINTER(CtxDesc), C.c_uint32, C.POINTER(C.c_int),
                                            C.POINTER(_P)]),
     "dsgd_group_run_rounds": (C.c_int, [C.POINTER(_P), C.c_uint32, C.POINTER(RunDesc)]),
+    "dsgd_ctx_allreduce_backend": (C.c_int, [_P, C.POINTER(C.c_char_p), C.POINTER(C.c_char_p)]),
     "dsgd_nccl_unique_id": (C.c_int, [_P]),
     "dsgd_ctx_attach_multicast": (C.c_int, [_P, _P, _P, _P, _P]),
     "dsgd_ctx_init_nccl": (C.c_int, [_P, _P, C.c_int, C.c_int]),
@@ -169,7 +170,7 @@ def load():
         f = getattr(lib, name)
         f.restype = res
         f.argtypes = args
-    if lib.dsgd_abi_version() != 1:
+    if lib.dsgd_abi_version() != 2:
         raise ImportError("libdsgd_b200.so ABI version mismatch")
     _lib = lib
     return lib

@@ -64,7 +64,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         # each object's cubin is embedded once
         cuda = os.path.dirname(os.path.dirname(os.path.realpath(NVCC)))
         link = ["g++", "-shared", *objs, "-o", SO + ".tmp", "-L" + os.path.join(cuda, "lib64"),
-                "-lcudart_static", "-lnccl", "-lcuda", "-ldl", "-lrt", "-lpthread"]
+                "-lcudart_static", "-lnccl", "-ldl", "-lrt", "-lpthread"]
         subprocess.run(link, check=True)
     os.replace(SO + ".tmp", SO)
     return SO

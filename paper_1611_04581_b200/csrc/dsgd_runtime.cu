@@ -18,6 +18,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -29,6 +30,9 @@
 #include "dsgd_b200.h"
 #include "dsgd_internal.h"
 #include "dsgd_kernels.cuh"
+#include "dsgd_multicast.h"
+
+#include <unistd.h>
 
 namespace dsgd {
 
@@ -94,6 +98,15 @@ struct HandleBlob {
   uint64_t off_ar;   // all-reduce counters: [0] exchange written, [1] average written
   uint64_t off_arf;  // reserved
   uint64_t off_x2;   // second exchange buffer (one-shot all-reduce, round parity)
+  uint64_t off_hb;   // host-barrier slots (rank 0's are the ones used)
+  // NVLS: rank 0's multicast object, shared as a POSIX fd fetched with
+  // pidfd_getfd(pid, fd) (mc_kind 0: none, everybody uses the peer-memory
+  // two-shot)
+  uint32_t mc_kind;
+  int32_t mc_pid;
+  int32_t mc_fd;
+  int32_t pad2;
+  uint64_t mc_size;
 };
 static_assert(sizeof(HandleBlob) <= DSGD_HANDLE_BYTES, "handle blob too large");
 
@@ -106,6 +119,7 @@ struct PeerNode {  // device-addressable view of one node (local or IPC-mapped)
   char* x2 = nullptr;                 // second exchange buffer (one-shot, odd rounds)
   char* avg = nullptr;                // all-reduce average buffer
   unsigned long long* ar = nullptr;   // [0] exchange written, [1] average written (rounds)
+  unsigned long long* hb = nullptr;   // host-barrier slots (connect-time agreement)
 };
 
 struct Prof {
@@ -180,6 +194,10 @@ struct dsgd_ctx {
   char* nvls_x_mc = nullptr;
   char* nvls_avg_mc = nullptr;
   size_t off_x2 = 0;
+  size_t off_hb = 0;
+  std::string ar_mode;             // requested backend (DSGD_ALLREDUCE or the default)
+  dsgd::McState mc;                // NVLS multicast buffers owned by the library
+  std::string nvls_note;           // why NVLS is not in use (empty when it is)
 
   uint64_t ar_rounds = 0;          // peer-memory all-reduce rounds run
   uint64_t n_chunks = 0;
@@ -1325,6 +1343,148 @@ dsgd_status node_step(dsgd_ctx* c, int mode, const dsgd_hyperparams* h, const Gr
   return DSGD_OK;
 }
 
+// ------------------------------------------------ NVLS set-up (library-owned)
+// The two-shot all-reduce runs its reduce in the NVSwitch when the requested
+// backend is "nvls" (the default for p > 2 outside the one-shot's small-d
+// range) and every GPU of the group joins one multicast object.
+bool wants_nvls(const dsgd_ctx* c) {
+  return c->distributed() && c->p2p_allreduce && !c->ar_oneshot && c->ar_mode == "nvls";
+}
+
+size_t nvls_half(const dsgd_ctx* c) { return align_up(c->d * c->es, size_t(1) << 21); }
+size_t nvls_bytes(const dsgd_ctx* c) { return 2 * nvls_half(c); }
+
+void attach_nvls(dsgd_ctx* c, char* x, char* x_mc, char* avg, char* avg_mc) {
+  c->peers[c->first].x = x;      // kernel 1 writes here (unicast)
+  c->peers[c->first].avg = avg;  // next round / flush read here
+  c->nvls_x_mc = x_mc;
+  c->nvls_avg_mc = avg_mc;
+  c->p2p_allreduce = true;
+  c->ar_oneshot = false;
+  c->ar_nvls = true;
+  c->nvls_note.clear();
+  // reduce CTAs on SMs of their own (1024 threads, padded smem) and a wider
+  // delta grid: 271.5 vs 328.7 us/round at p = 4, d = 25M
+  // (profiles/r1_tune_allreduce_n4.md); the environment still overrides
+  if (!std::getenv("DSGD_AR_DELTA_FRAC")) c->ar_delta_frac = 1.5;
+  if (!std::getenv("DSGD_AR_COMM_FRAC")) c->ar_comm_frac = 0.5;
+}
+
+void attach_mc_state(dsgd_ctx* c) {
+  char* uc = reinterpret_cast<char*>(c->mc.uc);
+  char* mc = reinterpret_cast<char*>(c->mc.mcva);
+  const size_t half = nvls_half(c);
+  attach_nvls(c, uc, mc, uc + half, mc + half);
+}
+
+// Connect-time agreement of one-process-per-GPU ranks over the already
+// mapped peer memory: every rank posts (phase, ok) into rank 0's slots and
+// waits until all posted phase `phase`; *all_ok tells whether every rank
+// succeeded.  (A rank that posted a later phase passed this one.)
+dsgd_status host_barrier(dsgd_ctx* c, uint32_t phase, bool ok, bool* all_ok) {
+  unsigned long long* slots = c->peers[0].hb;
+  if (!slots) return set_error(DSGD_ESTATE, "no barrier slots");
+  const unsigned long long v = ((unsigned long long)phase << 8) | (ok ? 1u : 2u);
+  DSGD_CUDA(cudaMemcpy(slots + c->first, &v, sizeof(v), cudaMemcpyDefault));
+  std::vector<unsigned long long> got(c->p);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    DSGD_CUDA(cudaMemcpy(got.data(), slots, sizeof(v) * c->p, cudaMemcpyDefault));
+    bool done = true, good = true;
+    for (unsigned long long g : got) {
+      const unsigned long long ph = g >> 8;
+      if (ph < phase) done = false;
+      else if (ph == phase && (g & 0xff) != 1) good = false;
+    }
+    if (done) {
+      *all_ok = good;
+      return DSGD_OK;
+    }
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60))
+      return set_error(DSGD_ETIMEOUT, "a peer never reached the NVLS set-up barrier");
+    usleep(100);
+  }
+}
+
+// Every rank joins rank 0's multicast object: import (pidfd_getfd) ->
+// barrier -> add this GPU -> barrier -> back it, bind and map -> barrier.
+// Any failure anywhere leaves every rank on the peer-memory two-shot.
+dsgd_status join_nvls(dsgd_ctx* c, const HandleBlob& b0) {
+  bool ok = true, all = false;
+  if (c->first != 0) {
+    ok = dsgd::mc_import_fd(&c->mc, b0.mc_pid, b0.mc_fd, b0.mc_size) == DSGD_OK;
+    if (!ok) c->nvls_note = dsgd::g_error;
+  }
+  DSGD_TRY(host_barrier(c, 1, ok, &all));
+  if (c->mc.export_fd >= 0) {  // rank 0: everybody holds its own handle now
+    close(c->mc.export_fd);
+    c->mc.export_fd = -1;
+  }
+  if (all) {
+    ok = dsgd::mc_add_device(&c->mc, c->device) == DSGD_OK;
+    if (!ok) c->nvls_note = dsgd::g_error;
+    DSGD_TRY(host_barrier(c, 2, ok, &all));
+  }
+  if (all) {
+    ok = dsgd::mc_bind_map(&c->mc, c->device, true) == DSGD_OK;
+    if (!ok) c->nvls_note = dsgd::g_error;
+    DSGD_TRY(host_barrier(c, 3, ok, &all));
+  }
+  if (!all) {
+    if (c->nvls_note.empty()) c->nvls_note = "a peer could not join the multicast object";
+    dsgd::mc_release(&c->mc, c->device);
+    return DSGD_OK;
+  }
+  attach_mc_state(c);
+  return DSGD_OK;
+}
+
+// In-process group on distinct GPUs: one object, every GPU added by this
+// thread before any backing is bound.
+dsgd_status inproc_nvls(InprocGroup* g) {
+  dsgd_ctx* c0 = g->ctx[0];
+  for (dsgd_ctx* c : g->ctx) {
+    if (!wants_nvls(c)) return DSGD_OK;
+    for (dsgd_ctx* o : g->ctx)
+      if (o != c && o->device == c->device) return DSGD_OK;  // ranks sharing a GPU
+    if (!dsgd::mc_supported(c->device)) {
+      for (dsgd_ctx* o : g->ctx) o->nvls_note = "a GPU reports no multicast (NVLS) support";
+      return DSGD_OK;
+    }
+  }
+  dsgd_status st;
+  {
+    DeviceGuard dg(c0->device);
+    st = dsgd::mc_create(&c0->mc, c0->device, c0->p, nvls_bytes(c0), false);
+  }
+  for (dsgd_ctx* c : g->ctx) {
+    if (st != DSGD_OK) break;
+    if (c != c0) {
+      c->mc.mc = c0->mc.mc;
+      c->mc.size = c0->mc.size;
+      c->mc.owns_mc = false;
+    }
+    DeviceGuard dg(c->device);
+    st = dsgd::mc_add_device(&c->mc, c->device);
+  }
+  for (dsgd_ctx* c : g->ctx) {
+    if (st != DSGD_OK) break;
+    DeviceGuard dg(c->device);
+    st = dsgd::mc_bind_map(&c->mc, c->device, false);
+  }
+  if (st != DSGD_OK) {
+    const std::string why = dsgd::g_error;
+    for (auto it = g->ctx.rbegin(); it != g->ctx.rend(); ++it) {  // owner last
+      DeviceGuard dg((*it)->device);
+      dsgd::mc_release(&(*it)->mc, (*it)->device);
+      (*it)->nvls_note = why;
+    }
+    return DSGD_OK;
+  }
+  for (dsgd_ctx* c : g->ctx) attach_mc_state(c);
+  return DSGD_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1388,15 +1548,20 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
     off += 256;
     c->off_x2 = off;
     off += vb;
+    c->off_hb = off;
+    off += 256;
   }
   c->arena_bytes = off;
   // multi-GPU all-reduce backend: oneshot (default p <= 2), p2p (two-shot,
   // default p > 2), nccl
   {
     // one kernel per round wins at p <= 2, and at p <= 4 while d is latency-bound
-    std::string mode = (c->p <= 2 || (c->p <= 4 && c->d < (4u << 20))) ? "oneshot" : "p2p";
+    // (nvls falls back to the peer-memory two-shot "p2p" when the GPUs
+    // cannot join a multicast object)
+    std::string mode = (c->p <= 2 || (c->p <= 4 && c->d < (4u << 20))) ? "oneshot" : "nvls";
     if (const char* e = std::getenv("DSGD_ALLREDUCE")) mode = e;
     if (mode == "p2p2k") mode = "p2p";
+    c->ar_mode = mode;
     c->p2p_allreduce = mode != "nccl";
     c->ar_oneshot = mode == "oneshot" && c->p <= 4;
   }
@@ -1463,6 +1628,7 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
       pn.avg = c->arena + c->off_a;
       pn.ar = reinterpret_cast<unsigned long long*>(c->arena + c->off_ar);
       pn.x2 = c->arena + c->off_x2;
+      pn.hb = reinterpret_cast<unsigned long long*>(c->arena + c->off_hb);
     }
     if (i == 0 && (c->flags & DSGD_CTX_CENTER)) {
       pn.c_in = c->arena + c->off_c_in;
@@ -1479,6 +1645,7 @@ void dsgd_ctx_destroy(dsgd_ctx* c) {
   DeviceGuard g(c->device);
   cudaStreamSynchronize(c->stream);
   if (c->comm) ncclCommDestroy(c->comm);
+  dsgd::mc_release(&c->mc, c->device);
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   for (uint32_t i = 0; i < c->n_local; ++i) {
     cudaFree(c->delta[i]);
@@ -2348,6 +2515,28 @@ dsgd_status dsgd_ctx_export_handle(dsgd_ctx* c, void* blob) {
   b.off_a = c->off_a;
   b.off_ar = c->off_ar;
   b.off_x2 = c->off_x2;
+  b.off_hb = c->off_hb;
+  // NVLS: rank 0 creates the multicast object every rank joins in
+  // dsgd_ctx_connect_peers (the decision is the same on every rank)
+  if (c->first == 0 && wants_nvls(c) && c->mc.mc == 0) {
+    if (!dsgd::mc_supported(c->device)) {
+      c->nvls_note = "the GPU reports no multicast (NVLS) support";
+    } else {
+      int fd = -1;
+      const dsgd_status s1 = dsgd::mc_create(&c->mc, c->device, c->p, nvls_bytes(c), true);
+      const dsgd_status s2 = s1 == DSGD_OK ? dsgd::mc_export_fd(&c->mc, &fd) : s1;
+      if (s2 != DSGD_OK) {
+        c->nvls_note = dsgd::g_error;
+        dsgd::mc_release(&c->mc, c->device);
+      }
+    }
+  }
+  if (c->first == 0 && c->mc.mc && c->mc.export_fd >= 0) {
+    b.mc_kind = 2;
+    b.mc_pid = (int32_t)getpid();
+    b.mc_fd = c->mc.export_fd;
+    b.mc_size = c->mc.size;
+  }
   std::memset(blob, 0, DSGD_HANDLE_BYTES);
   std::memcpy(blob, &b, sizeof(b));
   return DSGD_OK;
@@ -2397,6 +2586,7 @@ dsgd_status dsgd_ctx_connect_peers(dsgd_ctx* c, const void* blobs) {
       pn.avg = m + b.off_a;
       pn.ar = reinterpret_cast<unsigned long long*>(m + b.off_ar);
       pn.x2 = m + b.off_x2;
+      pn.hb = reinterpret_cast<unsigned long long*>(m + b.off_hb);
     }
     if (b.flags & DSGD_CTX_CENTER) {
       pn.c_in = m + b.off_c_in;
@@ -2404,6 +2594,11 @@ dsgd_status dsgd_ctx_connect_peers(dsgd_ctx* c, const void* blobs) {
     }
   }
   c->connected = true;
+  HandleBlob b0;
+  std::memcpy(&b0, base, sizeof(b0));
+  if (b0.mc_kind == 2 && wants_nvls(c)) return join_nvls(c, b0);
+  if (wants_nvls(c) && c->nvls_note.empty())
+    c->nvls_note = "rank 0 created no multicast object";
   return DSGD_OK;
 }
 
@@ -2480,6 +2675,10 @@ dsgd_status dsgd_group_create_inproc(const dsgd_ctx_desc* base, uint32_t p, cons
     c->connected = true;
     c->grp = grp;
   }
+  {
+    const dsgd_status st = inproc_nvls(grp.get());
+    if (st != DSGD_OK) return fail(st);
+  }
   for (uint32_t r = 0; r < p; ++r) out[r] = grp->ctx[r];
   return DSGD_OK;
 }
@@ -2492,18 +2691,21 @@ dsgd_status dsgd_ctx_attach_multicast(dsgd_ctx* c, void* x, void* x_mc, void* av
   if (!x || !x_mc || !avg || !avg_mc) return set_error(DSGD_EINVAL, "null multicast buffer");
   for (void* q : {x, x_mc, avg, avg_mc})
     if (!aligned16(q)) return set_error(DSGD_EINVAL, "multicast buffers must be 16-byte aligned");
-  c->peers[c->first].x = static_cast<char*>(x);      // kernel 1 writes here (unicast)
-  c->peers[c->first].avg = static_cast<char*>(avg);  // next round / flush read here
-  c->nvls_x_mc = static_cast<char*>(x_mc);
-  c->nvls_avg_mc = static_cast<char*>(avg_mc);
-  c->p2p_allreduce = true;
-  c->ar_oneshot = false;
-  c->ar_nvls = true;
-  // reduce CTAs on SMs of their own (1024 threads, padded smem) and a wider
-  // delta grid: 271.5 vs 328.7 us/round at p = 4, d = 25M
-  // (profiles/r1_tune_allreduce_n4/split/); the environment still overrides
-  if (!std::getenv("DSGD_AR_DELTA_FRAC")) c->ar_delta_frac = 1.5;
-  if (!std::getenv("DSGD_AR_COMM_FRAC")) c->ar_comm_frac = 0.5;
+  if (c->mc.mc) return set_error(DSGD_ESTATE, "the library already set up multicast buffers");
+  attach_nvls(c, static_cast<char*>(x), static_cast<char*>(x_mc), static_cast<char*>(avg),
+              static_cast<char*>(avg_mc));
+  return DSGD_OK;
+}
+
+dsgd_status dsgd_ctx_allreduce_backend(dsgd_ctx* c, const char** name, const char** note) {
+  DSGD_TRY(check_ctx(c));
+  const char* n = !c->distributed()       ? "local"
+                  : !c->p2p_allreduce     ? "nccl"
+                  : c->ar_oneshot         ? "oneshot"
+                  : c->ar_nvls            ? "nvls"
+                                          : "p2p";
+  if (name) *name = n;
+  if (note) *note = c->nvls_note.c_str();
   return DSGD_OK;
 }
 

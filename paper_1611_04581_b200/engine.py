@@ -481,49 +481,27 @@ class Group:
 
     @classmethod
     def distributed(cls, d: int, rank: int, world: int, device: int, dtype="f32",
-                    nccl: bool = True, allreduce: bool = True, **kw) -> "Group":
-        """One node per process/GPU; wires IPC peers and NCCL through the
-        already-initialised torch.distributed process group (any backend)."""
-        import os
+                    nccl: bool = True, **kw) -> "Group":
+        """One node per process/GPU; wires IPC peers (and, for the NVLS
+        all-reduce, the library's own NVSwitch multicast object) and NCCL
+        through the already-initialised torch.distributed process group (any
+        backend) as the out-of-band channel.  The all-reduce backend is the
+        library's choice (``allreduce_backend``)."""
         g = cls(d, p=world, dtype=dtype, device=device, first_node=rank, n_local=1, **kw)
         g.connect_peers(exchange_blobs(g.export_handle(), rank, world))
         if nccl and world > 1:
             g.init_nccl(broadcast_nccl_id(rank, world), rank, world)
-        small = world <= 2 or (world <= 4 and d < (4 << 20))  # one kernel per round
-        g.allreduce_backend = "local" if world == 1 else os.environ.get(
-            "DSGD_ALLREDUCE", "oneshot" if small else "nvls")
-        if g.allreduce_backend == "nvls" and allreduce:
-            why = g._attach_nvls(device)
-            if why:  # no multicast (NVLS) on this system: two-shot over peer memory
-                g.allreduce_backend = "p2p"
-                g.nvls_unavailable = why
         return g
 
-    def _attach_nvls(self, device: int):
-        """Map NVSwitch multicast exchange / average buffers (torch symmetric
-        memory is the plumbing) and switch the all-reduce to multimem."""
-        try:
-            import torch
-            import torch.distributed as dist
-            import torch.distributed._symmetric_memory as symm
-            tdt = torch.float32 if self.dtype == N.F32 else torch.float64
-            es = 4 if self.dtype == N.F32 else 8
-            n = (self.d + 63) // 64 * 64
-            buf = symm.empty(2 * n, dtype=tdt, device=f"cuda:{device}")
-            group = dist.group.WORLD
-            try:
-                h = symm.rendezvous(buf, group.group_name)
-            except TypeError:
-                h = symm.rendezvous(buf, group)
-            mc = int(h.multicast_ptr or 0)
-            if not mc:
-                return "no multicast pointer (NVLS unsupported)"
-            base = buf.data_ptr()
-            self.attach_multicast(base, mc, base + n * es, mc + n * es)
-            self._symm = (buf, h)
-            return None
-        except Exception as e:  # pragma: no cover - depends on the box
-            return f"{type(e).__name__}: {e}"
+    @property
+    def allreduce_backend(self) -> str:
+        """dsgd_ctx_allreduce_backend: local / oneshot / nvls / p2p / nccl."""
+        return self.allreduce_info()[0]
+
+    def allreduce_info(self):
+        name, note = C.c_char_p(), C.c_char_p()
+        N.check(self.lib.dsgd_ctx_allreduce_backend(self._ctx, C.byref(name), C.byref(note)))
+        return name.value.decode(), (note.value or b"").decode()
 
     def attach_multicast(self, x: int, x_mc: int, avg: int, avg_mc: int) -> None:
         N.check(self.lib.dsgd_ctx_attach_multicast(self._ctx, x, x_mc, avg, avg_mc))

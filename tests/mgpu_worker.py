@@ -131,8 +131,7 @@ def timeout_case(rank, world, local, dtype, dist):
     h = Hyperparams(alpha0=0.1, anneal_at=(), mu=0.9, weight_decay=0.0)
     res = {}
     for proto in ("pull-gossip", "all-reduce"):
-        g = Group.distributed(4096, rank, world, local, dtype=dtype, quadratic=True,
-                              allreduce=proto == "all-reduce")
+        g = Group.distributed(4096, rank, world, local, dtype=dtype, quadratic=True)
         g.set_timeout(0.5)
         g.set_quadratic(np.ones(4096))
         g.set_state(0, np.full(4096, float(rank)))

@@ -38,7 +38,6 @@ def main():
             try:
                 g = Group.distributed(d, rank, world, local, dtype="f32",
                                       nccl=proto != N.PULL_GOSSIP,
-                                      allreduce=proto == N.ALLREDUCE,
                                       quadratic=True, center=proto == N.ELASTIC_AVG)
                 gen = torch.Generator(device=f"cuda:{local}")
                 gen.manual_seed(11 + rank)
