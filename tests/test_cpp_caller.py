@@ -57,3 +57,21 @@ def test_cpp_multiprocess_worker_runs(tmp_path):
         assert out.returncode == 0, out.stdout + out.stderr
         j = json.loads(out.stdout.strip().splitlines()[-1])
         assert j["ok"] is True and j["param_updates_per_s"] > 0
+
+
+@pytest.mark.gpu
+def test_cpp_worker_nvls_without_torch(tmp_path):
+    """p > 2 from a C++-only host: the library creates the NVSwitch
+    multicast object itself (cuMulticastCreate, pidfd_getfd, bind) and the
+    all-reduce runs in the switch; every rank ends bit-identical."""
+    import json
+    import torch
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    exe = build_worker(tmp_path)
+    out = subprocess.run([exe, "--gpus", "4", "--d", "25000000", "--rounds", "30",
+                          "--protocol", "all-reduce"], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    j = json.loads(out.stdout.strip().splitlines()[-1])
+    assert j["ok"] is True and j["ranks_identical"] is True
+    assert j["allreduce_backend"] == "nvls", j

@@ -16,6 +16,7 @@
 #include <sys/wait.h>
 #include <unistd.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -31,9 +32,21 @@ struct Shared {
   pthread_barrier_t barrier;
   char nccl_id[DSGD_NCCL_ID_BYTES];
   double ms[64];
+  double wall_ms[64];
+  uint64_t hash[64];
   int status[64];
+  char backend[32];
+  char note[256];
   char blobs[64][DSGD_HANDLE_BYTES];
 };
+
+// FNV-1a over the parameter bytes: ranks of an all-reduce must agree bit for bit
+uint64_t fnv(const std::vector<double>& v) {
+  uint64_t h = 1469598103934665603ull;
+  const unsigned char* b = reinterpret_cast<const unsigned char*>(v.data());
+  for (size_t i = 0; i < v.size() * sizeof(double); ++i) h = (h ^ b[i]) * 1099511628211ull;
+  return h;
+}
 
 int run_worker(int rank, int world, uint64_t d, uint64_t rounds, dsgd_protocol proto,
                Shared* sh) {
@@ -51,6 +64,13 @@ int run_worker(int rank, int world, uint64_t d, uint64_t rounds, dsgd_protocol p
     pthread_barrier_wait(&sh->barrier);
     check(dsgd_ctx_connect_peers(ctx.get(), sh->blobs));
     check(dsgd_ctx_init_nccl(ctx.get(), sh->nccl_id, rank, world));
+    if (rank == 0) {  // the library's own all-reduce choice (NVLS set up without torch)
+      const char* name = nullptr;
+      const char* note = nullptr;
+      check(dsgd_ctx_allreduce_backend(ctx.get(), &name, &note));
+      std::snprintf(sh->backend, sizeof(sh->backend), "%s", name);
+      std::snprintf(sh->note, sizeof(sh->note), "%s", note);
+    }
     if (proto == DSGD_ELASTIC_AVG) check(dsgd_ea_init_center(ctx.get()));
     check(dsgd_ctx_seed_streams(ctx.get(), 1, "run/trial0"));
 
@@ -68,8 +88,11 @@ int run_worker(int rank, int world, uint64_t d, uint64_t rounds, dsgd_protocol p
     pthread_barrier_wait(&sh->barrier);
     check(dsgd_profile_enable(ctx.get(), 1));
     run.rounds = rounds;
+    const auto t0 = std::chrono::steady_clock::now();
     check(dsgd_run_rounds(ctx.get(), &run));
     ctx.sync();
+    sh->wall_ms[rank] =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     double ms = 0.0;
     for (int k = 0; k < DSGD_K_COUNT; ++k) {
       double part = 0.0;
@@ -80,6 +103,7 @@ int run_worker(int rank, int world, uint64_t d, uint64_t rounds, dsgd_protocol p
     sh->ms[rank] = ms;
     std::vector<double> th(d);
     ctx.get_state(0, &th, nullptr, nullptr);
+    sh->hash[rank] = fnv(th);
     sh->status[rank] = std::isfinite(th[0]) && std::isfinite(th[d - 1]) ? 0 : 2;
   } catch (const std::exception& e) {
     std::fprintf(stderr, "rank %d: %s\n", rank, e.what());
@@ -128,16 +152,22 @@ int main(int argc, char** argv) {
     waitpid(pid, &st, 0);
     if (!WIFEXITED(st) || WEXITSTATUS(st) != 0) bad = 1;
   }
-  double worst = 0.0;
+  double worst = 0.0, wall = 0.0;
+  bool same = true;
   for (int r = 0; r < world; ++r) {
     worst = std::max(worst, sh->ms[r]);
+    wall = std::max(wall, sh->wall_ms[r]);
     bad |= sh->status[r];
+    same = same && sh->hash[r] == sh->hash[0];
   }
   const double us_round = worst * 1e3 / static_cast<double>(rounds);
+  const double us_wall = wall * 1e3 / static_cast<double>(rounds);
   std::printf("{\"tool\": \"dsgd_worker\", \"protocol\": \"%s\", \"gpus\": %d, \"d\": %llu, "
-              "\"rounds\": %llu, \"us_per_round_kernels\": %.2f, "
-              "\"param_updates_per_s\": %.4e, \"ok\": %s}\n",
+              "\"rounds\": %llu, \"allreduce_backend\": \"%s\", \"nvls_note\": \"%s\", "
+              "\"us_per_round_kernels\": %.2f, \"us_per_round_wall\": %.2f, "
+              "\"param_updates_per_s\": %.4e, \"ranks_identical\": %s, \"ok\": %s}\n",
               proto_name.c_str(), world, (unsigned long long)d, (unsigned long long)rounds,
-              us_round, world * (double)d / (us_round * 1e-6), bad ? "false" : "true");
+              sh->backend, sh->note, us_round, us_wall, world * (double)d / (us_wall * 1e-6),
+              same ? "true" : "false", bad ? "false" : "true");
   return bad;
 }
