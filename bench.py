@@ -36,6 +36,18 @@ METRIC = "worker param-updates/sec and aggregation-step GB/s vs HBM/NVLink roofl
 UNIT = "param-updates/s"
 D_DEFAULT = 25_000_000
 POOL = 4
+SPEC_HBM_GBS = 8000.0  # the north star's ~8 TB/s HBM denominator (DGX B200 spec)
+
+
+def workload_config(d: int, world: int) -> dict:
+    """The `config` of BOTH arms (ours and --impl reference): the same
+    workload, key for key."""
+    return {"workload": "configs[3]: synchronous all-reduce SGD round (allreduce_round, Nesterov "
+                        "momentum 0.9, wd 1e-4, aggregate momentum scope), synthetic gradients",
+            "d_per_worker": d, "p": world, "parallelism": f"dp{world}",
+            "grad_source": f"pool of {POOL} synthetic N(0,1) gradient vectors per worker, served "
+                           "in turn through the Objective plugin slot",
+            "l2": "inputs larger than L2 (~400 MB/step/worker working set)"}
 
 
 def parse():
@@ -145,10 +157,10 @@ def host_info() -> dict:
     return {"cpu_model": model, "nproc": len(os.sched_getaffinity(0))}
 
 
-def cpu_reference(protocol: int, p: int, d: int, rounds: int, threaded: bool):
+def cpu_reference(protocol: int, p: int, d: int, rounds: int, threaded: bool, grad="pool"):
     import oracle as O
     h = O.HyperParams(alpha0=0.1, anneal_at=(), mu=0.9, weight_decay=1e-4, beta_ea=0.1)
-    return O.ref_time_rounds(protocol, p, d, rounds, threaded, h)
+    return O.ref_time_rounds(protocol, p, d, rounds, threaded, h, grad)
 
 
 def run_reference(args, world, rank):
@@ -175,8 +187,9 @@ def run_reference(args, world, rank):
             "ms_per_step": per * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": "all-reduce SGD round, momentum 0.9, wd 1e-4 (configs[3])",
-                       "d_per_worker": d_sample, "p": p, "parallelism": f"dp{p} (threads)"},
+            "config": workload_config(args.d, p),
+            "reference_path": "run_transport (ring_allreduce over p worker threads)" if threaded
+                              else "simulator rules (allreduce_round), 1 thread",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
                              "sample": sample, "host": host_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -345,19 +358,25 @@ def main():
     t_nv = (nv_bytes * units / d / (nv_peak * 1e9)
             if (world > 1 and kname == "allreduce_comm") else 0.0)
     bound = "nvlink" if t_nv > t_hbm else "hbm"
-    traffic = None
-    if world == 1 and es == 4:  # DRAM bytes of the same kernel from the committed ncu capture
-        try:
-            with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                                   "r1_ncu_traffic.json")) as f:
-                t = json.load(f).get(f"k_local_tma<float>/d={d}")
-            if t:
-                traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
-        except (OSError, ValueError, KeyError):
-            traffic = None
+    traffic, traffic_src = None, None
+    if world == 1 and es == 4:  # DRAM bytes of the same kernel: a PRIOR ncu capture (committed)
+        for cap in ("r2_ncu_traffic.json", "r1_ncu_traffic.json"):
+            try:
+                with open(os.path.join(ROOT, "profiles", cap)) as f:
+                    t = json.load(f).get(f"k_local_tma<float>/d={d}")
+                if t:
+                    traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
+                    traffic_src = (f"prior ncu --set full capture of the same kernel and size "
+                                   f"(profiles/{cap}), not measured in this run")
+                    break
+            except (OSError, ValueError, KeyError):
+                continue
     roofline = {"bound": bound, "kernel": kdesc, "achieved": achieved, "peak": peak,
                 "peak_source": peak_src, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "traffic_source": traffic_src,
+                "frac_of_spec_hbm": (achieved / SPEC_HBM_GBS) if achieved else None,
+                "spec_hbm_gbs": SPEC_HBM_GBS,
                 "algorithmic_bytes_per_launch": bpp * units,
                 "params_per_launch": units,
                 "kernel_avg_us": kavg_ms * 1e3,
@@ -443,6 +462,44 @@ def main():
                "path": "pinned host gradient -> device (copy stream, double-buffered) + "
                        "dsgd_allreduce_round(external gradient, grad_norm_out -> host)"}
 
+    # ---------------- e2e, the Objective plugin contract (objectives.hpp:43-48):
+    # every step the evaluation point theta + mu*delta_prev goes device ->
+    # host, the host Objective (here QuadraticObjective(spectrum 1, optimum 0):
+    # g = point) produces the gradient, which goes host -> device and the
+    # round runs on it -- the round trip a host-side model forces per step
+    e2e_plugin = None
+    if True:
+        pin = torch.empty(d, dtype=tdt).pin_memory()
+        dgrad = torch.empty(d, dtype=tdt, device=f"cuda:{local}")
+        steps_p = max(3, min(args.steps, 10))
+
+        def plugin_steps(n):
+            for _ in range(n):
+                grp.eval_point(h, 0, dgrad.data_ptr())
+                with torch.cuda.stream(stream):
+                    pin.copy_(dgrad, non_blocking=True)  # D2H: the evaluation point
+                stream.synchronize()
+                # host Objective: g = spectrum * (point - optimum) = point
+                with torch.cuda.stream(stream):
+                    dgrad.copy_(pin, non_blocking=True)  # H2D: the gradient
+                grp.allreduce_round(h, grad=[dgrad.data_ptr()])
+            grp.sync()
+
+        plugin_steps(2)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        plugin_steps(steps_p)
+        torch.cuda.synchronize()
+        p_ms = max_over_ranks((time.perf_counter() - t0) * 1e3)
+        e2e_plugin = {"value": world * d / (p_ms / steps_p * 1e-3), "unit": UNIT,
+                      "h2d_bytes_per_step": es * d * world, "d2h_bytes_per_step": es * d * world,
+                      "steps": steps_p, "ms_per_step": p_ms / steps_p,
+                      "path": "dsgd_eval_point (theta + mu*delta_prev) -> host, host "
+                              "QuadraticObjective(1, 0) gradient -> device, "
+                              "dsgd_allreduce_round(external gradient); wall clock"}
+        del pin, dgrad
+
     # ---------------- extras: gossip / EASGD shapes
     extras = {}
     if world == 1 and not args.no_extras:
@@ -472,14 +529,11 @@ def main():
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": args.dtype, "data": "synthetic",
-                "config": {"workload": "configs[3]: synchronous all-reduce SGD round (Nesterov "
-                                       "momentum 0.9, wd 1e-4), aggregate momentum scope",
-                           "d_per_worker": d, "p": world, "parallelism": f"dp{world}",
-                           "grad_source": f"pool of {POOL} synthetic N(0,1) device buffers/worker",
-                           "l2": "inputs larger than L2 (~400 MB/step/worker working set)"},
+                "config": workload_config(d, world),
                 "gbs": step_bytes / (step_ms * 1e-3) / 1e9,
                 "gbs_note": "aggregation-step algorithmic HBM GB/s per GPU",
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "e2e_objective_plugin": e2e_plugin,
                 "gpu_launches": (k1 - k0) + (n1 - n0),
                 "gpu_launches_detail": {"kernels": k1 - k0, "nccl_calls": n1 - n0},
                 "per_kernel": per_kernel,
@@ -536,6 +590,84 @@ def run_extras(args, local, h):
             torch.cuda.empty_cache()
         except Exception as e:  # pragma: no cover
             out[name] = {"error": str(e)}
+    # run_sync's own call pattern: every round raises grad_norm_out
+    # (simulator.cpp:239) -- accumulated on the device, read once per run
+    name = "all-reduce p=1 x 25M with grad_norm_out (run_sync pattern)"
+    try:
+        from paper_1611_04581_b200.engine import Hyperparams
+        d = args.d
+        grp = Group(d, 1, dtype="f32", device=local, grad=True)
+        gen = torch.Generator(device=f"cuda:{local}")
+        gen.manual_seed(5)
+        pool = [torch.randn(d, generator=gen, device=f"cuda:{local}") for _ in range(POOL)]
+        ptrs = [t.data_ptr() for t in pool]
+        grp.copy_in_async(0, N.BUF_THETA, pool[0].data_ptr(), d)
+        grp.run_rounds(N.ALLREDUCE, h, 5, grad_pool=ptrs, grad_norm=True)
+        grp.sync()
+        stream = torch.cuda.ExternalStream(grp.stream(), device=f"cuda:{local}")
+        res = {}
+        for norm in (False, True):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            k = 50
+            e0.record(stream)
+            gn = grp.run_rounds(N.ALLREDUCE, h, k, grad_pool=ptrs, grad_norm=norm)
+            e1.record(stream)
+            grp.sync()
+            torch.cuda.synchronize()
+            res[norm] = (e0.elapsed_time(e1) / k, gn)
+        out[name] = {"ms_per_round": res[True][0], "ms_per_round_without_norm": res[False][0],
+                     "overhead": res[True][0] / res[False][0] - 1.0,
+                     "max_grad_norm": res[True][1],
+                     "param_updates_per_s": d / (res[True][0] * 1e-3)}
+        grp.close()
+        del pool
+        torch.cuda.empty_cache()
+    except Exception as e:  # pragma: no cover
+        out[name] = {"error": str(e)}
+    # the reference arm's own arithmetic on the GPU: fp64, gradient from the
+    # fused QuadraticObjective(spectrum 1, optimum 0) -- bit-exact with the
+    # reference in fp64 (tests/test_gpu_parity.py); 48 B/param
+    name = "all-reduce p=1 x 25M fp64, QuadraticObjective(1, 0) (reference arithmetic)"
+    try:
+        d = args.d
+        grp = Group(d, 1, dtype="f64", device=local, quadratic=True)
+        ones = torch.ones(d, dtype=torch.float64, device=f"cuda:{local}")
+        zeros = torch.zeros(d, dtype=torch.float64, device=f"cuda:{local}")
+        gen = torch.Generator(device=f"cuda:{local}")
+        gen.manual_seed(6)
+        th = torch.randn(d, generator=gen, device=f"cuda:{local}", dtype=torch.float64)
+        torch.cuda.synchronize()
+        grp.copy_in_async(0, N.BUF_SPECTRUM, ones.data_ptr(), d)
+        grp.copy_in_async(0, N.BUF_OPT, zeros.data_ptr(), d)
+        grp.copy_in_async(0, N.BUF_THETA, th.data_ptr(), d)
+        grp.run_rounds(N.ALLREDUCE, h, 3, grad="quadratic")
+        grp.sync()
+        stream = torch.cuda.ExternalStream(grp.stream(), device=f"cuda:{local}")
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        k = 30
+        e0.record(stream)
+        grp.run_rounds(N.ALLREDUCE, h, k, grad="quadratic")
+        e1.record(stream)
+        grp.sync()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / k
+        hbm, _ = peaks()
+        byts = 48 * d  # theta, delta, s, opt read + theta', delta' written, fp64
+        ref_s = cpu_reference(0, 1, d, 2, False, grad="quadratic") / 2 \
+            if not args.no_cpu else None
+        out[name] = {"ms_per_round": ms, "param_updates_per_s": d / (ms * 1e-3),
+                     "hbm_gbs": byts / (ms * 1e-3) / 1e9, "hbm_frac": byts / (ms * 1e-3) / 1e9 / hbm,
+                     "bytes_per_param": 48,
+                     "reference_cpu_param_updates_per_s": (d / ref_s) if ref_s else None,
+                     "reference_cpu_sample": "2 allreduce_round of the compiled reference, "
+                                             "QuadraticObjective(1, 0), p=1, 1 thread"}
+        grp.close()
+        del ones, zeros, th
+        torch.cuda.empty_cache()
+    except Exception as e:  # pragma: no cover
+        out[name] = {"error": str(e)}
     # F4: the asynchronous event loop in the library (dsgd_run_events): one
     # async_pull_event kernel per Poisson tick, 8 nodes x 10M on one GPU
     name = "async-pull p=8 x 10M (1 GPU, events)"

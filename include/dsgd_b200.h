@@ -287,6 +287,12 @@ dsgd_status dsgd_gossip_stale_step(dsgd_ctx* ctx, const dsgd_hyperparams* h,
 /* mix_toward protocols.cpp:42-51 for ONE local node, in place:
  * theta_i += beta * (partner - theta_i) (gossip_fresh_mix 265-269). */
 dsgd_status dsgd_mix_toward(dsgd_ctx* ctx, uint32_t local, const void* partner, double beta);
+/* The point a host Objective is evaluated at by compute_local_delta
+ * (protocols.cpp:90-93): out = theta + mu * delta_prev (theta when mu == 0),
+ * for one local node, into a device buffer of d dtype elements on the
+ * context stream -- the input of an Objective::stochastic_gradient plugin
+ * (objectives.hpp:44-49) whose result comes back as DSGD_GRAD_BUFFER. */
+dsgd_status dsgd_eval_point(dsgd_ctx* ctx, const dsgd_hyperparams* h, uint32_t local, void* out);
 /* pull_mix 161-171 / push_mix 195-228 without the SGD step */
 dsgd_status dsgd_pull_mix(dsgd_ctx* ctx, const uint32_t* partner_of);
 dsgd_status dsgd_push_mix(dsgd_ctx* ctx, const uint32_t* target_of);

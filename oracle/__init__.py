@@ -233,7 +233,7 @@ def _configure_ref(_ref):
                                     C.c_char_p, C.c_uint64]
     _ref.ref_time_rounds.restype = C.c_double
     _ref.ref_time_rounds.argtypes = [C.c_int, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int,
-                                     C.POINTER(Hyper)]
+                                     C.POINTER(Hyper), C.c_int]
     return _ref
 
 
@@ -613,9 +613,14 @@ def ref_stream(seed: int, kind: int, count: int, n: int = 0):
 
 
 def ref_time_rounds(protocol: int, p: int, d: int, rounds: int, threaded: bool,
-                    h: HyperParams) -> float:
+                    h: HyperParams, grad: str = "quadratic") -> float:
+    """Seconds for `rounds` rounds of the compiled reference (simulator
+    rules on 1 thread, or run_transport's threads); grad: 'quadratic'
+    (QuadraticObjective(1, 0)) or 'pool' (4 synthetic N(0,1) gradient
+    vectors through the Objective plugin slot, served in turn)."""
     hc = h.to_c()
-    sec = ref().ref_time_rounds(protocol, p, d, rounds, int(threaded), C.byref(hc))
+    sec = ref().ref_time_rounds(protocol, p, d, rounds, int(threaded), C.byref(hc),
+                                {"quadratic": 0, "pool": 1}[grad])
     if sec < 0:
         raise RuntimeError(ref().ref_last_error().decode())
     return sec

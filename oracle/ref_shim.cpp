@@ -8,6 +8,7 @@
 // bench.py.  Nothing here is product code; nothing is copied from the
 // reference -- this file only calls its public API (protocols.hpp,
 // simulator.hpp, transport.hpp).
+#include <atomic>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -47,6 +48,31 @@ class FixedGradientObjective : public Objective {
 
  private:
   std::vector<double> g_;
+};
+
+// A pool of synthetic N(0, 1) gradient vectors served in turn through the
+// plugin slot (thread-safe: run_transport's workers share one objective).
+class PoolGradientObjective : public Objective {
+ public:
+  PoolGradientObjective(std::size_t d, std::size_t n) : d_(d) {
+    for (std::size_t k = 0; k < n; ++k) {
+      RngStream s(0x9001 + k);
+      std::vector<double> g(d);
+      for (double& x : g) x = s.normal();
+      pool_.emplace_back(std::move(g));
+    }
+  }
+  std::size_t dim() const override { return d_; }
+  double value(const ParamVec&) const override { return 0.0; }
+  ParamVec gradient(const ParamVec&) const override {
+    return pool_[next_.fetch_add(1) % pool_.size()];
+  }
+  std::pair<double, double> convexity_params() const override { return {1.0, 1.0}; }
+
+ private:
+  std::size_t d_;
+  std::vector<ParamVec> pool_;
+  mutable std::atomic<std::size_t> next_{0};
 };
 
 thread_local std::string g_err;
@@ -455,7 +481,7 @@ int ref_ring_allreduce(std::uint32_t p, std::uint64_t d, const double* in, doubl
 // mode 1: the threaded transport backend run_transport (p worker threads,
 // +1 EA server thread).  Returns seconds for all rounds, or -1.
 double ref_time_rounds(int protocol, std::uint32_t p, std::uint64_t d, std::uint64_t rounds,
-                       int mode, const dsgdo_hyper* hp) {
+                       int mode, const dsgdo_hyper* hp, int grad_kind) {
   try {
     dsgdo_sim c{};
     c.protocol = protocol;
@@ -471,7 +497,14 @@ double ref_time_rounds(int protocol, std::uint32_t p, std::uint64_t d, std::uint
     c.seed = 1;
     c.run_id = "run/trial0";
     SimConfig cfg = to_sim(c);
-    QuadraticObjective obj(spec, ParamVec(opt));
+    // grad_kind 0: QuadraticObjective(spectrum 1, optimum 0); 1: a pool of 4
+    // synthetic N(0, 1) gradient vectors served in turn through the
+    // Objective plugin slot (the GPU bench's external-gradient pool)
+    QuadraticObjective quad(spec, ParamVec(opt));
+    std::unique_ptr<PoolGradientObjective> pool;
+    if (grad_kind == 1) pool = std::make_unique<PoolGradientObjective>(d, 4);
+    const Objective& obj = grad_kind == 1 ? static_cast<const Objective&>(*pool)
+                                          : static_cast<const Objective&>(quad);
     using clk = std::chrono::steady_clock;
     if (mode == 1) {
       // run_transport also builds the initial nodes and trace records; time

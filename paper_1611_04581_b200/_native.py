@@ -123,6 +123,7 @@ _SIGS = {
     "dsgd_gossip_stale_step": (C.c_int, [_P, C.POINTER(Hyper), C.POINTER(GradSpec), C.c_uint32,
                                          _P]),
     "dsgd_mix_toward": (C.c_int, [_P, C.c_uint32, _P, C.c_double]),
+    "dsgd_eval_point": (C.c_int, [_P, C.POINTER(Hyper), C.c_uint32, _P]),
     "dsgd_pull_mix": (C.c_int, [_P, _U32P]),
     "dsgd_push_mix": (C.c_int, [_P, _U32P]),
     "dsgd_ea_init_center": (C.c_int, [_P]),

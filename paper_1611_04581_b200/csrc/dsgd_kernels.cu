@@ -205,7 +205,7 @@ __device__ __forceinline__ void step_load(const StepArgs<T>& a, const NodeIO<T>&
   if constexpr (MODE == kModeApply) ld(ax, n.aux, k);
   if constexpr (MODE == kModeApplyDelta) ld(ax, n.partner ? n.partner : n.aux, k);  // avg_t
   if constexpr (MODE == kModeStep || MODE == kModePull || MODE == kModeStale ||
-                MODE == kModeArDelta) {
+                MODE == kModeArDelta || MODE == kModeLookahead) {
     ld(dp, n.delta, k);
   } else if constexpr (MODE == kModeApplyDelta) {
     if (a.agg)
@@ -213,7 +213,7 @@ __device__ __forceinline__ void step_load(const StepArgs<T>& a, const NodeIO<T>&
     else
       ld(dp, n.delta, k);  // per-node scope: own delta_prev
   }
-  if constexpr (MODE != kModeMix && MODE != kModeApply)
+  if constexpr (MODE != kModeMix && MODE != kModeApply && MODE != kModeLookahead)
     ld_grad_inputs(gb, s, o, xi, n, a.spec, a.opt, a.quad, k);
 }
 
@@ -256,6 +256,9 @@ __device__ __forceinline__ void step_store(const StepArgs<T>& a, const NodeIO<T>
                              a.wd, a.mu_nz, a.wd_pos, a.quad, norm, nacc);
     } else if constexpr (MODE == kModeApply) {
       out_t.v[l] = radd(x.v[l], ax.v[l]);
+    } else if constexpr (MODE == kModeLookahead) {
+      // la = theta; la.axpy(mu, delta_prev)  (protocols.cpp:92-93)
+      out_t.v[l] = a.mu_nz ? radd(x.v[l], rmul(a.mu, dp.v[l])) : x.v[l];
     } else if constexpr (MODE == kModeApplyDelta) {
       // theta_{t+1} = theta_t + avg_t  (protocols.cpp:126), then round t+1's
       // compute_local_delta at theta_{t+1}, in one pass
@@ -603,6 +606,7 @@ cudaError_t launch_step(int mode, const StepArgs<T>& a, int vec, uint32_t grid, 
     DSGD_STEP_CASE(kModeApply)
     DSGD_STEP_CASE(kModeAsync)
     DSGD_STEP_CASE(kModeApplyDelta)
+    DSGD_STEP_CASE(kModeLookahead)
     default:
       return cudaErrorInvalidValue;
   }

@@ -48,7 +48,8 @@ enum StepMode : int {
   kModeArDelta = 4,  // compute_local_delta -> aux            protocols.cpp:85-100
   kModeApply = 5,    // theta += aux (averaged delta)        protocols.cpp:125-129
   kModeAsync = 6,    // async_pull_event                      protocols.cpp:278-297
-  kModeApplyDelta = 7  // previous round's theta += avg fused with this round's delta
+  kModeApplyDelta = 7,  // previous round's theta += avg fused with this round's delta
+  kModeLookahead = 8    // out = theta + mu * delta_prev (compute_local_delta's evaluation point)
 };
 
 template <typename T>

@@ -2106,6 +2106,31 @@ dsgd_status dsgd_gossip_stale_step(dsgd_ctx* c, const dsgd_hyperparams* h,
   });
 }
 
+dsgd_status dsgd_eval_point(dsgd_ctx* c, const dsgd_hyperparams* h, uint32_t local, void* out) {
+  DSGD_TRY(check_ctx(c));
+  DSGD_TRY(flush_pending(c));
+  if (!h) return set_error(DSGD_EINVAL, "null hyperparams");
+  if (local >= c->n_local) return set_error(DSGD_EINVAL, "local node out of range");
+  if (!out) return set_error(DSGD_EINVAL, "null output buffer");
+  return dispatch(c, [&](auto z) -> dsgd_status {
+    using T = decltype(z);
+    dsgd::StepArgs<T> a{};
+    a.node[0].theta_in = as<T>(c->theta_ptr(local, c->cur));
+    a.node[0].theta_out = static_cast<T*>(out);
+    a.node[0].delta = as<T>(c->delta[local]);
+    a.d = c->d;
+    a.mu = (T)h->mu;
+    a.mu_nz = h->mu != 0.0;
+    a.n_local = 1;
+    const bool vec = aligned16(out);
+    const uint64_t W = vec ? 16 / sizeof(T) : 1;
+    a.blocks_per_node = blocks_for(c, (c->d / W + 1) / 2, 1);
+    LaunchScope ls(c, DSGD_K_OTHER);
+    DSGD_CUDA(dsgd::launch_step<T>(dsgd::kModeLookahead, a, vec, a.blocks_per_node, c->stream));
+    return DSGD_OK;
+  });
+}
+
 dsgd_status dsgd_mix_toward(dsgd_ctx* c, uint32_t local, const void* partner, double beta) {
   DSGD_TRY(check_ctx(c));
   DSGD_TRY(flush_pending(c));

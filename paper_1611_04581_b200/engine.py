@@ -367,6 +367,11 @@ class Group:
         hc = h.to_c()
         return self._run(self.lib.dsgd_async_pull_event, C.byref(hc), i, j, **kw)
 
+    def eval_point(self, h: Hyperparams, local: int, out_ptr: int) -> None:
+        """dsgd_eval_point: theta + mu * delta_prev of one node into a device buffer."""
+        hc = h.to_c()
+        N.check(self.lib.dsgd_eval_point(self._ctx, C.byref(hc), local, out_ptr))
+
     def pull_mix(self, partner_of) -> None:
         arr, ptr = _u32(partner_of)
         N.check(self.lib.dsgd_pull_mix(self._ctx, ptr))
@@ -409,9 +414,13 @@ class Group:
 
     def run_rounds(self, protocol: int, h: Hyperparams, rounds: int, scope: str = "aggregate",
                    grad=None, grad_pool: Optional[Sequence[int]] = None,
-                   host_noise_sigma: float = 0.0, noise: bool = False) -> None:
-        """run_sync's round loop (simulator.cpp:234-369) on this context."""
-        gs = self._grad(grad, noise, False)
+                   host_noise_sigma: float = 0.0, noise: bool = False,
+                   grad_norm: bool = False):
+        """run_sync's round loop (simulator.cpp:234-369) on this context;
+        grad_norm: also track max ||g|| like run_sync's &result.max_grad_norm
+        (device-side, read once at the end) and return it."""
+        self._norm.value = 0.0
+        gs = self._grad(grad, noise, grad_norm)
         pool = None
         if grad_pool:
             pool = (C.c_void_p * len(grad_pool))(*grad_pool)
@@ -422,6 +431,7 @@ class Group:
                        host_noise_sigma, rounds)
         rd._keep = (gs, pool)
         N.check(self.lib.dsgd_run_rounds(self._ctx, C.byref(rd)))
+        return self._norm.value if grad_norm else None
 
     def _run_desc(self, protocol: int, h: Hyperparams, rounds: int, scope: str, grad,
                   grad_pool, host_noise_sigma: float, noise: bool):
