@@ -405,11 +405,31 @@ __global__ void __launch_bounds__(kBlock) k_step_tma(const __grid_constant__ Ste
   block_signal(a.signal);
 }
 
-// Gossip-family step of one node with EVERY stream (NVLink partner, theta,
-// delta, gradient / s+opt, noise) staged through smem, 3 stages ahead.
+// Gossip-family step with EVERY stream (partner snapshot -- local, or a
+// peer GPU's over NVLink --, theta, delta, gradient / s+opt, noise) staged
+// through shared memory by cp.async.bulk, kStages tiles ahead, for any
+// number of local nodes: the tiles of all nodes form one work list
+// (node-major), so p workers on one GPU stream as one (configs[1]/[2]
+// single-GPU shapes) and one node per GPU gets deep NVLink pipelines.
+template <int MODE>
+struct StepSlots {
+  static constexpr bool kPartner =
+      MODE == kModePull || MODE == kModeStale || MODE == kModeMix || MODE == kModeAsync;
+  static constexpr bool kGrad = MODE != kModeMix;
+  static constexpr bool kDelta = kGrad && MODE != kModeAsync;  // async: no momentum term
+};
+
+template <typename T, int MODE>
+__host__ __device__ inline int step_nslots(int quad, bool noise) {
+  using S = StepSlots<MODE>;
+  return (S::kPartner ? 1 : 0) + 1 + (S::kDelta ? 1 : 0) +
+         (S::kGrad ? (quad ? 2 : 1) + (noise ? 1 : 0) : 0);
+}
+
 template <typename T, int MODE>
 __global__ void __launch_bounds__(kBlock) k_step_tma2(const __grid_constant__ StepArgs<T> a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  using S = StepSlots<MODE>;
   constexpr uint64_t TILE = st_tile<T>();
   constexpr uint32_t TB = (uint32_t)(TILE * sizeof(T));
   constexpr int W = Vec<T>::N;
@@ -417,46 +437,60 @@ __global__ void __launch_bounds__(kBlock) k_step_tma2(const __grid_constant__ St
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
   T* stage = reinterpret_cast<T*>(smem_raw + 128);
   if (!block_wait(a.wait)) return;
-  const NodeIO<T>& n = a.node[0];
-  const T* src[6];
+  const bool noise = a.node[0].noise != nullptr;  // the same for every node of a launch
+  // slot layout (identical for every node)
   int q = 0;
-  src[q++] = n.partner;   // slot 0: the peer snapshot (NVLink)
-  src[q++] = n.theta_in;  // slot 1
-  const bool mix_only = MODE == kModeMix;
-  const bool uses_dp = !mix_only && MODE != kModeAsync;  // async: no momentum term
-  const int s_dp = q;
-  if (uses_dp) src[q++] = n.delta;
-  const int s_g = q;
-  if (!mix_only) {
-    if (a.quad) {
-      src[q++] = a.spec;
-      src[q++] = a.opt;
-    } else {
-      src[q++] = n.grad;
-    }
-  }
-  const int s_nz = q;
-  if (!mix_only && n.noise) src[q++] = n.noise;
+  const int s_p = S::kPartner ? q++ : -1;
+  const int s_x = q++;
+  const int s_dp = S::kDelta ? q++ : -1;
+  const int s_g = S::kGrad ? q : -1;
+  if (S::kGrad) q += a.quad ? 2 : 1;
+  const int s_nz = (S::kGrad && noise) ? q++ : -1;
   const int nsl = q;
   const uint64_t nt = a.d / TILE;
+  const uint64_t total = nt * a.n_local;
+  auto issue = [&](uint64_t work, int sg) {
+    const uint32_t node = (uint32_t)(work / nt);
+    const uint64_t off = (work - (uint64_t)node * nt) * TILE;
+    const NodeIO<T>& n = a.node[node];
+    T* dst = stage + (uint64_t)sg * nsl * TILE;
+    mbar_expect_tx(&bars[sg], TB * nsl);
+    if (S::kPartner) bulk_g2s(dst + (uint64_t)s_p * TILE, n.partner + off, TB, &bars[sg]);
+    bulk_g2s(dst + (uint64_t)s_x * TILE, n.theta_in + off, TB, &bars[sg]);
+    if (S::kDelta) bulk_g2s(dst + (uint64_t)s_dp * TILE, n.delta + off, TB, &bars[sg]);
+    if (S::kGrad) {
+      if (a.quad) {
+        bulk_g2s(dst + (uint64_t)s_g * TILE, a.spec + off, TB, &bars[sg]);
+        bulk_g2s(dst + (uint64_t)(s_g + 1) * TILE, a.opt + off, TB, &bars[sg]);
+      } else {
+        bulk_g2s(dst + (uint64_t)s_g * TILE, n.grad + off, TB, &bars[sg]);
+      }
+      if (noise) bulk_g2s(dst + (uint64_t)s_nz * TILE, n.noise + off, TB, &bars[sg]);
+    }
+  };
   if (threadIdx.x == 0) {
     for (int sg = 0; sg < kStages; ++sg) mbar_init(&bars[sg], 1);
     fence_mbar_init();
     for (int sg = 0; sg < kStages; ++sg) {
-      const uint64_t tile = blockIdx.x + (uint64_t)sg * gridDim.x;
-      if (tile < nt) {
-        mbar_expect_tx(&bars[sg], TB * nsl);
-        for (int i = 0; i < nsl; ++i)
-          bulk_g2s(stage + ((uint64_t)sg * nsl + i) * TILE, src[i] + tile * TILE, TB, &bars[sg]);
-      }
+      const uint64_t work = blockIdx.x + (uint64_t)sg * gridDim.x;
+      if (work < total) issue(work, sg);
     }
   }
   __syncthreads();
-  const bool norm = n.norm != nullptr;
   double nacc = 0.0;
+  uint32_t cur = 0xffffffffu;  // node of the running norm accumulator
   for (uint64_t j = 0;; ++j) {
-    const uint64_t tile = blockIdx.x + j * gridDim.x;
-    if (tile >= nt) break;
+    const uint64_t work = blockIdx.x + j * gridDim.x;
+    if (work >= total) break;
+    const uint32_t node = (uint32_t)(work / nt);
+    const uint64_t tile = work - (uint64_t)node * nt;
+    if (node != cur) {  // CTA-uniform: flush the previous node's sum of g^2
+      if (cur != 0xffffffffu) block_add_double(nacc, a.node[cur].norm);
+      nacc = 0.0;
+      cur = node;
+    }
+    const NodeIO<T>& n = a.node[node];
+    const bool norm = n.norm != nullptr;
     const int sg = (int)(j % kStages);
     mbar_wait(&bars[sg], (uint32_t)((j / kStages) & 1));
     const T* base = stage + (uint64_t)sg * nsl * TILE + (uint64_t)threadIdx.x * W;
@@ -470,17 +504,17 @@ __global__ void __launch_bounds__(kBlock) k_step_tma2(const __grid_constant__ St
 #pragma unroll
         for (int l = 0; l < W; ++l) dst.v[l] = v.t[l];
       };
-      rd(0, in[u].xj);
-      rd(1, in[u].x);
-      if (!mix_only) {
-        if (uses_dp) rd(s_dp, in[u].dp);
+      if (S::kPartner) rd(s_p, in[u].xj);
+      rd(s_x, in[u].x);
+      if (S::kDelta) rd(s_dp, in[u].dp);
+      if (S::kGrad) {
         if (a.quad) {
           rd(s_g, in[u].s);
           rd(s_g + 1, in[u].o);
         } else {
           rd(s_g, in[u].gb);
         }
-        if (n.noise) {
+        if (noise) {
           rd(s_nz, in[u].xi);
         } else if (n.nsigma != T(0)) {
           float z[W];
@@ -493,54 +527,58 @@ __global__ void __launch_bounds__(kBlock) k_step_tma2(const __grid_constant__ St
         }
       }
     }
-    __syncthreads();
+    __syncthreads();  // stage sg consumed by every thread
     if (threadIdx.x == 0) {
       const uint64_t nxt = blockIdx.x + (j + kStages) * gridDim.x;
-      if (nxt < nt) {
-        mbar_expect_tx(&bars[sg], TB * nsl);
-        for (int i = 0; i < nsl; ++i)
-          bulk_g2s(stage + ((uint64_t)sg * nsl + i) * TILE, src[i] + nxt * TILE, TB, &bars[sg]);
-      }
+      if (nxt < total) issue(nxt, sg);
     }
     const uint64_t k0 = tile * TILE + (uint64_t)threadIdx.x * W;
     step_store<T, MODE, true>(a, n, k0, in[0], norm, nacc);
     step_store<T, MODE, true>(a, n, k0 + (uint64_t)kBlock * W, in[1], norm, nacc);
   }
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t kk = nt * TILE + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; kk < a.d;
-       kk += stride)
-    step_group<T, MODE, false>(a, n, kk, norm, nacc);
-  block_add_double(nacc, n.norm);
+  if (cur != 0xffffffffu) block_add_double(nacc, a.node[cur].norm);
+  // ragged tails [nt * TILE, d) of every node: the scalar path
+  const uint64_t tail = a.d - nt * TILE;
+  if (tail) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint32_t node = 0; node < a.n_local; ++node) {
+      const NodeIO<T>& n = a.node[node];
+      double tacc = 0.0;
+      for (uint64_t kk = nt * TILE + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; kk < a.d;
+           kk += stride)
+        step_group<T, MODE, false>(a, n, kk, n.norm != nullptr, tacc);
+      block_add_double(tacc, n.norm);
+    }
+  }
   block_signal(a.signal);
 }
 
 template <typename T, int MODE>
-cudaError_t launch_step_tma(const StepArgs<T>& a, cudaStream_t s) {
-  static const bool all_staged = [] {  // DSGD_GOSSIP_STAGE_ALL=0: stage the partner only
-    const char* e = getenv("DSGD_GOSSIP_STAGE_ALL");
-    return !(e && e[0] == '0');
-  }();
-  if (all_staged) {
-    const int nsl = 2 + (MODE == kModeMix ? 0 : 1 + (a.quad ? 2 : 1) + (a.node[0].noise ? 1 : 0));
-    const size_t smem = 128 + (size_t)3 * nsl * st_tile<T>() * sizeof(T);
-    static size_t attr = 0;
-    if (attr < smem) {
-      cudaFuncSetAttribute(k_step_tma2<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
-      attr = smem;
-    }
-    int resident = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_step_tma2<T, MODE>, kBlock, smem);
-    if (resident < 1) resident = 1;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const uint64_t tiles = a.d / st_tile<T>();
-    uint32_t g = (uint32_t)sms * (uint32_t)resident;
-    if (tiles < g) g = (uint32_t)(tiles ? tiles : 1);
-    DSGD_COUNTED(k_step_tma2<T, MODE><<<g, kBlock, smem, s>>>(a));
-    return cudaGetLastError();
+cudaError_t launch_step_staged(const StepArgs<T>& a, cudaStream_t s) {
+  const int nsl = step_nslots<T, MODE>(a.quad, a.node[0].noise != nullptr);
+  const size_t smem = 128 + (size_t)3 * nsl * st_tile<T>() * sizeof(T);
+  static size_t attr = 0;
+  if (attr < smem) {
+    cudaFuncSetAttribute(k_step_tma2<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = smem;
   }
+  int resident = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_step_tma2<T, MODE>, kBlock, smem);
+  if (resident < 1) resident = 1;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t work = a.d / st_tile<T>() * a.n_local;
+  uint32_t g = (uint32_t)sms * (uint32_t)resident;
+  if (work < g) g = (uint32_t)(work ? work : 1);
+  DSGD_COUNTED(k_step_tma2<T, MODE><<<g, kBlock, smem, s>>>(a));
+  return cudaGetLastError();
+}
+
+// Partner-only staging (DSGD_GOSSIP_STAGE_ALL=0), one node per GPU.
+template <typename T, int MODE>
+cudaError_t launch_step_tma(const StepArgs<T>& a, cudaStream_t s) {
   const size_t smem = 128 + (size_t)kStStages * st_tile<T>() * sizeof(T);
   static int resident = 0;
   if (!resident) {
@@ -561,30 +599,27 @@ cudaError_t launch_step_tma(const StepArgs<T>& a, cudaStream_t s) {
 
 template <typename T>
 cudaError_t launch_step(int mode, const StepArgs<T>& a, int vec, uint32_t grid, cudaStream_t s) {
-  // one async event (single context): every stream staged, in place on node i
-  if (mode == kModeAsync && a.tma_partner && vec && a.n_local == 1) {
-    const int nsl = 2 + (a.quad ? 2 : 1) + (a.node[0].noise ? 1 : 0);
-    const size_t smem = 128 + (size_t)3 * nsl * st_tile<T>() * sizeof(T);
-    static size_t attr = 0;
-    if (attr < smem) {
-      cudaFuncSetAttribute(k_step_tma2<T, kModeAsync>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
-      attr = smem;
+  static const bool staged = [] {  // DSGD_STEP_STAGED=0: the LDG kernels
+    const char* e = getenv("DSGD_STEP_STAGED");
+    return !(e && e[0] == '0');
+  }();
+  static const bool all_staged = [] {  // DSGD_GOSSIP_STAGE_ALL=0: stage the peer partner only
+    const char* e = getenv("DSGD_GOSSIP_STAGE_ALL");
+    return !(e && e[0] == '0');
+  }();
+  // the staged kernel needs every node's streams 16-B aligned and a whole
+  // tile; one node per GPU whose partner is remote always stages it
+  const bool tiles = a.d >= st_tile<T>();
+  if (vec && tiles && (staged || a.tma_partner) && (all_staged || !a.tma_partner)) {
+    switch (mode) {
+      case kModeStep: return launch_step_staged<T, kModeStep>(a, s);
+      case kModePull: return launch_step_staged<T, kModePull>(a, s);
+      case kModeStale: return launch_step_staged<T, kModeStale>(a, s);
+      case kModeMix: return launch_step_staged<T, kModeMix>(a, s);
+      case kModeAsync: return launch_step_staged<T, kModeAsync>(a, s);
+      default: break;
     }
-    int resident = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_step_tma2<T, kModeAsync>, kBlock,
-                                                  smem);
-    if (resident < 1) resident = 1;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const uint64_t tiles = a.d / st_tile<T>();
-    uint32_t g = (uint32_t)sms * (uint32_t)resident;
-    if (tiles < g) g = (uint32_t)(tiles ? tiles : 1);
-    DSGD_COUNTED(k_step_tma2<T, kModeAsync><<<g, kBlock, smem, s>>>(a));
-    return cudaGetLastError();
   }
-  // one node whose partner is a peer GPU: stage the NVLink stream in smem
   if (a.tma_partner && vec && a.n_local == 1 && a.blocks_per_node == grid) {
     if (mode == kModePull) return launch_step_tma<T, kModePull>(a, s);
     if (mode == kModeStale) return launch_step_tma<T, kModeStale>(a, s);
