@@ -6,6 +6,7 @@ Median of `--reps` repetitions of `--rounds` rounds each; prints one JSON line
 per measurement plus the host's CPU model and thread count.
 
     python tools/cpu_reference.py [--rounds 1] [--reps 3]
+    python tools/cpu_reference.py --sweep [--max-seconds 1800]   (configs[4])
 
 Test/measurement infrastructure (it executes oracle/_ref, never the product)."""
 import argparse
@@ -30,11 +31,67 @@ def host():
     return {"cpu_model": model, "nproc": len(os.sched_getaffinity(0))}
 
 
+def mem_bytes():
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+def sweep(a):
+    """configs[4]: d = 1M..1B per worker x {pull-gossip, elastic-avg,
+    all-reduce} x p = 2/4/8, one round each (the reference's cost is linear
+    in d), through the reference's threaded transport (p worker threads, +1
+    EASGD server) -- its own parallel path -- and, up to 64M, the
+    single-thread simulator rules.  Sizes whose fp64 state (~6 vectors of
+    d doubles per node) exceeds half the available RAM are skipped and
+    reported as such; the sweep stops issuing new sizes after
+    --max-seconds."""
+    import time
+    import oracle as O
+    h = O.HyperParams(alpha0=0.1, anneal_at=(), mu=0.9, weight_decay=1e-4, beta_ea=0.1)
+    avail = mem_bytes()
+    print(json.dumps({"host": host(), "mem_available_bytes": avail}), flush=True)
+    protos = [("pull-gossip", O.PULL), ("elastic-avg", O.ELASTIC), ("all-reduce", O.ALLREDUCE)]
+    t_start = time.time()
+    for d in (1 << 20, 4 << 20, 16 << 20, 64 << 20, 256 << 20, 1 << 30):
+        for p in (2, 4, 8):
+            for name, proto in protos:
+                need = 6 * 8 * d * p
+                if avail and need > avail // 2:
+                    print(json.dumps({"config": "configs[4]", "protocol": name, "p": p, "d": d,
+                                      "skipped": f"fp64 state ~{need / 2**30:.0f} GiB > half of "
+                                                 f"{avail / 2**30:.0f} GiB available"}), flush=True)
+                    continue
+                if time.time() - t_start > a.max_seconds:
+                    print(json.dumps({"config": "configs[4]", "protocol": name, "p": p, "d": d,
+                                      "skipped": "time budget"}), flush=True)
+                    continue
+                for threaded in ((True, False) if d <= (64 << 20) else (True,)):
+                    sec = O.ref_time_rounds(proto, p, d, 1, threaded, h, "pool")
+                    print(json.dumps({"config": "configs[4]", "protocol": name, "p": p, "d": d,
+                                      "path": "run_transport (threads)" if threaded
+                                              else "simulator rules (1 thread)",
+                                      "threads": (p + (1 if proto == O.ELASTIC else 0))
+                                      if threaded else 1,
+                                      "s_per_round": sec, "param_updates_per_s": p * d / sec,
+                                      "grad": "pool of 4 synthetic N(0,1) vectors (plugin slot)"}),
+                          flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rounds", type=int, default=1)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--max-seconds", type=float, default=1800)
     a = ap.parse_args()
+    if a.sweep:
+        return sweep(a)
     import oracle as O
     h = O.HyperParams(alpha0=0.1, anneal_at=(), mu=0.9, weight_decay=1e-4, beta_ea=0.1)
     cases = [  # (config, protocol, p, d, threaded)
