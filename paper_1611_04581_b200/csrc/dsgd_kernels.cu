@@ -716,18 +716,20 @@ __device__ __forceinline__ void nvls_group(const float* x, float* y, float inv_d
                "f"(c), "f"(d)
                : "memory");
 }
-__device__ __forceinline__ void nvls_group4(const float* x, float* y, uint64_t step, float div) {
-  float r[16];
+// U switch reductions in flight per thread (U x 16 B), then U multicast stores
+template <int U>
+__device__ __forceinline__ void nvls_groupU(const float* x, float* y, uint64_t step, float div) {
+  float r[4 * U];
 #pragma unroll
-  for (int u = 0; u < 4; ++u)
+  for (int u = 0; u < U; ++u)
     asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
                  : "=f"(r[4 * u]), "=f"(r[4 * u + 1]), "=f"(r[4 * u + 2]), "=f"(r[4 * u + 3])
                  : "l"(x + u * step)
                  : "memory");
 #pragma unroll
-  for (int q = 0; q < 16; ++q) r[q] = __fdiv_rn(r[q], div);
+  for (int q = 0; q < 4 * U; ++q) r[q] = __fdiv_rn(r[q], div);
 #pragma unroll
-  for (int u = 0; u < 4; ++u)
+  for (int u = 0; u < U; ++u)
     asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(y + u * step),
                  "f"(r[4 * u]), "f"(r[4 * u + 1]), "f"(r[4 * u + 2]), "f"(r[4 * u + 3])
                  : "memory");
@@ -745,7 +747,7 @@ __device__ __forceinline__ void nvls_scalar(const double* x, double* y, double d
   asm volatile("multimem.st.relaxed.sys.global.f64 [%0], %1;" ::"l"(y), "d"(a) : "memory");
 }
 
-template <typename T>
+template <typename T, int U>
 __global__ void __launch_bounds__(1024) k_ar_nvls(const __grid_constant__ ArNvlsArgs<T> a) {
   if (!block_wait(a.wait)) return;
   fence_proxy_alias();  // peers wrote x through their unicast mappings
@@ -756,8 +758,8 @@ __global__ void __launch_bounds__(1024) k_ar_nvls(const __grid_constant__ ArNvls
     // lo is a multiple of 4 elements (16 B): vector body, scalar tail
     const uint64_t nv = (a.hi - a.lo) / 4;
     uint64_t v = tid;
-    for (; v + 3 * stride < nv; v += 4 * stride)  // four switch reductions in flight
-      nvls_group4(a.x_mc + a.lo + 4 * v, a.avg_mc + a.lo + 4 * v, 4 * stride, div);
+    for (; v + (U - 1) * stride < nv; v += U * stride)  // U switch reductions in flight
+      nvls_groupU<U>(a.x_mc + a.lo + 4 * v, a.avg_mc + a.lo + 4 * v, 4 * stride, div);
     for (; v < nv; v += stride)
       nvls_group(a.x_mc + a.lo + 4 * v, a.avg_mc + a.lo + 4 * v, div);
     for (uint64_t k = a.lo + 4 * nv + tid; k < a.hi; k += stride)
@@ -780,13 +782,26 @@ cudaError_t launch_ar_nvls(const ArNvlsArgs<T>& a, uint32_t grid, cudaStream_t s
     const int kb = e ? atoi(e) : 120;  // measured best at p = 4 (r1_tune_allreduce_n4/split/)
     return kb < 0 ? 0 : (kb > 200 ? 200 : kb) * 1024;
   }();
+  static const int unroll = [] {  // DSGD_NVLS_UNROLL: switch reductions in flight per thread
+    const char* e = getenv("DSGD_NVLS_UNROLL");
+    const int u = e ? atoi(e) : 4;
+    return u >= 8 ? 8 : (u >= 4 ? 4 : 2);
+  }();
   static bool attr = false;
   if (pad && !attr) {
-    cudaFuncSetAttribute(k_ar_nvls<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad);
+    cudaFuncSetAttribute(k_ar_nvls<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad);
+    cudaFuncSetAttribute(k_ar_nvls<T, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad);
+    cudaFuncSetAttribute(k_ar_nvls<T, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad);
     attr = true;
   }
   // one padded CTA per SM: 1024 threads keep enough switch reductions in flight
-  DSGD_COUNTED(k_ar_nvls<T><<<grid, pad ? 1024 : kBlock, pad, s>>>(a));
+  const int threads = pad ? 1024 : kBlock;
+  if (unroll == 8)
+    DSGD_COUNTED(k_ar_nvls<T, 8><<<grid, threads, pad, s>>>(a));
+  else if (unroll == 2)
+    DSGD_COUNTED(k_ar_nvls<T, 2><<<grid, threads, pad, s>>>(a));
+  else
+    DSGD_COUNTED(k_ar_nvls<T, 4><<<grid, threads, pad, s>>>(a));
   return cudaGetLastError();
 }
 
