@@ -75,7 +75,7 @@ def main():
                     bound = max(28 * d / (hbm * 1e9), 4 * d / (nv * 1e9))
                 else:
                     be = "peer-read"
-                    bound = max(24 * d / (hbm * 1e9), 4 * d / (nv * 1e9))  # one puller/GPU
+                    bound = gossip_bound(world, d, 3, a.rounds, hbm, nv)
                 if rank == 0:
                     print(json.dumps({"protocol": name, "backend": be, "d": d, "gpus": world,
                                       "ms_per_round": ms,
@@ -89,6 +89,31 @@ def main():
                     print(json.dumps({"protocol": name, "d": d, "error": str(e)}), flush=True)
             dist.barrier()
     dist.destroy_process_group()
+
+
+def gossip_bound(world, d, warm, rounds, hbm, nv):
+    """Mean over the timed rounds of the busiest GPU's bound, from the
+    rounds' actual partner maps (the reference partner streams the run
+    draws): GPU i reads 4 B/param from a remote partner and serves 4 B/param
+    to each remote puller over NVLink, and streams (24 + 4 r_i) B/param of
+    HBM (quadratic objective: theta, delta, s, opt read, theta', delta'
+    written, + the snapshot served to r_i pullers)."""
+    from paper_1611_04581_b200.engine import Stream, draw_pull_partners
+    st = [Stream.make(1, "run/trial0", i, "partner-choice") for i in range(world)]
+    total = 0.0
+    for r in range(warm + rounds):
+        pm = draw_pull_partners(st) if r > 0 else list(range(world))  # round 0: ungated
+        if r < warm:
+            continue
+        worst = 0.0
+        for i in range(world):
+            pullers = sum(1 for q in range(world) if pm[q] == i and q != i)
+            t_in = (4 * d if pm[i] != i else 0) / (nv * 1e9)
+            t_out = 4 * d * pullers / (nv * 1e9)
+            t_hbm = (24 + 4 * pullers) * d / (hbm * 1e9)
+            worst = max(worst, t_in, t_out, t_hbm)
+        total += worst
+    return total / rounds
 
 
 def _run(g, proto, h, rounds, noise):
