@@ -213,6 +213,10 @@ def _configure_ref(_ref):
     _ref.ref_derive_stream_seed.argtypes = [C.c_uint64, C.c_char_p, C.c_uint32, C.c_int]
     _ref.ref_stream_draws.argtypes = [C.c_uint64, C.c_int, C.c_uint32, C.c_uint64, C.c_void_p]
     _ref.ref_run.argtypes = [C.POINTER(Sim), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    _ref.ref_run_max_grad_norm.argtypes = [C.POINTER(Sim), C.c_void_p]
+    if hasattr(_ref, "ref_run_resident"):  # the integration harness only
+        _ref.ref_run_resident.argtypes = [C.POINTER(Sim), C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.c_void_p, C.c_void_p]
     _ref.ref_run_transport.argtypes = [C.POINTER(Sim), C.c_void_p, C.c_void_p, C.c_void_p,
                                        C.c_void_p, C.c_uint64]
     _ref.ref_round.argtypes = [C.c_int, C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p,
@@ -560,6 +564,27 @@ def ref_run(cfg: SimConfig, transport: bool = False, chaos_seed: int = 0):
     else:
         _ref_check(ref().ref_run(C.byref(s), _ptr(theta), _ptr(dprev), _ptr(t), _ptr(center)))
     return theta, dprev, t, center
+
+
+def ref_run_max_grad_norm(cfg: SimConfig) -> float:
+    """RunResult::max_grad_norm of the reference's run_simulation."""
+    out = C.c_double(0.0)
+    s = cfg.to_c()
+    _ref_check(ref().ref_run_max_grad_norm(C.byref(s), C.byref(out)))
+    return out.value
+
+
+def ref_run_resident(cfg: SimConfig):
+    """integration/run_sync_b200.cpp through the harness (ref_library):
+    (theta, dprev, t, center, max_grad_norm)."""
+    p, d = cfg.p, cfg.d
+    theta, dprev = np.zeros((p, d)), np.zeros((p, d))
+    t, center = np.zeros(p, dtype=np.uint64), np.zeros(d)
+    gn = C.c_double(0.0)
+    s = cfg.to_c()
+    _ref_check(ref().ref_run_resident(C.byref(s), _ptr(theta), _ptr(dprev), _ptr(t),
+                                      _ptr(center), C.byref(gn)))
+    return theta, dprev, t, center, gn.value
 
 
 def ref_run_traced(cfg: SimConfig, trace_every: int, max_records: int = 4096):

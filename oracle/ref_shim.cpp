@@ -30,6 +30,9 @@
 #ifdef REF_HAVE_TRACE_IO
 #include "dsgd/trace_io.hpp"
 #endif
+#ifdef REF_B200_RESIDENT  // the integration harness: run_sync with the state on the GPU
+#include "run_sync_b200.hpp"
+#endif
 
 using namespace dsgd;
 
@@ -317,6 +320,43 @@ long ref_run_traced(const dsgdo_sim* c, std::uint64_t trace_every, double* rec,
       jsonl[n] = 0;
     }
     return static_cast<long>(r.trace.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+#ifdef REF_B200_RESIDENT
+// integration/run_sync_b200.cpp: run_sync with the node state resident on
+// the GPU (one dsgd_run_rounds); also returns max_grad_norm.
+int ref_run_resident(const dsgdo_sim* c, double* theta, double* dprev, std::uint64_t* t,
+                     double* center, double* max_grad_norm) {
+  try {
+    const SimConfig cfg = to_sim(*c);
+    QuadraticObjective obj(std::vector<double>(c->spectrum, c->spectrum + c->d),
+                           ParamVec(std::vector<double>(c->opt, c->opt + c->d)));
+    const RunResult r = dsgd_b200::run_sync_resident(cfg, obj);
+    export_nodes(r.final_nodes, c->d, theta, dprev, t);
+    if (center && r.final_server)
+      std::memcpy(center, r.final_server->theta_center.raw(), sizeof(double) * c->d);
+    if (max_grad_norm) *max_grad_norm = r.max_grad_norm;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+#endif
+
+// run_simulation's max_grad_norm (run_sync passes &result.max_grad_norm
+// to every rule, simulator.cpp:239-344).
+int ref_run_max_grad_norm(const dsgdo_sim* c, double* max_grad_norm) {
+  try {
+    const SimConfig cfg = to_sim(*c);
+    QuadraticObjective obj(std::vector<double>(c->spectrum, c->spectrum + c->d),
+                           ParamVec(std::vector<double>(c->opt, c->opt + c->d)));
+    *max_grad_norm = run_simulation(cfg, obj).max_grad_norm;
+    return 0;
   } catch (const std::exception& e) {
     g_err = e.what();
     return -1;

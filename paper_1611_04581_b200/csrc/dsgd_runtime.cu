@@ -237,6 +237,8 @@ struct dsgd_ctx {
   // multi-GPU
   std::shared_ptr<InprocGroup> grp;  // in-process group (null: one process per GPU)
   unsigned long long reduce_t = 0;   // in-process two-shot: round of the deferred reduces
+  std::vector<uint32_t> fresh_map;   // in-process gossip-fresh: the deferred mix's partners
+  double fresh_beta = 0.0;
   bool connected = false;
   std::vector<PeerNode> peers;   // all p nodes
   std::vector<void*> ipc_opened;
@@ -2041,6 +2043,23 @@ dsgd_status dsgd_gossip_fresh_round(dsgd_ctx* c, const dsgd_hyperparams* h,
     DSGD_TRY(do_local_step<T>(c, h, gs));
     finish_round(c, true, true);
     c->rounds_done -= 1;
+    if (c->grp && c->distributed()) {
+      // in-process group: the mix reads the partner's post-step theta of this
+      // round, so every rank's step is issued before any mix; the last rank
+      // issues the mixes of all ranks, in rank order
+      c->fresh_map.assign(partner_of, partner_of + c->p);
+      c->fresh_beta = h->beta_gossip;
+      if (c->first + 1 == c->p)
+        for (dsgd_ctx* r : c->grp->ctx) {
+          DeviceGuard dg(r->device);
+          GradSel none;
+          none.quad = 1;
+          DSGD_TRY(do_pull<T>(r, nullptr, none, r->fresh_map.data(), dsgd::kModeMix,
+                              (T)r->fresh_beta));
+          finish_round(r, true, false);
+        }
+      return norm_end(c, gs, g);
+    }
     DSGD_TRY(do_pull<T>(c, nullptr, gs, partner_of, dsgd::kModeMix, (T)h->beta_gossip));
     finish_round(c, true, false);
     return norm_end(c, gs, g);

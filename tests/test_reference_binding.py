@@ -137,3 +137,26 @@ def test_binding_errors_keep_reference_types():
             O.ref_round("pull", n, h, partner=np.array([0, 5], dtype=np.uint32), spec=np.ones(3))
         with pytest.raises(ValueError, match="push target must differ from sender"):
             O.ref_round("push", n, h, partner=np.array([0, 0], dtype=np.uint32), spec=np.ones(3))
+
+
+@pytest.mark.gpu
+@needs_lib
+@pytest.mark.parametrize("name", sorted(n for n, c in run_cases().items()
+                                        if not c.poisson and c.protocol != O.ASYNC_PULL))
+def test_resident_run_sync_matches_golden(name):
+    """integration/run_sync_b200.cpp: run_sync with
+    the node state on the GPU for the whole run (one dsgd_run_rounds) --
+    byte-identical final state, and max_grad_norm (accumulated on the
+    device, read once) equal to the reference's within its summation order."""
+    cfg = run_cases()[name]
+    g = np.load(os.path.join(GOLD, "runs.npz"))
+    with O.ref_library(HARNESS):
+        th, dp, t, c, gn = O.ref_run_resident(cfg)
+    assert same(th, g[f"{name}_theta"])
+    assert same(dp, g[f"{name}_dprev"])
+    assert t.tolist() == g[f"{name}_t"].tolist()
+    if cfg.protocol == O.ELASTIC:
+        assert same(c, g[f"{name}_center"])
+    if O.ref_available():  # this container: the unmodified reference's own number
+        assert gn == pytest.approx(O.ref_run_max_grad_norm(cfg), rel=1e-12)
+    assert gn > 0.0
