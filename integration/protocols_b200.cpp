@@ -117,7 +117,9 @@ dsgd_grad_spec prepare(DevCtx& x, std::span<NodeState> nodes, std::span<const Ob
     const QuadraticObjective* q = as_quadratic(objs[0]);
     if (q->dim() != d) throw std::invalid_argument("ParamVec dimension mismatch");
     const std::vector<double>& s = q->spectrum();
-    const std::vector<double>& o = q->optimum()->values();
+    // optimum() returns the optional by value: keep it alive while `o` is used
+    const std::optional<ParamVec> opt = q->optimum();
+    const std::vector<double>& o = opt->values();
     if (!x.quad_set || x.spec != s || x.opt != o) {
       check(dsgd_set_vector(x.c, 0, DSGD_BUF_SPECTRUM, s.data()));
       check(dsgd_set_vector(x.c, 0, DSGD_BUF_OPT, o.data()));

@@ -90,6 +90,14 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -111,6 +119,21 @@ __device__ __forceinline__ bool wait_flag(const unsigned long long* p, unsigned 
     }
     __nanosleep(ns);
     if (ns < 1024) ns <<= 1;
+  }
+  return true;
+}
+
+// wait_flag for a flag written on this GPU (gpu-scope acquire).
+__device__ __forceinline__ bool wait_flag_gpu(const unsigned long long* p, unsigned long long need,
+                                              unsigned long long timeout_ns, unsigned int* error) {
+  if (ld_acquire_gpu(p) >= need) return true;
+  const unsigned long long t0 = globaltimer();
+  while (ld_acquire_gpu(p) < need) {
+    if (globaltimer() - t0 > timeout_ns) {
+      atomicExch(error, 1u);
+      return false;
+    }
+    __nanosleep(64);
   }
   return true;
 }

@@ -7,10 +7,31 @@
 // sweep over HBM.  The per-element arithmetic is written once (sgd_delta,
 // mix) in the reference's exact operation order; see dsgd_device.cuh.
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "dsgd_kernels.cuh"
 
 namespace dsgd {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: one process
+// may drive several GPUs (in-process rank groups), so remember what was set
+// for every (kernel, current device) pair.
+template <typename K>
+void smem_attr(K* kernel, size_t smem) {
+  static std::mutex m;
+  static std::map<std::pair<const void*, int>, size_t> set;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(m);
+  size_t& have = set[{(const void*)kernel, dev}];
+  if (have < smem) {
+    cudaFuncSetAttribute((const void*)kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    have = smem;
+  }
+}
 
 // Kernels issued by this thread (tail launches included): dsgd_launch_count.
 // (the file is compiled once per dtype, DSGD_KERNEL_DTYPE = 32 / 64, in
@@ -557,12 +578,7 @@ template <typename T, int MODE>
 cudaError_t launch_step_staged(const StepArgs<T>& a, cudaStream_t s) {
   const int nsl = step_nslots<T, MODE>(a.quad, a.node[0].noise != nullptr);
   const size_t smem = 128 + (size_t)3 * nsl * st_tile<T>() * sizeof(T);
-  static size_t attr = 0;
-  if (attr < smem) {
-    cudaFuncSetAttribute(k_step_tma2<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    attr = smem;
-  }
+  smem_attr(k_step_tma2<T, MODE>, smem);
   int resident = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_step_tma2<T, MODE>, kBlock, smem);
   if (resident < 1) resident = 1;
@@ -580,10 +596,9 @@ cudaError_t launch_step_staged(const StepArgs<T>& a, cudaStream_t s) {
 template <typename T, int MODE>
 cudaError_t launch_step_tma(const StepArgs<T>& a, cudaStream_t s) {
   const size_t smem = 128 + (size_t)kStStages * st_tile<T>() * sizeof(T);
+  smem_attr(k_step_tma<T, MODE>, smem);
   static int resident = 0;
   if (!resident) {
-    cudaFuncSetAttribute(k_step_tma<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_step_tma<T, MODE>, kBlock, smem);
     if (resident < 1) resident = 1;
   }
@@ -787,12 +802,10 @@ cudaError_t launch_ar_nvls(const ArNvlsArgs<T>& a, uint32_t grid, cudaStream_t s
     const int u = e ? atoi(e) : 4;
     return u >= 8 ? 8 : (u >= 4 ? 4 : 2);
   }();
-  static bool attr = false;
-  if (pad && !attr) {
-    cudaFuncSetAttribute(k_ar_nvls<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad);
-    cudaFuncSetAttribute(k_ar_nvls<T, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad);
-    cudaFuncSetAttribute(k_ar_nvls<T, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad);
-    attr = true;
+  if (pad) {
+    smem_attr(k_ar_nvls<T, 2>, pad);
+    smem_attr(k_ar_nvls<T, 4>, pad);
+    smem_attr(k_ar_nvls<T, 8>, pad);
   }
   // one padded CTA per SM: 1024 threads keep enough switch reductions in flight
   const int threads = pad ? 1024 : kBlock;
@@ -1125,12 +1138,7 @@ cudaError_t launch_os2(const ArOneShotArgs<T>& a, int max_ctas, cudaStream_t s) 
   const int nsl = P + 1 + (a.agg ? 0 : 1) + (a.quad ? 2 : 1) + (a.node.noise ? 1 : 0);
   const size_t smem = 128 + (size_t)S * nsl * os_tile<T>() * sizeof(T);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  static size_t attr = 0;
-  if (attr < smem) {
-    cudaFuncSetAttribute(k_ar_oneshot_tma2<T, P, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    attr = smem;
-  }
+  smem_attr(k_ar_oneshot_tma2<T, P, S>, smem);
   int resident = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_ar_oneshot_tma2<T, P, S>, kBlock, smem);
   if (resident < 1) resident = 1;
@@ -1173,10 +1181,9 @@ cudaError_t launch_ar_oneshot_p(const ArOneShotArgs<T>& a, int vec, uint32_t gri
   }
   if (vec && a.pending && !a.apply_only && a.tma_rank >= 0) {
     const size_t smem = 128 + (size_t)kOsStages * P * os_tile<T>() * sizeof(T);
+    smem_attr(k_ar_oneshot_tma<T, P>, smem);
     static int resident = 0;  // CTAs per SM at this smem size (persistent grid)
     if (!resident) {
-      cudaFuncSetAttribute(k_ar_oneshot_tma<T, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_ar_oneshot_tma<T, P>, kBlock,
                                                     smem);
       if (resident < 1) resident = 1;
@@ -1268,7 +1275,7 @@ __host__ __device__ constexpr uint64_t lt_tile() {
   return (uint64_t)kBlock * Vec<T>::N * 2;
 }
 
-template <typename T>
+template <typename T, bool NORM>
 __global__ void __launch_bounds__(kBlock) k_local_tma(const __grid_constant__ AllreduceArgs<T> a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr uint64_t TILE = lt_tile<T>();
@@ -1290,10 +1297,25 @@ __global__ void __launch_bounds__(kBlock) k_local_tma(const __grid_constant__ Al
   if (n.noise) src[ns++] = n.noise;
   const uint64_t nt = a.d / TILE;
   // programmatic dependent launch: let the next round's grid be scheduled
-  // now, and wait here until the previous round's grid has finished and its
-  // writes are visible (theta / delta are read-after-write across rounds)
+  // now.  Then either wait until the previous round's grid has finished and
+  // its writes are visible (theta / delta are read-after-write across
+  // rounds), or -- chained rounds -- only until the previous round's CTA
+  // with this index, the sole writer of this CTA's tiles (and sole reader of
+  // the snapshot this CTA overwrites), has published them: no grid-wide
+  // drain between rounds.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  __shared__ int chain_ok;
+  if (a.cta_chain) {
+    if (threadIdx.x == 0) {
+      chain_ok = wait_flag_gpu(&a.cta_flags[blockIdx.x], a.cta_seq - 1, a.timeout_ns, a.error);
+      // generic-proxy stores of the previous round -> this round's bulk reads
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    __syncthreads();
+    if (!chain_ok) return;
+  } else {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < kLtStages; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
@@ -1307,7 +1329,7 @@ __global__ void __launch_bounds__(kBlock) k_local_tma(const __grid_constant__ Al
     }
   }
   __syncthreads();
-  const bool norm = n.norm != nullptr;  // grad_norm_out: sum of g^2 (fp64)
+  constexpr bool norm = NORM;  // grad_norm_out: sum of g^2 (fp64)
   double nacc = 0.0;
   for (uint64_t j = 0;; ++j) {
     const uint64_t tile = blockIdx.x + j * gridDim.x;
@@ -1395,16 +1417,21 @@ __global__ void __launch_bounds__(kBlock) k_local_tma(const __grid_constant__ Al
     n.theta_out[k] = radd(x.v[0], avg);
     n.delta[k] = a.per_node ? d0 : avg;
   }
-  block_add_double(nacc, n.norm);
+  if constexpr (NORM) block_add_double(nacc, n.norm);
+  if (a.cta_flags) {
+    __syncthreads();  // every thread's theta / delta stores before the release
+    if (threadIdx.x == 0) st_release_gpu(&a.cta_flags[blockIdx.x], a.cta_seq);
+  }
 }
 
 template <typename T>
 cudaError_t launch_local_tma(const AllreduceArgs<T>& a, cudaStream_t s) {
   const size_t smem = 128 + (size_t)kLtStages * 5 * lt_tile<T>() * sizeof(T);
+  smem_attr(k_local_tma<T, false>, smem);
+  smem_attr(k_local_tma<T, true>, smem);
   static int resident = 0;
   if (!resident) {
-    cudaFuncSetAttribute(k_local_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_local_tma<T>, kBlock, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_local_tma<T, false>, kBlock, smem);
     if (resident < 1) resident = 1;
   }
   int dev = 0, sms = 148;
@@ -1428,7 +1455,8 @@ cudaError_t launch_local_tma(const AllreduceArgs<T>& a, cudaStream_t s) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   ++g_launches;
-  return cudaLaunchKernelEx(&cfg, k_local_tma<T>, a);
+  if (a.node[0].norm) return cudaLaunchKernelEx(&cfg, k_local_tma<T, true>, a);
+  return cudaLaunchKernelEx(&cfg, k_local_tma<T, false>, a);
 }
 
 // Two-shot all-reduce delta kernel (kModeArDelta / kModeApplyDelta) of one
@@ -1552,14 +1580,8 @@ __global__ void __launch_bounds__(kBlock) k_ard_tma(const __grid_constant__ Step
 template <typename T>
 cudaError_t launch_ard_tma(int mode, const StepArgs<T>& a, uint32_t grid, cudaStream_t s) {
   const size_t smem = 128 + (size_t)kLtStages * 6 * lt_tile<T>() * sizeof(T);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_ard_tma<T, kModeArDelta>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    cudaFuncSetAttribute(k_ard_tma<T, kModeApplyDelta>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  smem_attr(k_ard_tma<T, kModeArDelta>, smem);
+  smem_attr(k_ard_tma<T, kModeApplyDelta>, smem);
   const uint64_t tiles = a.d / lt_tile<T>();
   if (tiles < grid) grid = (uint32_t)(tiles ? tiles : 1);
   if (mode == kModeApplyDelta)
@@ -1572,11 +1594,7 @@ cudaError_t launch_ard_tma(int mode, const StepArgs<T>& a, uint32_t grid, cudaSt
 template <typename T>
 cudaError_t launch_allreduce_local(const AllreduceArgs<T>& a, int vec, int norm, uint32_t grid,
                                    cudaStream_t s) {
-  static const bool tma = [] {  // DSGD_LOCAL_TMA=0 selects the LDG kernel
-    const char* e = getenv("DSGD_LOCAL_TMA");
-    return !(e && e[0] == '0');
-  }();
-  if (tma && a.p == 1 && vec) return launch_local_tma<T>(a, s);  // norm fused too
+  if (local_tma_enabled() && a.p == 1 && vec) return launch_local_tma<T>(a, s);  // norm fused too
   // the vector kernel covers d - d % W; a scalar launch finishes the tail
   if (vec) {
     if (norm)
@@ -2110,6 +2128,14 @@ __global__ void __launch_bounds__(kBlock) k_norm_fold(double* acc, uint64_t n, d
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, part[w]);
     *max = fmax(*max, m);
   }
+}
+
+bool local_tma_enabled() {
+  static const bool tma = [] {  // DSGD_LOCAL_TMA=0 selects the LDG kernel
+    const char* e = getenv("DSGD_LOCAL_TMA");
+    return !(e && e[0] == '0');
+  }();
+  return tma;
 }
 
 cudaError_t launch_norm_fold(double* acc, uint64_t n, double* max, cudaStream_t s) {

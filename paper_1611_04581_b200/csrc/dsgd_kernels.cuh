@@ -138,6 +138,15 @@ struct AllreduceArgs {
   int mu_nz, wd_pos, quad;
   int per_node;
   uint32_t p;
+  // k_local_tma round-to-round chaining (dsgd_run_rounds, p = 1): CTA b
+  // publishes cta_flags[b] = cta_seq when its tiles are written; with
+  // cta_chain set, CTA b of the next round waits for exactly that flag
+  // (its tiles are the same) instead of the whole previous grid
+  unsigned long long* cta_flags;
+  unsigned long long cta_seq;
+  int cta_chain;
+  unsigned int* error;
+  unsigned long long timeout_ns;
 };
 
 // Single-context EASGD sweep over p nodes in node order.
@@ -251,6 +260,8 @@ cudaError_t launch_trace(const TraceArgs<T>& a, uint32_t grid, cudaStream_t s);
 template <typename T>
 cudaError_t launch_spatial_mean(const T* const* x, uint32_t p, uint64_t d, T* out, cudaStream_t s);
 // max over `n` per-round sums of g^2 of sqrt(sum) into *max, zeroing the sums
+// true when the p = 1 fused round runs the staged k_local_tma (DSGD_LOCAL_TMA)
+bool local_tma_enabled();
 cudaError_t launch_norm_fold(double* acc, uint64_t n, double* max, cudaStream_t s);
 template <typename T>
 cudaError_t launch_fill_normal(T* out, uint64_t n, double sigma, uint64_t seed, uint64_t offset,

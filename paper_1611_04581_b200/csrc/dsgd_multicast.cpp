@@ -126,6 +126,15 @@ dsgd_status mc_import_fd(McState* s, int pid, int fd, size_t size) {
   return DSGD_OK;
 }
 
+void mc_share(McState* s, McState* owner) {
+  if (!owner->refs) owner->refs = new std::atomic<int>(1);
+  owner->refs->fetch_add(1);
+  s->mc = owner->mc;
+  s->size = owner->size;
+  s->gran = owner->gran;
+  s->refs = owner->refs;
+}
+
 dsgd_status mc_add_device(McState* s, int device) {
   CUdevice d;
   CU_TRY(cuDeviceGet, &d, device);
@@ -164,7 +173,16 @@ void mc_release(McState* s, int device) {
     if (DRV(cuDeviceGet)(&d, device) == CUDA_SUCCESS) DRV(cuMulticastUnbind)(s->mc, d, 0, s->size);
   }
   if (s->phys) DRV(cuMemRelease)(s->phys);
-  if (s->mc && s->owns_mc) DRV(cuMemRelease)(s->mc);
+  if (s->refs) {
+    // shared in-process object: only the last holder releases it (every
+    // other holder has unbound its device by then)
+    if (s->refs->fetch_sub(1) == 1) {
+      if (s->mc) DRV(cuMemRelease)(s->mc);
+      delete s->refs;
+    }
+  } else if (s->mc && s->owns_mc) {
+    DRV(cuMemRelease)(s->mc);
+  }
   if (s->export_fd >= 0) close(s->export_fd);
   *s = McState{};
 }

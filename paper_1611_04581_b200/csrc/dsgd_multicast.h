@@ -10,6 +10,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "dsgd_b200.h"
 
 namespace dsgd {
@@ -22,7 +24,10 @@ struct McState {
   size_t size = 0;
   size_t gran = 0;                        // mapping alignment
   int export_fd = -1;                     // rank 0: the exported POSIX fd (until all imported)
-  bool owns_mc = true;                    // false: another context of this process owns it
+  bool owns_mc = true;                    // releases `mc` (when `refs` is null)
+  // in-process group: the contexts sharing one object count its holders; the
+  // last one to release it (in any order) releases the object
+  std::atomic<int>* refs = nullptr;
   bool added = false, bound = false, mapped_uc = false, mapped_mc = false;
 };
 
@@ -35,6 +40,8 @@ dsgd_status mc_create(McState* s, int device, uint32_t p, size_t need, bool shar
 dsgd_status mc_export_fd(McState* s, int* fd);
 // Imports rank 0's object through pidfd_getfd(pid, fd).
 dsgd_status mc_import_fd(McState* s, int pid, int fd, size_t size);
+// `s` joins `owner`'s object in the same process (shared holder count).
+void mc_share(McState* s, McState* owner);
 dsgd_status mc_add_device(McState* s, int device);
 // Backing on `device`, bound to the object, mapped unicast and multicast.
 // Blocks until every device of the team has been added.

@@ -221,6 +221,12 @@ struct dsgd_ctx {
   double* scratch = nullptr;     // trace metrics (4 doubles)
   unsigned int* arrive = nullptr;
   unsigned int* error = nullptr;
+  // k_local_tma per-CTA round flags: inside dsgd_run_rounds, consecutive
+  // p = 1 rounds chain CTA to CTA instead of draining the whole grid
+  unsigned long long* lt_flags = nullptr;
+  uint64_t lt_seq = 0;           // k_local_tma launches (the flag value of the last one)
+  bool lt_run = false;           // inside dsgd_run_rounds
+  bool lt_prev = false;          // ... and the previous round was a k_local_tma launch
   char* staging = nullptr;       // pinned host staging (d * 8 bytes)
 
   int cur = 0;                   // theta buffer holding the current state
@@ -1112,8 +1118,25 @@ dsgd_status do_allreduce(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& 
     const bool vec = all_aligned(c, gs);
     const uint64_t W = vec ? 16 / sizeof(T) : 1;
     const uint32_t grid = blocks_for(c, c->d / W, 1);
+    static const bool chain_on = [] {  // DSGD_LT_CHAIN=0: grid-wide waits only
+      const char* e = getenv("DSGD_LT_CHAIN");
+      return !(e && e[0] == '0');
+    }();
+    const bool lt = chain_on && c->lt_run && dsgd::local_tma_enabled() && c->n_local == 1 && vec;
+    if (lt) {
+      // inside dsgd_run_rounds: publish per-CTA flags, and chain behind this
+      // run's own previous k_local_tma (every op in between is stream-ordered:
+      // host-noise copies, norm folds); the logistic producer kernels write
+      // the gradient, so they keep the grid-wide wait
+      a.cta_flags = c->lt_flags;
+      a.cta_seq = ++c->lt_seq;
+      a.cta_chain = c->lt_prev && !gs.logistic ? 1 : 0;
+      a.error = c->error;
+      a.timeout_ns = c->timeout_ns;
+    }
     LaunchScope ls(c, DSGD_K_ALLREDUCE);
     DSGD_CUDA(dsgd::launch_allreduce_local<T>(a, vec, gs.norm, grid, c->stream));
+    c->lt_prev = lt;
     c->prev_readers.clear();
     return DSGD_OK;
   }
@@ -1461,11 +1484,7 @@ dsgd_status inproc_nvls(InprocGroup* g) {
   }
   for (dsgd_ctx* c : g->ctx) {
     if (st != DSGD_OK) break;
-    if (c != c0) {
-      c->mc.mc = c0->mc.mc;
-      c->mc.size = c0->mc.size;
-      c->mc.owns_mc = false;
-    }
+    if (c != c0) dsgd::mc_share(&c->mc, &c0->mc);
     DeviceGuard dg(c->device);
     st = dsgd::mc_add_device(&c->mc, c->device);
   }
@@ -1607,6 +1626,8 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
   DSGD_CUDA(cudaMallocHost(&c->norm_host, sizeof(double) * kMaxLocal));
   DSGD_CUDA(cudaMalloc(&c->arrive, 256));
   DSGD_CUDA(cudaMemset(c->arrive, 0, 256));
+  DSGD_CUDA(cudaMalloc(&c->lt_flags, sizeof(unsigned long long) * 4096));
+  DSGD_CUDA(cudaMemset(c->lt_flags, 0, sizeof(unsigned long long) * 4096));
   if (c->trace_cap) {
     DSGD_CUDA(cudaMalloc(&c->trace_dev, sizeof(unsigned long long) * 3 * c->trace_cap));
     DSGD_CUDA(cudaMemset(c->trace_dev, 0, sizeof(unsigned long long) * 3 * c->trace_cap));
@@ -1661,6 +1682,7 @@ void dsgd_ctx_destroy(dsgd_ctx* c) {
   cudaFree(c->norm_max);
   cudaFreeHost(c->norm_host);
   cudaFree(c->arrive);
+  cudaFree(c->lt_flags);
   cudaFree(c->trace_dev);
   cudaFreeHost(c->staging);
   cudaFree(c->arena);
@@ -2512,7 +2534,12 @@ dsgd_status dsgd_run_rounds(dsgd_ctx* c, const dsgd_run_desc* run) {
   DSGD_TRY(run_check(c, run));
   if (c->grp && c->p > 1)
     return set_error(DSGD_EINVAL, "in-process group: use dsgd_group_run_rounds");
-  for (uint64_t r = 0; r < run->rounds; ++r) DSGD_TRY(run_one_round(c, run));
+  c->lt_run = true;
+  c->lt_prev = false;
+  dsgd_status st = DSGD_OK;
+  for (uint64_t r = 0; r < run->rounds && st == DSGD_OK; ++r) st = run_one_round(c, run);
+  c->lt_run = c->lt_prev = false;
+  DSGD_TRY(st);
   return run_finish(c);
 }
 

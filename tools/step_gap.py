@@ -33,6 +33,16 @@ def main():
             extra = f" kernel {kms / kn * 1e3:.1f} us"
         print(f"profile={prof}: {ms * 1e3:.1f} us/step{extra}", flush=True)
         g.profile(False)
+    # the per-call API path (one dsgd_allreduce_round per step, no run loop)
+    for _ in range(2):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for i in range(200):
+            g.allreduce_round(h, grad=[ptrs[i % 4]])
+        e1.record(s)
+        g.sync()
+        torch.cuda.synchronize()
+        print(f"per-call: {e0.elapsed_time(e1) / 200 * 1e3:.1f} us/step", flush=True)
 
 
 if __name__ == "__main__":
