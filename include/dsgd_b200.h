@@ -174,6 +174,9 @@ dsgd_status dsgd_get_state(dsgd_ctx* ctx, uint32_t local, double* theta, double*
                            uint64_t* t);
 dsgd_status dsgd_set_vector(dsgd_ctx* ctx, uint32_t local, dsgd_buffer which,
                             const double* host);
+/* DSGD_BUF_CENTER on rank 0 of a multi-GPU EASGD chain: waits (bounded by
+ * the context timeout -> DSGD_ETIMEOUT) until the last gated round's center
+ * has fully arrived from rank p-1, so no host barrier is needed first. */
 dsgd_status dsgd_get_vector(dsgd_ctx* ctx, uint32_t local, dsgd_buffer which, double* host);
 /* Raw asynchronous copies in the context dtype on the context stream (host
  * memory should be pinned); used by the end-to-end path. */

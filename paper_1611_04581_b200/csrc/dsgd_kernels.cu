@@ -1893,6 +1893,238 @@ __global__ void __launch_bounds__(kBlock) k_ea_chain(const __grid_constant__ EaC
   block_signal(a.signal);
 }
 
+// Staged chain (the B200 path, chunk = one st_tile): a persistent grid, CTA
+// b owning chunks b, b + G, ...  Warp 8 (producer) bulk-copies each chunk's
+// theta / delta / gradient (or s, opt) / host-noise tiles into a 4-stage
+// shared-memory ring as soon as a stage frees -- they do not depend on the
+// chain -- and the center tile once the previous rank has published it
+// (flag acquire, then proxy fence).  Warps 0-7 run the client update + SGD
+// step out of shared memory and write theta', delta' and the new center
+// back into the stage in place.  Warp 9 (signal) bulk-stores the three
+// tiles -- the center straight into the next rank's c_in over NVLink -- and,
+// once a chunk's bulk group has completed, publishes its flag with a
+// system-scope release; it runs one chunk behind, so neither the NVLink
+// write acknowledgement nor the flag wait ever stalls the arithmetic warps.
+// Per-coordinate operation order is k_ea_chain's (the single-context
+// sweep's) exactly.
+constexpr int kEcStages = 4;
+constexpr int kEcThreads = kBlock + 96;  // + producer, signal, publisher warps
+
+template <typename T>
+__device__ __forceinline__ void ec_slot_rd(const T* p, T (&v)[Vec<T>::N]) {
+  Vec<T> t;
+  t.u = *reinterpret_cast<const uint4*>(p);
+#pragma unroll
+  for (int l = 0; l < Vec<T>::N; ++l) v[l] = t.t[l];
+}
+template <typename T>
+__device__ __forceinline__ void ec_slot_wr(T* p, const T (&v)[Vec<T>::N]) {
+  Vec<T> t;
+#pragma unroll
+  for (int l = 0; l < Vec<T>::N; ++l) t.t[l] = v[l];
+  *reinterpret_cast<uint4*>(p) = t.u;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kEcThreads, 1)
+    k_ea_chain_tma(const __grid_constant__ EaChainArgs<T> a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr uint64_t TILE = st_tile<T>();
+  constexpr uint32_t TB = (uint32_t)(TILE * sizeof(T));
+  constexpr int W = Vec<T>::N;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* empty = full + kEcStages;
+  uint64_t* ready = empty + kEcStages;  // chunks handed to the publisher warp
+  T* stage = reinterpret_cast<T*>(smem_raw + 128);
+  const NodeIO<T>& n = a.node;
+  const bool hnoise = n.noise != nullptr;
+  constexpr int s_c = 0, s_x = 1, s_dp = 2, s_g = 3;  // center, theta, delta, g | s, opt
+  const int s_nz = a.quad ? 5 : 4;                      // host noise
+  const int nsl = s_nz + (hnoise ? 1 : 0);
+  const uint64_t nfull = a.d / TILE;
+  const uint64_t G = gridDim.x;
+  const uint64_t mine = nfull > blockIdx.x ? (nfull - 1 - blockIdx.x) / G + 1 : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int sg = 0; sg < kEcStages; ++sg) {
+      mbar_init(&full[sg], 1);
+      mbar_init(&empty[sg], 1);
+    }
+    *ready = 0;
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == kBlock / 32) {
+    if (lane == 0) {  // producer
+      auto issue_local = [&](uint64_t j, int sg) {
+        const uint64_t off = (blockIdx.x + j * G) * TILE;
+        T* dst = stage + (uint64_t)sg * nsl * TILE;
+        mbar_expect_tx(&full[sg], TB * (uint32_t)nsl);  // + the center tile, issued later
+        bulk_g2s(dst + s_x * TILE, n.theta_in + off, TB, &full[sg]);
+        bulk_g2s(dst + s_dp * TILE, n.delta + off, TB, &full[sg]);
+        if (a.quad) {
+          bulk_g2s(dst + s_g * TILE, a.spec + off, TB, &full[sg]);
+          bulk_g2s(dst + (s_g + 1) * TILE, a.opt + off, TB, &full[sg]);
+        } else {
+          bulk_g2s(dst + s_g * TILE, n.grad + off, TB, &full[sg]);
+        }
+        if (hnoise) bulk_g2s(dst + (uint64_t)s_nz * TILE, n.noise + off, TB, &full[sg]);
+      };
+      for (uint64_t j = 0; j < mine && j < (uint64_t)kEcStages; ++j) issue_local(j, (int)j);
+      bool live = true;
+      for (uint64_t j = 0; j < mine; ++j) {
+        const int sg = (int)(j % kEcStages);
+        if (j >= (uint64_t)kEcStages) {
+          mbar_wait(&empty[sg], (uint32_t)((j / kEcStages - 1) & 1));
+          issue_local(j, sg);
+        }
+        const uint64_t c = blockIdx.x + j * G;
+        // after a timeout (error raised) the remaining chunks run on stale
+        // centers so that every role still terminates
+        if (live) live = wait_flag(&a.flag_in[c], a.need, a.timeout_ns, a.error);
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // peer wrote c_in
+        bulk_g2s(stage + (uint64_t)sg * nsl * TILE + s_c * TILE, a.c_in + c * TILE, TB, &full[sg]);
+      }
+    }
+  } else if (warp == kBlock / 32 + 1) {  // signal warp
+    for (uint64_t j = 0; j < mine; ++j) {
+      const int sg = (int)(j % kEcStages);
+      // the update warps' center stores (NVLink) and shared-memory results
+      // of chunk j are performed relative to this warp past the barrier
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + sg), "r"(kBlock + 32) : "memory");
+      if (lane == 0) {
+        const uint64_t off = (blockIdx.x + j * G) * TILE;
+        T* src = stage + (uint64_t)sg * nsl * TILE;
+        bulk_s2g(n.theta_out + off, src + s_x * TILE, TB);
+        bulk_s2g(n.delta + off, src + s_dp * TILE, TB);
+        bulk_commit();
+        // chunk j's center is out: hand it to the publisher warp
+        asm volatile("st.release.cta.shared::cta.u64 [%0], %1;" ::"r"(smem_u32(ready)),
+                     "l"((unsigned long long)(j + 1))
+                     : "memory");
+        bulk_wait_read<0>();
+        mbar_arrive(&empty[sg]);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) bulk_wait<0>();  // theta' / delta' landed before the round counter
+  } else if (warp == kBlock / 32 + 2) {  // publisher warp
+    if (lane == 0) {
+      // one system fence publishes every chunk handed over before it: the
+      // fence waits for the SM's outstanding NVLink writes, so it must not
+      // sit on the stage-recycling path (that is the signal warp's)
+      uint64_t pub = 0;
+      while (pub < mine) {
+        unsigned long long got;
+        asm volatile("ld.acquire.cta.shared::cta.u64 %0, [%1];" : "=l"(got) : "r"(smem_u32(ready))
+                     : "memory");
+        if (got == pub) {
+          __nanosleep(32);
+          continue;
+        }
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+        for (; pub < got; ++pub) st_relaxed_sys(&a.flag_out[blockIdx.x + pub * G], a.seq);
+      }
+    }
+  } else {  // warps 0-7: the update
+    const bool norm = n.norm != nullptr;
+    double nacc = 0.0;
+    for (uint64_t j = 0; j < mine; ++j) {
+      const int sg = (int)(j % kEcStages);
+      const uint64_t c = blockIdx.x + j * G;
+      mbar_wait(&full[sg], (uint32_t)((j / kEcStages) & 1));
+      T* base = stage + (uint64_t)sg * nsl * TILE + (uint64_t)threadIdx.x * W;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const uint64_t o = (uint64_t)u * kBlock * W;
+        T cv[W], x[W], dp[W], gb[W], sv[W], ov[W], xi[W];
+        ec_slot_rd(base + s_c * TILE + o, cv);
+        ec_slot_rd(base + s_x * TILE + o, x);
+        ec_slot_rd(base + s_dp * TILE + o, dp);
+        if (a.quad) {
+          ec_slot_rd(base + s_g * TILE + o, sv);
+          ec_slot_rd(base + (s_g + 1) * TILE + o, ov);
+#pragma unroll
+          for (int l = 0; l < W; ++l) gb[l] = T(0);
+        } else {
+          ec_slot_rd(base + s_g * TILE + o, gb);
+#pragma unroll
+          for (int l = 0; l < W; ++l) sv[l] = ov[l] = T(0);
+        }
+        if (hnoise) {
+          ec_slot_rd(base + (uint64_t)s_nz * TILE + o, xi);
+        } else if (n.nsigma != T(0)) {
+          float z[W];
+          dev_normals<W>(n.nkey, n.nctr, n.nbase + c * TILE + (uint64_t)threadIdx.x * W + o, z);
+#pragma unroll
+          for (int l = 0; l < W; ++l) xi[l] = rmul(n.nsigma, (T)z[l]);
+        } else {
+#pragma unroll
+          for (int l = 0; l < W; ++l) xi[l] = T(0);
+        }
+#pragma unroll
+        for (int l = 0; l < W; ++l) {
+          const T uu = rmul(a.beta, rsub(x[l], cv[l]));
+          const T xv = rsub(x[l], uu);
+          const T dl = sgd_delta(xv, dp[l], gb[l], sv[l], ov[l], xi[l], n.alpha, a.mu, a.wd,
+                                 a.mu_nz, a.wd_pos, a.quad, norm, nacc);
+          dp[l] = dl;
+          x[l] = radd(xv, dl);
+          cv[l] = radd(cv[l], uu);
+        }
+        // the running center straight into the next rank's c_in (NVLink
+        // stores from the SM: the TMA engine stays free for the HBM stages)
+        ec_slot_wr(a.c_out + c * TILE + (uint64_t)threadIdx.x * W + o, cv);
+        ec_slot_wr(base + s_x * TILE + o, x);
+        ec_slot_wr(base + s_dp * TILE + o, dp);
+      }
+      fence_async_smem();  // theta' / delta' are read next by the signal warp's bulk stores
+      asm volatile("bar.arrive %0, %1;" ::"r"(1 + sg), "r"(kBlock + 32) : "memory");
+    }
+    if (norm) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nacc += __shfl_xor_sync(0xffffffffu, nacc, o);
+      if (lane == 0) atomicAdd(n.norm, nacc);
+    }
+  }
+  __syncthreads();
+  // the ragged last chunk [nfull * TILE, d): its owner, with plain loads
+  if (nfull * TILE < a.d && blockIdx.x == nfull % G) {
+    __shared__ int ok;
+    if (threadIdx.x == 0) ok = wait_flag(&a.flag_in[nfull], a.need, a.timeout_ns, a.error) ? 1 : 0;
+    __syncthreads();
+    if (!ok) return;
+    const bool norm = n.norm != nullptr;
+    double nacc = 0.0;
+    for (uint64_t kk = nfull * TILE + threadIdx.x; kk < a.d; kk += blockDim.x) {
+      const T cv0 = a.c_in[kk];
+      T xv = n.theta_in[kk];
+      const T u = rmul(a.beta, rsub(xv, cv0));
+      xv = rsub(xv, u);
+      const T gb = a.quad ? T(0) : n.grad[kk];
+      const T sv = a.quad ? a.spec[kk] : T(0), ov = a.quad ? a.opt[kk] : T(0);
+      const T dl = sgd_delta(xv, n.delta[kk], gb, sv, ov, noise_at(n, kk), n.alpha, a.mu, a.wd,
+                             a.mu_nz, a.wd_pos, a.quad, norm, nacc);
+      n.delta[kk] = dl;
+      n.theta_out[kk] = radd(xv, dl);
+      a.c_out[kk] = radd(cv0, u);
+    }
+    if (norm) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nacc += __shfl_xor_sync(0xffffffffu, nacc, o);
+      if (lane == 0) atomicAdd(n.norm, nacc);
+    }
+    __syncthreads();  // every thread's center stores before the (cumulative) release
+    if (threadIdx.x == 0) st_release_sys(&a.flag_out[nfull], a.seq);
+  }
+  block_signal(a.signal);
+}
+
+template <typename T>
+uint64_t ea_chain_tile() {
+  return st_tile<T>();
+}
+
 template <typename T>
 cudaError_t launch_ea_chain(const EaChainArgs<T>& a, int vec, uint32_t grid, cudaStream_t s,
                             bool mix_only) {
@@ -1901,6 +2133,19 @@ cudaError_t launch_ea_chain(const EaChainArgs<T>& a, int vec, uint32_t grid, cud
       DSGD_COUNTED(k_ea_chain<T, true, true><<<grid, kBlock, 0, s>>>(a));
     else
       DSGD_COUNTED(k_ea_chain<T, false, true><<<grid, kBlock, 0, s>>>(a));
+    return cudaGetLastError();
+  }
+  if (vec && a.chunk == st_tile<T>() && a.d >= st_tile<T>() && ea_chain_staged()) {
+    const bool hnoise = a.node.noise != nullptr;
+    const int nsl = (a.quad ? 5 : 4) + (hnoise ? 1 : 0);
+    const size_t smem = 128 + (size_t)kEcStages * nsl * st_tile<T>() * sizeof(T);
+    smem_attr(k_ea_chain_tma<T>, smem);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t nfull = a.d / st_tile<T>();
+    const uint32_t g = (uint32_t)std::min<uint64_t>(nfull, (uint64_t)sms);
+    DSGD_COUNTED(k_ea_chain_tma<T><<<g, kEcThreads, smem, s>>>(a));
     return cudaGetLastError();
   }
   if (vec)
@@ -2130,6 +2375,27 @@ __global__ void __launch_bounds__(kBlock) k_norm_fold(double* acc, uint64_t n, d
   }
 }
 
+__global__ void k_wait_chunks(const unsigned long long* flags, uint64_t n, unsigned long long need,
+                              unsigned long long timeout_ns, unsigned int* error) {
+  for (uint64_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x)
+    if (!wait_flag(&flags[c], need, timeout_ns, error)) return;
+}
+
+cudaError_t launch_wait_chunks(const unsigned long long* flags, uint64_t n, unsigned long long need,
+                               unsigned long long timeout_ns, unsigned int* error, cudaStream_t s) {
+  const uint32_t g = (uint32_t)std::min<uint64_t>((n + kBlock - 1) / kBlock, 1024);
+  DSGD_COUNTED(k_wait_chunks<<<g ? g : 1, kBlock, 0, s>>>(flags, n, need, timeout_ns, error));
+  return cudaGetLastError();
+}
+
+bool ea_chain_staged() {
+  static const bool on = [] {  // DSGD_EA_STAGED=0: the one-CTA-per-chunk LDG chain
+    const char* e = getenv("DSGD_EA_STAGED");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool local_tma_enabled() {
   static const bool tma = [] {  // DSGD_LOCAL_TMA=0 selects the LDG kernel
     const char* e = getenv("DSGD_LOCAL_TMA");
@@ -2152,6 +2418,7 @@ cudaError_t launch_norm_fold(double* acc, uint64_t n, double* max, cudaStream_t 
                                           bool);                                                   \
   template cudaError_t launch_logistic<T>(const LogisticArgs<T>&, uint32_t, cudaStream_t);         \
   template cudaError_t launch_push<T>(const PushArgs<T>&, int, uint32_t, cudaStream_t);            \
+  template uint64_t ea_chain_tile<T>();                                                           \
   template cudaError_t launch_ea_chain<T>(const EaChainArgs<T>&, int, uint32_t, cudaStream_t,      \
                                           bool);                                                   \
   template cudaError_t launch_ar_reduce<T>(const ArReduceArgs<T>&, uint32_t, cudaStream_t);        \

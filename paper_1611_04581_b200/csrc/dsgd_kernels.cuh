@@ -262,6 +262,14 @@ cudaError_t launch_spatial_mean(const T* const* x, uint32_t p, uint64_t d, T* ou
 // max over `n` per-round sums of g^2 of sqrt(sum) into *max, zeroing the sums
 // true when the p = 1 fused round runs the staged k_local_tma (DSGD_LOCAL_TMA)
 bool local_tma_enabled();
+// true unless DSGD_EA_STAGED=0: the multi-GPU EASGD chain runs k_ea_chain_tma
+// with one flag per ea_chain_tile<T>() elements (every rank the same)
+bool ea_chain_staged();
+// waits (bounded; error flag on timeout) until flags[0..n) >= need
+cudaError_t launch_wait_chunks(const unsigned long long* flags, uint64_t n, unsigned long long need,
+                               unsigned long long timeout_ns, unsigned int* error, cudaStream_t s);
+template <typename T>
+uint64_t ea_chain_tile();
 cudaError_t launch_norm_fold(double* acc, uint64_t n, double* max, cudaStream_t s);
 template <typename T>
 cudaError_t launch_fill_normal(T* out, uint64_t n, double sigma, uint64_t seed, uint64_t offset,

@@ -234,6 +234,7 @@ struct dsgd_ctx {
   uint64_t rounds_done = 0;      // rounds this context has run (lock-step)
   uint64_t seq = 0;              // round counters published so far (multi-GPU)
   uint64_t ea_seq = 0;           // gated EASGD rounds run (multi-GPU chain)
+  uint64_t ea_chunk_used = 1024; // elements per chain flag of the last chain round
   void* ea_update_out[kMaxLocal] = {};   // optional ea_client_step update outputs
   std::vector<uint32_t> prev_readers;  // nodes that read this context's snapshot last round
   bool ar_pending = false;             // multi-GPU all-reduce: theta += avg not yet applied
@@ -1219,8 +1220,10 @@ dsgd_status do_ea(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& gs, int
   a.need = r == 0 ? c->ea_seq - 1 : c->ea_seq;
   a.seq = c->ea_seq;
   a.d = c->d;
-  a.chunk = c->ea_chunk;
+  // staged chain: one flag per staged tile (the same on every rank)
+  a.chunk = dsgd::ea_chain_staged() ? dsgd::ea_chain_tile<T>() : c->ea_chunk;
   a.n_chunks = (c->d + a.chunk - 1) / a.chunk;
+  c->ea_chunk_used = a.chunk;
   a.mu = (T)h->mu;
   a.wd = (T)h->weight_decay;
   a.beta = (T)h->beta_ea;
@@ -1842,6 +1845,21 @@ dsgd_status dsgd_logistic_set_sample_range(dsgd_ctx* c, uint32_t local, uint64_t
   return DSGD_OK;
 }
 
+// Rank 0 of a multi-GPU EASGD chain holds the center in its c_in, written
+// chunk by chunk by rank p-1's last gated round: wait (on the device,
+// bounded) until every chunk of that round has arrived.
+dsgd_status center_arrived(dsgd_ctx* c) {
+  if (!c->distributed() || c->first != 0 || c->ea_seq == 0 || !c->connected) return DSGD_OK;
+  const uint64_t n = (c->d + c->ea_chunk_used - 1) / c->ea_chunk_used;
+  DSGD_CUDA(dsgd::launch_wait_chunks(reinterpret_cast<const unsigned long long*>(c->arena + c->off_flags),
+                                     n, c->ea_seq, c->timeout_ns, c->error, c->stream));
+  DSGD_CUDA(cudaStreamSynchronize(c->stream));
+  unsigned int err = 0;
+  DSGD_CUDA(cudaMemcpy(&err, c->error, sizeof(err), cudaMemcpyDeviceToHost));
+  if (err) return set_error(DSGD_ETIMEOUT, "the EASGD center never arrived from the last rank");
+  return DSGD_OK;
+}
+
 dsgd_status dsgd_get_vector(dsgd_ctx* c, uint32_t local, dsgd_buffer which, double* host) {
   DSGD_TRY(check_ctx(c));
   if (which == DSGD_BUF_THETA || which == DSGD_BUF_DELTA) DSGD_TRY(flush_pending(c));
@@ -1849,6 +1867,7 @@ dsgd_status dsgd_get_vector(dsgd_ctx* c, uint32_t local, dsgd_buffer which, doub
   char* p = buffer_of(c, local, which);
   if (!p) return set_error(DSGD_ESTATE, "buffer not allocated for this context");
   DeviceGuard g(c->device);
+  if (which == DSGD_BUF_CENTER) DSGD_TRY(center_arrived(c));
   return download_vec(c, p, host);
 }
 

@@ -36,7 +36,8 @@ def main():
         timeout_case(rank, world, local, dtype, dist)
         return
     for proto, oid in names.items():
-        d = 1031
+        # EASGD: a staged chain with several chunks per CTA and a ragged tail
+        d = 1031 if proto != "elastic-avg" else 148 * 5 * 2048 + 1031
         hk = dict(alpha0=0.05, anneal_at=(20,), mu=0.9, weight_decay=1e-4, beta_gossip=0.4,
                   beta_ea=0.15, tau=1)
         ar = proto.startswith("all-reduce")

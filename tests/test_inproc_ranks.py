@@ -152,3 +152,13 @@ def test_inproc_p8_staged_sizes(proto, dtype, monkeypatch):
     (k_step_tma2) and a multi-chunk EASGD chain (7 hops + ring closure)."""
     res = run_group(proto, 8, dtype, 5 * 4096 + 7, 8, monkeypatch)
     check(res, proto)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_inproc_ea_chain_staged_ring_wraps(dtype, monkeypatch):
+    """The staged EASGD chain (k_ea_chain_tma) with every CTA cycling its
+    4-stage shared-memory ring several times (> 4 chunks per CTA on a
+    148-SM grid) and a ragged last chunk: 3 ranks (2 hops + ring closure),
+    4 rounds, bit-exact with the oracle."""
+    res = run_group("elastic-avg", 3, dtype, 148 * 6 * 2048 + 13, 4, monkeypatch)
+    check(res, "elastic-avg")
