@@ -238,6 +238,10 @@ def _configure_ref(_ref):
     _ref.ref_time_rounds.restype = C.c_double
     _ref.ref_time_rounds.argtypes = [C.c_int, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int,
                                      C.POINTER(Hyper), C.c_int]
+    if hasattr(_ref, "ref_time_rounds_sharded"):
+        _ref.ref_time_rounds_sharded.restype = C.c_double
+        _ref.ref_time_rounds_sharded.argtypes = [C.c_int, C.c_uint32, C.c_uint64, C.c_uint64,
+                                                 C.c_int, C.POINTER(Hyper), C.c_int, C.c_uint32]
     return _ref
 
 
@@ -638,14 +642,20 @@ def ref_stream(seed: int, kind: int, count: int, n: int = 0):
 
 
 def ref_time_rounds(protocol: int, p: int, d: int, rounds: int, threaded: bool,
-                    h: HyperParams, grad: str = "quadratic") -> float:
+                    h: HyperParams, grad: str = "quadratic", shards: int = 1) -> float:
     """Seconds for `rounds` rounds of the compiled reference (simulator
     rules on 1 thread, or run_transport's threads); grad: 'quadratic'
     (QuadraticObjective(1, 0)) or 'pool' (4 synthetic N(0,1) gradient
-    vectors through the Objective plugin slot, served in turn)."""
+    vectors through the Objective plugin slot, served in turn).  shards > 1:
+    d split into coordinate ranges, one independent reference run per shard
+    on its own thread(s), all concurrently (ref_time_rounds_sharded)."""
     hc = h.to_c()
-    sec = ref().ref_time_rounds(protocol, p, d, rounds, int(threaded), C.byref(hc),
-                                {"quadratic": 0, "pool": 1}[grad])
+    gk = {"quadratic": 0, "pool": 1}[grad]
+    if shards > 1:
+        sec = ref().ref_time_rounds_sharded(protocol, p, d, rounds, int(threaded), C.byref(hc),
+                                            gk, shards)
+    else:
+        sec = ref().ref_time_rounds(protocol, p, d, rounds, int(threaded), C.byref(hc), gk)
     if sec < 0:
         raise RuntimeError(ref().ref_last_error().decode())
     return sec

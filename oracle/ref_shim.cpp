@@ -8,7 +8,9 @@
 // bench.py.  Nothing here is product code; nothing is copied from the
 // reference -- this file only calls its public API (protocols.hpp,
 // simulator.hpp, transport.hpp).
+#include <algorithm>
 #include <atomic>
+#include <barrier>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -520,8 +522,15 @@ int ref_ring_allreduce(std::uint32_t p, std::uint64_t d, const double* in, doubl
 // with the seeded partner streams / EA sweep, gated every round after 0);
 // mode 1: the threaded transport backend run_transport (p worker threads,
 // +1 EA server thread).  Returns seconds for all rounds, or -1.
-double ref_time_rounds(int protocol, std::uint32_t p, std::uint64_t d, std::uint64_t rounds,
-                       int mode, const dsgdo_hyper* hp, int grad_kind) {
+}  // extern "C"
+
+namespace {
+// Rounds of the compiled reference, timed.  `sync` (sharded runs): every
+// shard's thread arrives there right before its first timed round and right
+// after its last, so the clock covers the rounds of all shards together.
+double time_rounds_impl(int protocol, std::uint32_t p, std::uint64_t d, std::uint64_t rounds,
+                        int mode, const dsgdo_hyper* hp, int grad_kind,
+                        std::barrier<>* sync) {
   try {
     dsgdo_sim c{};
     c.protocol = protocol;
@@ -546,6 +555,12 @@ double ref_time_rounds(int protocol, std::uint32_t p, std::uint64_t d, std::uint
     const Objective& obj = grad_kind == 1 ? static_cast<const Objective&>(*pool)
                                           : static_cast<const Objective&>(quad);
     using clk = std::chrono::steady_clock;
+    if (mode == 2) {  // one run_transport of `rounds` rounds, wall time (sharded runs)
+      cfg.rounds = rounds;
+      const auto t0 = clk::now();
+      (void)run_transport(cfg, obj);
+      return std::chrono::duration<double>(clk::now() - t0).count();
+    }
     if (mode == 1) {
       // run_transport also builds the initial nodes and trace records; time
       // `rounds + 1` and 1 round and keep the difference (per-round cost).
@@ -570,6 +585,7 @@ double ref_time_rounds(int protocol, std::uint32_t p, std::uint64_t d, std::uint
     }
     const Hyperparams& h = cfg.hyper;
     std::vector<std::uint32_t> partners(p);
+    if (sync) sync->arrive_and_wait();
     const auto t0 = clk::now();
     for (std::uint64_t r = 1; r <= rounds; ++r) {  // r > 0: every round gated (tau = 1)
       switch (protocol) {
@@ -592,11 +608,69 @@ double ref_time_rounds(int protocol, std::uint32_t p, std::uint64_t d, std::uint
           for (NodeState& n : nodes) n = local_sgd_step(std::move(n), obj, cfg.noise, h);
       }
     }
+    if (sync) sync->arrive_and_wait();
     return std::chrono::duration<double>(clk::now() - t0).count();
   } catch (const std::exception& e) {
     g_err = e.what();
+    if (sync) sync->arrive_and_drop();
     return -1.0;
   }
+}
+}  // namespace
+
+extern "C" {
+
+double ref_time_rounds(int protocol, std::uint32_t p, std::uint64_t d, std::uint64_t rounds,
+                       int mode, const dsgdo_hyper* hp, int grad_kind) {
+  return time_rounds_impl(protocol, p, d, rounds, mode, hp, grad_kind, nullptr);
+}
+
+// The same rounds on every host thread: d split into `shards` coordinate
+// ranges (every rule of this path is coordinate-separable), each shard an
+// independent reference run on its own thread -- the reference's own code
+// using all the cores a host gives it.  Simulator rules (mode 0): the clock
+// spans the rounds of all shards (start / end barriers).  Threaded
+// transport (mode 1): `shards` concurrent run_transport calls of p threads
+// each, (rounds + 1) minus 1 round of wall time, as in ref_time_rounds.
+double ref_time_rounds_sharded(int protocol, std::uint32_t p, std::uint64_t d,
+                               std::uint64_t rounds, int mode, const dsgdo_hyper* hp,
+                               int grad_kind, std::uint32_t shards) {
+  if (shards <= 1 || d < shards) return ref_time_rounds(protocol, p, d, rounds, mode, hp, grad_kind);
+  using clk = std::chrono::steady_clock;
+  auto size_of = [&](std::uint32_t i) { return d / shards + (i + 1 == shards ? d % shards : 0); };
+  std::vector<double> secs(shards, 0.0);
+  if (mode == 0) {
+    std::barrier<> sync((std::ptrdiff_t)shards);
+    std::vector<std::thread> th;
+    for (std::uint32_t i = 0; i < shards; ++i)
+      th.emplace_back([&, i] {
+        secs[i] = time_rounds_impl(protocol, p, size_of(i), rounds, 0, hp, grad_kind, &sync);
+      });
+    for (auto& t : th) t.join();
+    double m = 0.0;
+    for (double v : secs) {
+      if (v < 0) return -1.0;
+      m = std::max(m, v);
+    }
+    return m;
+  }
+  auto wall = [&](std::uint64_t r) {
+    const auto t0 = clk::now();
+    std::vector<std::thread> th;
+    for (std::uint32_t i = 0; i < shards; ++i)
+      th.emplace_back([&, i] {
+        secs[i] = time_rounds_impl(protocol, p, size_of(i), r, 2, hp, grad_kind, nullptr);
+      });
+    for (auto& t : th) t.join();
+    for (double v : secs)
+      if (v < 0) return -1.0;
+    return std::chrono::duration<double>(clk::now() - t0).count();
+  };
+  // concurrent wall of rounds + 1 rounds minus that of 1 round: the node
+  // construction inside run_transport stays out of the per-round figure
+  const double a = wall(rounds + 1), b = wall(1);
+  if (a < 0 || b < 0) return -1.0;
+  return std::max(0.0, a - b);
 }
 
 }  // extern "C"
