@@ -33,6 +33,33 @@ void smem_attr(K* kernel, size_t smem) {
   }
 }
 
+// Programmatic dependent launch (DSGD_PDL, default on): the kernel may be
+// scheduled while the previous kernel of the stream drains; the kernel
+// itself executes griddepcontrol.wait before touching global memory.
+static bool pdl_enabled() {
+  static const bool pdl = [] {  // DSGD_PDL=0: plain stream-ordered launches
+    const char* e = getenv("DSGD_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return pdl;
+}
+
+template <typename K, typename A>
+cudaError_t launch_pdl(K* kernel, uint32_t grid, uint32_t block, size_t smem, cudaStream_t s,
+                       const A& args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args);
+}
+
 // Kernels issued by this thread (tail launches included): dsgd_launch_count.
 // (the file is compiled once per dtype, DSGD_KERNEL_DTYPE = 32 / 64, in
 // parallel; the counter lives in the fp32 object)
@@ -457,6 +484,10 @@ __global__ void __launch_bounds__(kBlock) k_step_tma2(const __grid_constant__ St
   constexpr int kStages = 3;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
   T* stage = reinterpret_cast<T*>(smem_raw + 128);
+  // programmatic dependent launch: the next launch may be scheduled now;
+  // this one touches no global memory before the previous grid is done
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (!block_wait(a.wait)) return;
   const bool noise = a.node[0].noise != nullptr;  // the same for every node of a launch
   // slot layout (identical for every node)
@@ -588,8 +619,8 @@ cudaError_t launch_step_staged(const StepArgs<T>& a, cudaStream_t s) {
   const uint64_t work = a.d / st_tile<T>() * a.n_local;
   uint32_t g = (uint32_t)sms * (uint32_t)resident;
   if (work < g) g = (uint32_t)(work ? work : 1);
-  DSGD_COUNTED(k_step_tma2<T, MODE><<<g, kBlock, smem, s>>>(a));
-  return cudaGetLastError();
+  ++g_launches;
+  return launch_pdl(k_step_tma2<T, MODE>, g, kBlock, smem, s, a);
 }
 
 // Partner-only staging (DSGD_GOSSIP_STAGE_ALL=0), one node per GPU.
@@ -1440,23 +1471,9 @@ cudaError_t launch_local_tma(const AllreduceArgs<T>& a, cudaStream_t s) {
   const uint64_t tiles = a.d / lt_tile<T>();
   uint32_t g = (uint32_t)sms * (uint32_t)resident;
   if (tiles < g) g = (uint32_t)(tiles ? tiles : 1);
-  static const bool pdl = [] {  // DSGD_PDL=0: plain stream-ordered launches
-    const char* e = getenv("DSGD_PDL");
-    return !(e && e[0] == '0');
-  }();
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(g);
-  cfg.blockDim = dim3(kBlock);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
   ++g_launches;
-  if (a.node[0].norm) return cudaLaunchKernelEx(&cfg, k_local_tma<T, true>, a);
-  return cudaLaunchKernelEx(&cfg, k_local_tma<T, false>, a);
+  if (a.node[0].norm) return launch_pdl(k_local_tma<T, true>, g, kBlock, smem, s, a);
+  return launch_pdl(k_local_tma<T, false>, g, kBlock, smem, s, a);
 }
 
 // Two-shot all-reduce delta kernel (kModeArDelta / kModeApplyDelta) of one

@@ -180,6 +180,7 @@ struct dsgd_ctx {
   bool ar_tma = true;              // ... staging the peer reads through smem (bulk async copies)
   bool ar_nvls = false;            // ... two-shot with the reduce/broadcast in the NVSwitch
   uint32_t ar_pipes = 2;           // two-shot: independent pipelines (streams) over d
+  bool ar_pipes_env = false;       // DSGD_AR_PIPES given (no size-based choice)
   double ar_delta_frac = 2.0;      // delta-kernel CTAs per SM, split over the pipelines
   double ar_comm_frac = 2.0;       // reduce-kernel CTAs per SM, split over the pipelines
   cudaStream_t pipe_stream[4] = {};
@@ -812,7 +813,7 @@ void ar_waits(dsgd_ctx* c, int which, unsigned long long need, dsgd::WaitSpec* w
 // Joins the two-shot pipeline streams back into the context stream.
 dsgd_status join_pipes(dsgd_ctx* c) {
   if (!c->pipes_forked) return DSGD_OK;
-  for (uint32_t h = 0; h < c->ar_pipes; ++h) {
+  for (uint32_t h = 0; h < 4; ++h) {  // every pipeline stream (the size table may pick 4)
     DSGD_CUDA(cudaEventRecord(c->pipe_event[h], c->pipe_stream[h]));
     DSGD_CUDA(cudaStreamWaitEvent(c->stream, c->pipe_event[h], 0));
   }
@@ -824,7 +825,7 @@ dsgd_status join_pipes(dsgd_ctx* c) {
 // (e.g. the caller's gradient upload).  Recorded every round.
 dsgd_status fork_pipes(dsgd_ctx* c) {
   DSGD_CUDA(cudaEventRecord(c->pipe_event[4], c->stream));
-  for (uint32_t h = 0; h < c->ar_pipes; ++h)
+  for (uint32_t h = 0; h < 4; ++h)
     DSGD_CUDA(cudaStreamWaitEvent(c->pipe_stream[h], c->pipe_event[4], 0));
   c->pipes_forked = true;
   return DSGD_OK;
@@ -1022,8 +1023,12 @@ dsgd_status do_allreduce_p2p(dsgd_ctx* c, const dsgd_hyperparams* h, const GradS
   // reduce overlaps pipeline h'`s HBM-bound delta kernel.
   if (t == 0) {  // the split is fixed for the context's lifetime (counters per pipeline)
     uint32_t k0 = c->ar_pipes;
+    // NVLS at >= ~700M per worker: 4 pipelines (10.37 vs 11.37 ms per round
+    // at 1B, p = 4, profiles/r2_split_n4.md) unless DSGD_AR_PIPES is set
+    if (!c->ar_pipes_env && c->ar_nvls && c->d >= (700ull << 20)) k0 = 4;
     // small d is latency-bound: one pipeline (fewer launches / cross-GPU waits)
-    if (c->d < (8u << 20) || k0 * c->p > (uint32_t)kMaxWait) k0 = 1;
+    if (c->d < (8u << 20)) k0 = 1;
+    while (k0 > 1 && k0 * c->p > (uint32_t)kMaxWait) k0 /= 2;  // wait slots per kernel
     c->ar_pipes_used = k0;
   }
   const uint32_t K = c->ar_pipes_used;
@@ -1393,9 +1398,14 @@ void attach_nvls(dsgd_ctx* c, char* x, char* x_mc, char* avg, char* avg_mc) {
   c->nvls_note.clear();
   // reduce CTAs on SMs of their own (1024 threads, padded smem) and a wider
   // delta grid: 271.5 vs 328.7 us/round at p = 4, d = 25M
-  // (profiles/r1_tune_allreduce_n4.md); the environment still overrides
-  if (!std::getenv("DSGD_AR_DELTA_FRAC")) c->ar_delta_frac = 1.5;
-  if (!std::getenv("DSGD_AR_COMM_FRAC")) c->ar_comm_frac = 0.5;
+  // (profiles/r1_tune_allreduce_n4.md).  Per-worker size table measured at
+  // p = 4 (profiles/r2_split_n4.md): 1.5 / 0.5 CTAs per SM up to ~200M, 1.25
+  // / 0.75 from there to ~700M, 1.5 / 0.5 with 4 pipelines above (see
+  // ar_pipes_for).  p = 8 runs the same table (no 8-GPU box measured it).
+  // The environment still overrides.
+  const bool mid = c->d >= (200ull << 20) && c->d < (700ull << 20);
+  if (!std::getenv("DSGD_AR_DELTA_FRAC")) c->ar_delta_frac = mid ? 1.25 : 1.5;
+  if (!std::getenv("DSGD_AR_COMM_FRAC")) c->ar_comm_frac = mid ? 0.75 : 0.5;
 }
 
 void attach_mc_state(dsgd_ctx* c) {
@@ -1594,7 +1604,10 @@ dsgd_status dsgd_ctx_create(const dsgd_ctx_desc* desc, dsgd_ctx** out) {
     c->trace_cap = (uint32_t)std::max(1, atoi(e));
     if (c->trace_cap < 64) c->trace_cap = 65536;
   }
-  if (const char* e = std::getenv("DSGD_AR_PIPES")) c->ar_pipes = (uint32_t)std::min(4, std::max(1, atoi(e)));
+  if (const char* e = std::getenv("DSGD_AR_PIPES")) {
+    c->ar_pipes = (uint32_t)std::min(4, std::max(1, atoi(e)));
+    c->ar_pipes_env = true;
+  }
   if (const char* e = std::getenv("DSGD_AR_DELTA_FRAC")) c->ar_delta_frac = std::max(0.05, atof(e));
   if (const char* e = std::getenv("DSGD_AR_COMM_FRAC")) c->ar_comm_frac = std::max(0.05, atof(e));
 

@@ -135,10 +135,13 @@ def test_inproc_allreduce_backends_staged_sizes(world, backend, dtype, monkeypat
     check(res, "all-reduce")
 
 
+@pytest.mark.parametrize("pipes", [2, 4])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
-def test_inproc_two_shot_two_pipelines(dtype, monkeypatch):
-    """d >= 8M per rank: the two-shot round splits d into 2 pipelines (own
-    counters per pipeline); all four ranks' exchanges, then the reduces."""
+def test_inproc_two_shot_pipelines(dtype, pipes, monkeypatch):
+    """d >= 8M per rank: the two-shot round splits d into 2 (default) or 4
+    (the >= 700M-per-worker default) pipelines with own counters; all four
+    ranks' exchanges, then the reduces."""
+    monkeypatch.setenv("DSGD_AR_PIPES", str(pipes))
     res = run_group("all-reduce", 4, dtype, (8 << 20) + 1031, 3, monkeypatch, backend="p2p",
                     sigma=None)
     check(res, "all-reduce")
