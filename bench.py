@@ -427,6 +427,22 @@ def main():
             roofline["peak"] = nv_peak
             roofline["peak_source"] = "B200_PROFILING.md measured peer copy per direction"
             roofline["frac"] = roofline["achieved"] / nv_peak
+        # the same kernel against the raw link: NVLink packet bytes per data
+        # byte and the best raw rate of one SM-issued stream, both from
+        # PRIOR ncu link-counter captures (profiles/r2_nvlink_ncu.md)
+        if nn:
+            # busiest direction: NVLS 1.41 both ways; one-shot tx = served
+            # reads (1.125) + the peer's read requests (0.1875); p2p two-shot
+            # tx (stores + requests) 1.37-1.50
+            raw = {"nvls": 1.41, "oneshot": 1.3125, "p2p": 1.44}.get(backend)
+            if raw:
+                roofline["nvlink_raw"] = {
+                    "raw_bytes_per_data_byte": raw,
+                    "achieved_raw_gbs": nv_launch / t_c / 1e9 * raw,
+                    "raw_ceiling_gbs": 690.0,
+                    "frac_of_raw_ceiling": nv_launch / t_c / 1e9 * raw / 690.0,
+                    "source": "prior ncu nvl{rx,tx}__bytes captures (profiles/r2_nvlink_ncu.md, "
+                              "r2_ncu_nvlink/*.csv), not measured in this run"}
     per_kernel = {k: {"ms_total": v[0], "launches": v[1]} for k, v in prof.items() if v[1]}
 
     # ---------------- end-to-end through the C ABI (host gradients, pinned)
