@@ -439,8 +439,10 @@ def main():
                 roofline["nvlink_raw"] = {
                     "raw_bytes_per_data_byte": raw,
                     "achieved_raw_gbs": nv_launch / t_c / 1e9 * raw,
-                    "raw_ceiling_gbs": 690.0,
-                    "frac_of_raw_ceiling": nv_launch / t_c / 1e9 * raw / 690.0,
+                    # the highest raw rate seen on this pool: the tx side of
+                    # the N=2 one-shot round (served reads + requests)
+                    "raw_ceiling_gbs": 755.0,
+                    "frac_of_raw_ceiling": nv_launch / t_c / 1e9 * raw / 755.0,
                     "source": "prior ncu nvl{rx,tx}__bytes captures (profiles/r2_nvlink_ncu.md, "
                               "r2_ncu_nvlink/*.csv), not measured in this run"}
     per_kernel = {k: {"ms_total": v[0], "launches": v[1]} for k, v in prof.items() if v[1]}
