@@ -56,7 +56,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--d", type=int, default=D_DEFAULT)
+    # --params: the same (torchrun's own parser rejects "--d" as ambiguous)
+    ap.add_argument("--d", "--params", dest="d", type=int, default=D_DEFAULT)
     ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
     ap.add_argument("--no-extras", action="store_true", help="skip the gossip/EASGD extra lines")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
