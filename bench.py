@@ -693,14 +693,16 @@ def run_extras(args, local, h):
         ms = e0.elapsed_time(e1) / k
         hbm, _ = peaks()
         byts = 48 * d  # theta, delta, s, opt read + theta', delta' written, fp64
-        ref_s = cpu_reference(0, 1, d, 2, False, grad="quadratic") / 2 \
+        shards = host_shards(1, False)
+        ref_s = cpu_reference(0, 1, d, 4, False, grad="quadratic", shards=shards) / 4 \
             if not args.no_cpu else None
         out[name] = {"ms_per_round": ms, "param_updates_per_s": d / (ms * 1e-3),
                      "hbm_gbs": byts / (ms * 1e-3) / 1e9, "hbm_frac": byts / (ms * 1e-3) / 1e9 / hbm,
                      "bytes_per_param": 48,
                      "reference_cpu_param_updates_per_s": (d / ref_s) if ref_s else None,
-                     "reference_cpu_sample": "2 allreduce_round of the compiled reference, "
-                                             "QuadraticObjective(1, 0), p=1, 1 thread"}
+                     "reference_cpu_sample": f"4 allreduce_round of the compiled reference, "
+                                             f"QuadraticObjective(1, 0), p=1, d split over "
+                                             f"{shards} host threads"}
         grp.close()
         del ones, zeros, th
         torch.cuda.empty_cache()

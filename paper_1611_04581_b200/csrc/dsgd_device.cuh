@@ -142,6 +142,11 @@ __device__ __forceinline__ bool wait_flag_gpu(const unsigned long long* p, unsig
 }
 
 __device__ __forceinline__ bool block_wait(const WaitSpec& w) {
+  // programmatic dependent launch: a kernel that starts with block_wait may
+  // be launched while the previous kernel of its stream drains; nothing of
+  // it touches global memory before that grid has completed
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const bool tr = w.trace && blockIdx.x == 0 && threadIdx.x == 0;
   if (tr) w.trace[0] = globaltimer();
   if (w.n == 0) {

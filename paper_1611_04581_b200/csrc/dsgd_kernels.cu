@@ -75,6 +75,15 @@ extern thread_local uint64_t g_launches;
     __VA_ARGS__;          \
   } while (0)
 
+// a counted launch with programmatic dependent launch (the kernel must start
+// with griddepcontrol.wait -- block_wait does -- before any global access)
+#define DSGD_PDL_LAUNCH(kernel, grid, block, smem, stream, args)                    \
+  do {                                                                              \
+    ++g_launches;                                                                   \
+    const cudaError_t e_ = launch_pdl(kernel, grid, block, smem, stream, args);     \
+    if (e_ != cudaSuccess) return e_;                                               \
+  } while (0)
+
 // compute_local_delta protocols.cpp:85-100 for one coordinate:
 //   la = mu != 0 ? theta + mu*delta_prev : theta          (92-93)
 //   g  = obj.stochastic_gradient(la)                       (30; quadratic: objectives.cpp:75)
@@ -841,11 +850,11 @@ cudaError_t launch_ar_nvls(const ArNvlsArgs<T>& a, uint32_t grid, cudaStream_t s
   // one padded CTA per SM: 1024 threads keep enough switch reductions in flight
   const int threads = pad ? 1024 : kBlock;
   if (unroll == 8)
-    DSGD_COUNTED(k_ar_nvls<T, 8><<<grid, threads, pad, s>>>(a));
+    DSGD_PDL_LAUNCH((k_ar_nvls<T, 8>), grid, threads, pad, s, a);
   else if (unroll == 2)
-    DSGD_COUNTED(k_ar_nvls<T, 2><<<grid, threads, pad, s>>>(a));
+    DSGD_PDL_LAUNCH((k_ar_nvls<T, 2>), grid, threads, pad, s, a);
   else
-    DSGD_COUNTED(k_ar_nvls<T, 4><<<grid, threads, pad, s>>>(a));
+    DSGD_PDL_LAUNCH((k_ar_nvls<T, 4>), grid, threads, pad, s, a);
   return cudaGetLastError();
 }
 
@@ -1180,7 +1189,7 @@ cudaError_t launch_os2(const ArOneShotArgs<T>& a, int max_ctas, cudaStream_t s) 
   const uint64_t tiles = a.d / os_tile<T>();
   uint32_t g = (uint32_t)sms * (uint32_t)resident;
   if (tiles < g) g = (uint32_t)(tiles ? tiles : 1);
-  DSGD_COUNTED(k_ar_oneshot_tma2<T, P, S><<<g, kBlock, smem, s>>>(a));
+  DSGD_PDL_LAUNCH((k_ar_oneshot_tma2<T, P, S>), g, kBlock, smem, s, a);
   return cudaGetLastError();
 }
 
@@ -1602,9 +1611,9 @@ cudaError_t launch_ard_tma(int mode, const StepArgs<T>& a, uint32_t grid, cudaSt
   const uint64_t tiles = a.d / lt_tile<T>();
   if (tiles < grid) grid = (uint32_t)(tiles ? tiles : 1);
   if (mode == kModeApplyDelta)
-    DSGD_COUNTED(k_ard_tma<T, kModeApplyDelta><<<grid, kBlock, smem, s>>>(a));
+    DSGD_PDL_LAUNCH((k_ard_tma<T, kModeApplyDelta>), grid, kBlock, smem, s, a);
   else
-    DSGD_COUNTED(k_ard_tma<T, kModeArDelta><<<grid, kBlock, smem, s>>>(a));
+    DSGD_PDL_LAUNCH((k_ard_tma<T, kModeArDelta>), grid, kBlock, smem, s, a);
   return cudaGetLastError();
 }
 
@@ -1962,6 +1971,8 @@ __global__ void __launch_bounds__(kEcThreads, 1)
   const uint64_t G = gridDim.x;
   const uint64_t mine = nfull > blockIdx.x ? (nfull - 1 - blockIdx.x) / G + 1 : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // PDL (see block_wait)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (threadIdx.x == 0) {
     for (int sg = 0; sg < kEcStages; ++sg) {
       mbar_init(&full[sg], 1);
@@ -2162,7 +2173,7 @@ cudaError_t launch_ea_chain(const EaChainArgs<T>& a, int vec, uint32_t grid, cud
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const uint64_t nfull = a.d / st_tile<T>();
     const uint32_t g = (uint32_t)std::min<uint64_t>(nfull, (uint64_t)sms);
-    DSGD_COUNTED(k_ea_chain_tma<T><<<g, kEcThreads, smem, s>>>(a));
+    DSGD_PDL_LAUNCH(k_ea_chain_tma<T>, g, kEcThreads, smem, s, a);
     return cudaGetLastError();
   }
   if (vec)
