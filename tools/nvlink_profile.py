@@ -35,7 +35,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=2)
     ap.add_argument("--protocol", default="all-reduce", choices=sorted(PROTO))
-    ap.add_argument("--d", type=int, default=25_000_000)
+    ap.add_argument("--d", "--params", dest="d", type=int, default=25_000_000)
     ap.add_argument("--rounds", type=int, default=6)
     ap.add_argument("--warmup", type=int, default=2)
     a = ap.parse_args()

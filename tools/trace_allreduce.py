@@ -15,7 +15,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--d", type=int, default=25_000_000)
+    ap.add_argument("--d", "--params", dest="d", type=int, default=25_000_000)
     ap.add_argument("--rounds", type=int, default=20)
     a = ap.parse_args()
     os.environ.setdefault("DSGD_TRACE", "4096")
@@ -51,6 +51,13 @@ def main():
     if len(t):
         span = (t.max() - t.min()) / 1e3
         out.append(f"  span {span:.1f} us over {a.rounds} rounds = {span / a.rounds:.1f} us/round")
+        # launch gap: the next kernel's entry stamp after this one's done stamp
+        order = np.argsort(t[:, 0])
+        ts = t[order]
+        gaps = (ts[1:, 0] - ts[:-1, 2]) / 1e3
+        if len(gaps):
+            out.append(f"  entry(k+1) - done(k): median {np.median(gaps):.1f} us "
+                       f"(negative = overlapped by programmatic dependent launch)")
         # per round: first entry to last done
     res = [None] * world
     dist.all_gather_object(res, "\n".join(out))
