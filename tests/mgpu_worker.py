@@ -36,8 +36,14 @@ def main():
         timeout_case(rank, world, local, dtype, dist)
         return
     for proto, oid in names.items():
-        # EASGD: a staged chain with several chunks per CTA and a ragged tail
+        # EASGD: a staged chain with several chunks per CTA and a ragged tail;
+        # MGPU_AR_D / MGPU_ROUNDS: the all-reduce at a size that takes the
+        # multi-pipeline two-shot path
         d = 1031 if proto != "elastic-avg" else 148 * 5 * 2048 + 1031
+        rounds = 25
+        if proto.startswith("all-reduce") and os.environ.get("MGPU_AR_D"):
+            d = int(os.environ["MGPU_AR_D"])
+            rounds = int(os.environ.get("MGPU_ROUNDS", "6"))
         hk = dict(alpha0=0.05, anneal_at=(20,), mu=0.9, weight_decay=1e-4, beta_gossip=0.4,
                   beta_ea=0.15, tau=1)
         ar = proto.startswith("all-reduce")
@@ -45,13 +51,13 @@ def main():
         cfg = O.SimConfig(protocol=oid, p=world, hyper=O.HyperParams(**hk), sigma=0.05,
                           spectrum=list(np.linspace(0.5, 2.0, d)),
                           init_kind=O.INIT_OFFSET_ONES if ar else O.INIT_GAUSSIAN,
-                          rounds=25, per_node_scope=pn, run_id=f"mg/{proto}")
+                          rounds=rounds, per_node_scope=pn, run_id=f"mg/{proto}")
         obj = P.QuadraticObjective(cfg.spectrum)
         dcfg = D.SimConfig(protocol="all-reduce" if ar else proto, p=world, hyper=Hyperparams(**hk),
                            noise=P.NoiseModel.gaussian_per_coord(0.05, d),
                            init=D.InitSpec("offset-ones" if ar else "gaussian-spread"),
                            momentum_scope="per-node" if pn else "aggregate",
-                           rounds=25, run_id=f"mg/{proto}")
+                           rounds=rounds, run_id=f"mg/{proto}")
         thetas = D.make_initial_nodes(dcfg, obj)
         g = Group.distributed(d, rank, world, local, dtype=dtype, quadratic=True, noise=True,
                               center=proto == "elastic-avg")
@@ -70,7 +76,7 @@ def main():
             g.set_center(c.astype(np.float64))
         dist.barrier()
         g.seed_streams(1, f"mg/{proto}")
-        g.run_rounds(D.PROTOCOLS[dcfg.protocol], Hyperparams(**hk), 25,
+        g.run_rounds(D.PROTOCOLS[dcfg.protocol], Hyperparams(**hk), rounds,
                      scope="per-node" if pn else "aggregate",
                      grad="quadratic", host_noise_sigma=0.05)
         g.sync()

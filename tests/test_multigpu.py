@@ -123,3 +123,29 @@ def test_multi_gpu_three_ranks_match_oracle():
             assert r["bit_exact"], (proto, r)
         if r["center_exact"] is not None:
             assert r["center_exact"], (proto, r)
+
+
+@pytest.mark.skipif("n_gpus() < 2")
+@pytest.mark.parametrize("backend,pipes", [("nvls", 4), ("nvls", 2), ("p2p", 4)])
+def test_multi_gpu_two_shot_pipelines(backend, pipes):
+    """The two-shot all-reduce at a size that splits d into pipelines
+    (8M + 1031 per rank, both momentum scopes): the NVLS reduce on its own
+    SMs with 2 / 4 pipelines (the >= 700M default) within tolerance and
+    every rank identical; the peer-memory ring reduce bit-exact with the
+    reference's threaded transport."""
+    world = min(4, n_gpus())
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr", "127.0.0.1", "--master-port",
+           str(29751 + pipes + (backend == "p2p")),
+           os.path.join(ROOT, "tests", "mgpu_worker.py"), "f32", "allreduce-only"]
+    env = dict(os.environ, DSGD_ALLREDUCE=backend, DSGD_AR_PIPES=str(pipes),
+               MGPU_AR_D=str((8 << 20) + 1031), MGPU_ROUNDS="6")
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    res = json.loads([l for l in out.stdout.splitlines() if l.startswith("RESULT ")][0][7:])
+    for proto, r in res.items():
+        assert r["ranks_identical"], (proto, r)
+        if r["nvls"]:
+            assert r["max_rel"] <= 1e-5, (proto, r)
+        else:
+            assert r["bit_exact"], (proto, r)
