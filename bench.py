@@ -407,6 +407,22 @@ def main():
         if single and kname == "allreduce_comm":
             t_c = kavg_ms * 1e-3  # the timed region's own per-launch time
         nv_launch = nv_bytes * (args.steps / nn if nn else 1.0)  # per launch (K pipelines)
+        if nn and nn > args.steps:
+            # K > 1 pipelines: their reduce kernels overlap each other and the
+            # delta kernels, so a per-launch event span includes the others'
+            # time; the comm kernels are active across the whole round, so the
+            # round's NVLink bytes over the round time is the kernel's rate
+            t_c = ms * 1e-3
+            nv_launch = nv_bytes
+            roofline["kernel_timing"] = ("K overlapping pipelines: NVLink bytes per round / "
+                                         "round time (per-launch events would double-count "
+                                         "the overlap)")
+            roofline["kernel_avg_us"] = ms * 1e3
+            if roofline.get("achieved") and kname == "allreduce_comm":
+                roofline["achieved"] = bpp * d / (ms * 1e-3) / 1e9
+                roofline["frac"] = roofline["achieved"] / peak
+                roofline["frac_of_roofline_time"] = roofline["roofline_time_us"] * kn / args.steps \
+                    / (ms * 1e3)
         roofline["allreduce_backend"] = backend
         roofline["allreduce_launches_per_round"] = nn / args.steps if nn else None
         note = grp.allreduce_info()[1]
