@@ -80,6 +80,11 @@ struct SignalSpec {
   unsigned long long value;
   unsigned int* arrive;         // grid arrival counter (own device memory)
   unsigned long long* trace;    // DSGD_TRACE: [2] last CTA done
+  // 1: the kernel writes only this GPU's memory (peers read it through our
+  // L2), so each CTA's arrival is a gpu-scope release and only the last CTA
+  // issues the system-scope release of the counter (DSGD_SIGNAL_GPU=0: the
+  // per-CTA system fence everywhere)
+  int local_only;
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
@@ -179,6 +184,21 @@ __device__ __forceinline__ void block_signal(const SignalSpec& s) {
     return;
   }
   __syncthreads();
+  if (s.local_only && threadIdx.x == 0) {
+    // release at gpu scope (cumulative over the CTA's writes, ordered by the
+    // barrier); the last arrival acquires every CTA's writes and publishes
+    // them to the peers with one system-scope release
+    const unsigned total = gridDim.x * gridDim.y;
+    unsigned prev;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(s.arrive)
+                 : "memory");
+    if (prev == total - 1) {
+      atomicExch(s.arrive, 0u);
+      st_release_sys(s.counter, s.value);
+      if (s.trace) s.trace[2] = globaltimer();
+    }
+    return;
+  }
   if (threadIdx.x == 0) {
     __threadfence_system();
     const unsigned total = gridDim.x * gridDim.y;

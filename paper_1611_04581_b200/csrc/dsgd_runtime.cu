@@ -573,7 +573,17 @@ dsgd_status all_peer_waits(dsgd_ctx* c, unsigned long long value, dsgd::WaitSpec
   return DSGD_OK;
 }
 
-void build_signal(dsgd_ctx* c, dsgd::SignalSpec* s) {
+// local_writes: the kernel stores only into this GPU's memory (see
+// SignalSpec::local_only)
+bool signal_gpu_scope() {
+  static const bool on = [] {  // DSGD_SIGNAL_GPU=0: a system fence in every CTA
+    const char* e = std::getenv("DSGD_SIGNAL_GPU");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+void build_signal(dsgd_ctx* c, dsgd::SignalSpec* s, bool local_writes = true) {
   if (!c->distributed()) {
     s->counter = nullptr;
     return;
@@ -581,6 +591,7 @@ void build_signal(dsgd_ctx* c, dsgd::SignalSpec* s) {
   s->counter = c->round_ptr(0);
   s->value = c->seq + 1;
   s->arrive = c->arrive;
+  s->local_only = local_writes && signal_gpu_scope() ? 1 : 0;
 }
 
 template <typename T>
@@ -1005,6 +1016,7 @@ dsgd_status do_allreduce_p2p(dsgd_ctx* c, const dsgd_hyperparams* h, const GradS
     a.signal.counter = c->peers[me].ar + 0;
     a.signal.value = t + 1;
     a.signal.arrive = c->arrive;
+    a.signal.local_only = signal_gpu_scope() ? 1 : 0;  // x', theta', delta: own memory
     trace_slot(c, DSGD_K_NCCL, &a.wait, &a.signal);
     const bool vec = all_aligned(c, gs);
     const uint64_t W = vec ? 16 / sizeof(T) : 1;
@@ -1071,6 +1083,7 @@ dsgd_status do_allreduce_p2p(dsgd_ctx* c, const dsgd_hyperparams* h, const GradS
       a.signal.counter = c->peers[me].ar + 2 * pi;
       a.signal.value = t + 1;
       a.signal.arrive = arrive;
+      a.signal.local_only = signal_gpu_scope() ? 1 : 0;  // x', theta', delta: own memory
       trace_slot(c, DSGD_K_AR_DELTA + 16 * pi, &a.wait, &a.signal);
       LaunchScope ls(c, DSGD_K_AR_DELTA, st);
       const int mode = fused ? dsgd::kModeApplyDelta : dsgd::kModeArDelta;
@@ -1237,7 +1250,10 @@ dsgd_status do_ea(dsgd_ctx* c, const dsgd_hyperparams* h, const GradSel& gs, int
   a.quad = gs.quad;
   a.timeout_ns = c->timeout_ns;
   a.error = c->error;
-  build_signal(c, &a.signal);
+  // the center goes into the next rank's memory, but every chunk of it is
+  // published with its own system-scope release (flag) before the CTA
+  // arrives, so the round counter needs only the gpu-scope arrival chain
+  build_signal(c, &a.signal, true);
   const bool vec = all_aligned(c, gs);
   // one CTA per chunk: a CTA blocked on its flag or in its release fence
   // leaves the SM to the other resident chunks (dispatch is in chunk order,
