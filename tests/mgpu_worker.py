@@ -137,8 +137,11 @@ def timeout_case(rank, world, local, dtype, dist):
     from paper_1611_04581_b200.engine import Group, Hyperparams
     h = Hyperparams(alpha0=0.1, anneal_at=(), mu=0.9, weight_decay=0.0)
     res = {}
-    for proto in ("pull-gossip", "all-reduce"):
-        g = Group.distributed(4096, rank, world, local, dtype=dtype, quadratic=True)
+    for proto in ("pull-gossip", "all-reduce", "elastic-avg"):
+        # elastic-avg: rank 0's second gated round waits for the ring closure
+        # from rank p-1 inside the staged chain kernel's producer warp
+        g = Group.distributed(4096, rank, world, local, dtype=dtype, quadratic=True,
+                              center=proto == "elastic-avg")
         g.set_timeout(0.5)
         g.set_quadratic(np.ones(4096))
         g.set_state(0, np.full(4096, float(rank)))
@@ -150,6 +153,8 @@ def timeout_case(rank, world, local, dtype, dist):
                 for _ in range(2):
                     if proto == "pull-gossip":
                         g.pull_gossip_round(h, [1] + [0] * (world - 1), grad="quadratic")
+                    elif proto == "elastic-avg":
+                        g.ea_round(h, gated=True, grad="quadratic")
                     else:
                         g.allreduce_round(h, grad="quadratic")
                 g.sync()
