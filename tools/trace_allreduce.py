@@ -17,6 +17,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--d", "--params", dest="d", type=int, default=25_000_000)
     ap.add_argument("--rounds", type=int, default=20)
+    ap.add_argument("--protocol", default="all-reduce",
+                    choices=["all-reduce", "pull-gossip", "elastic-avg"])
     a = ap.parse_args()
     os.environ.setdefault("DSGD_TRACE", "4096")
     import torch
@@ -26,13 +28,19 @@ def main():
     rank, world, local = (int(os.environ[k]) for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK"))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    g = Group.distributed(a.d, rank, world, local, dtype="f32", grad=True)
+    proto = {"all-reduce": N.ALLREDUCE, "pull-gossip": N.PULL_GOSSIP,
+             "elastic-avg": N.ELASTIC_AVG}[a.protocol]
+    g = Group.distributed(a.d, rank, world, local, dtype="f32", grad=True,
+                          center=proto == N.ELASTIC_AVG)
     pool = [torch.randn(a.d, device="cuda") for _ in range(2)]
-    h = Hyperparams(alpha0=0.1, anneal_at=(), mu=0.9, weight_decay=1e-4)
-    g.run_rounds(N.ALLREDUCE, h, 5, grad_pool=[t.data_ptr() for t in pool])
+    h = Hyperparams(alpha0=0.1, anneal_at=(), mu=0.9, weight_decay=1e-4, beta_ea=0.1)
+    if proto == N.ELASTIC_AVG:
+        g.ea_init_center()
+    g.seed_streams(1, "run/trial0")
+    g.run_rounds(proto, h, 5, grad_pool=[t.data_ptr() for t in pool])
     g.sync()
     dist.barrier()
-    g.run_rounds(N.ALLREDUCE, h, a.rounds, grad_pool=[t.data_ptr() for t in pool])
+    g.run_rounds(proto, h, a.rounds, grad_pool=[t.data_ptr() for t in pool])
     g.sync()
     tr = g.trace_dump()
     os.makedirs("gpurun_out", exist_ok=True)
