@@ -412,17 +412,17 @@ def main():
             # delta kernels, so a per-launch event span includes the others'
             # time; the comm kernels are active across the whole round, so the
             # round's NVLink bytes over the round time is the kernel's rate
-            t_c = ms * 1e-3
+            t_c = step_ms * 1e-3
             nv_launch = nv_bytes
             roofline["kernel_timing"] = ("K overlapping pipelines: NVLink bytes per round / "
                                          "round time (per-launch events would double-count "
                                          "the overlap)")
-            roofline["kernel_avg_us"] = ms * 1e3
+            roofline["kernel_avg_us"] = step_ms * 1e3
             if roofline.get("achieved") and kname == "allreduce_comm":
-                roofline["achieved"] = bpp * d / (ms * 1e-3) / 1e9
+                roofline["achieved"] = bpp * d / (step_ms * 1e-3) / 1e9
                 roofline["frac"] = roofline["achieved"] / peak
                 roofline["frac_of_roofline_time"] = roofline["roofline_time_us"] * kn / args.steps \
-                    / (ms * 1e3)
+                    / (step_ms * 1e3)
         roofline["allreduce_backend"] = backend
         roofline["allreduce_launches_per_round"] = nn / args.steps if nn else None
         note = grp.allreduce_info()[1]
