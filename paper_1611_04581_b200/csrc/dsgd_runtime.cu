@@ -1083,7 +1083,11 @@ dsgd_status do_allreduce_p2p(dsgd_ctx* c, const dsgd_hyperparams* h, const GradS
       a.signal.counter = c->peers[me].ar + 2 * pi;
       a.signal.value = t + 1;
       a.signal.arrive = arrive;
-      a.signal.local_only = signal_gpu_scope() ? 1 : 0;  // x', theta', delta: own memory
+      // per-CTA system fences here: the reduce of every rank starts on this
+      // counter, and one GPU-wide fence in the last CTA publishes it later
+      // than the CTAs' own fences do (N=4: 272 vs 289-310 us per round,
+      // profiles/r2_small_d.md)
+      a.signal.local_only = 0;
       trace_slot(c, DSGD_K_AR_DELTA + 16 * pi, &a.wait, &a.signal);
       LaunchScope ls(c, DSGD_K_AR_DELTA, st);
       const int mode = fused ? dsgd::kModeApplyDelta : dsgd::kModeArDelta;
