@@ -71,13 +71,19 @@ def sweep(a):
                     print(json.dumps({"config": "configs[4]", "protocol": name, "p": p, "d": d,
                                       "skipped": "time budget"}), flush=True)
                     continue
-                for threaded in ((True, False) if d <= (64 << 20) else (True,)):
-                    sec = O.ref_time_rounds(proto, p, d, 1, threaded, h, "pool")
+                nthr = len(os.sched_getaffinity(0))
+                # every host thread: d split into coordinate shards, one
+                # reference run (simulator rules) per shard, concurrently
+                runs = [("simulator rules, all threads (coordinate shards)", False, nthr)]
+                if d <= (64 << 20):  # the reference's own threaded transport
+                    runs.append(("run_transport (threads)", True, 1))
+                if d <= (16 << 20):
+                    runs.append(("simulator rules (1 thread)", False, 1))
+                for path, threaded, shards in runs:
+                    sec = O.ref_time_rounds(proto, p, d, 1, threaded, h, "pool", shards)
+                    threads = (p + (1 if proto == O.ELASTIC else 0)) if threaded else shards
                     print(json.dumps({"config": "configs[4]", "protocol": name, "p": p, "d": d,
-                                      "path": "run_transport (threads)" if threaded
-                                              else "simulator rules (1 thread)",
-                                      "threads": (p + (1 if proto == O.ELASTIC else 0))
-                                      if threaded else 1,
+                                      "path": path, "threads": threads,
                                       "s_per_round": sec, "param_updates_per_s": p * d / sec,
                                       "grad": "pool of 4 synthetic N(0,1) vectors (plugin slot)"}),
                           flush=True)
