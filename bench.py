@@ -37,6 +37,9 @@ UNIT = "param-updates/s"
 D_DEFAULT = 25_000_000
 POOL = 4
 SPEC_HBM_GBS = 8000.0  # the north star's ~8 TB/s HBM denominator (DGX B200 spec)
+# highest raw NVLink rate per direction seen on this pool (ncu nvltx on the N=2
+# one-shot round's serving side; profiles/r2_nvlink_ncu.md)
+RAW_CEIL = 755.0
 
 
 def workload_config(d: int, world: int) -> dict:
@@ -458,8 +461,8 @@ def main():
                     "achieved_raw_gbs": nv_launch / t_c / 1e9 * raw,
                     # the highest raw rate seen on this pool: the tx side of
                     # the N=2 one-shot round (served reads + requests)
-                    "raw_ceiling_gbs": 755.0,
-                    "frac_of_raw_ceiling": nv_launch / t_c / 1e9 * raw / 755.0,
+                    "raw_ceiling_gbs": RAW_CEIL,
+                    "frac_of_raw_ceiling": nv_launch / t_c / 1e9 * raw / RAW_CEIL,
                     "source": "prior ncu nvl{rx,tx}__bytes captures (profiles/r2_nvlink_ncu.md, "
                               "r2_ncu_nvlink/*.csv), not measured in this run"}
     per_kernel = {k: {"ms_total": v[0], "launches": v[1]} for k, v in prof.items() if v[1]}
@@ -807,25 +810,38 @@ def run_extras_dist(args, world, rank, local, h, max_over_ranks, barrier):
                 # each remote puller; bound per round = slowest GPU's NVLink / HBM
                 from paper_1611_04581_b200.engine import Stream, draw_pull_partners
                 st = [Stream.make(1, "run/trial0", i, "partner-choice") for i in range(world)]
-                t_bound = 0.0
+                t_bound = t_raw = 0.0
                 for r in range(3 + k):
                     pm = draw_pull_partners(st) if r > 0 else list(range(world))
                     if r < 3:
                         continue
-                    worst = 0.0
+                    worst = raw_worst = 0.0
                     for i in range(world):
                         pullers = sum(1 for q in range(world) if pm[q] == i and q != i)
                         nin = 4 * d if pm[i] != i else 0
                         t_nv = max(nin, 4 * d * pullers) / (nv * 1e9)
                         t_hbm = (20 + 4 * pullers) * d / (hbm * 1e9)
                         worst = max(worst, t_nv, t_hbm)
+                        # raw link: bulk peer reads carry 1.125 raw bytes per
+                        # data byte in, plus 0.1875 of read requests out
+                        raw_in, raw_out = 1.125 * nin, 1.125 * 4 * d * pullers + 0.1875 * nin
+                        raw_worst = max(raw_worst, max(raw_in, raw_out) / (RAW_CEIL * 1e9),
+                                        t_hbm)
                     t_bound += worst
+                    t_raw += raw_worst
                 bound_ms = t_bound / k * 1e3
+                raw_ms = t_raw / k * 1e3
             else:
                 # chain: every rank 24 B/param HBM + 4 B/param center over NVLink
                 bound_ms = max(24 * d / (hbm * 1e9), 4 * d / (nv * 1e9)) * 1e3
+                # raw link: 16-B peer stores carry 1.196 raw bytes per data byte
+                raw_ms = max(24 * d / (hbm * 1e9), 1.196 * 4 * d / (RAW_CEIL * 1e9)) * 1e3
             out[name] = {"ms_per_round": ms, "param_updates_per_s": world * d / (ms * 1e-3),
-                         "roofline_ms_per_round": bound_ms, "frac_of_roofline": bound_ms / ms}
+                         "roofline_ms_per_round": bound_ms, "frac_of_roofline": bound_ms / ms,
+                         "raw_link_ms_per_round": raw_ms, "frac_of_raw_link": raw_ms / ms,
+                         "raw_link_note": f"packet overhead per access type and a {RAW_CEIL:.0f} "
+                                          "GB/s raw ceiling from prior ncu link-counter captures "
+                                          "(profiles/r2_nvlink_ncu.md)"}
             barrier()
             grp.close()
             del pool
