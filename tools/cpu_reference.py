@@ -58,7 +58,7 @@ def sweep(a):
     print(json.dumps({"host": host(), "mem_available_bytes": avail}), flush=True)
     protos = [("pull-gossip", O.PULL), ("elastic-avg", O.ELASTIC), ("all-reduce", O.ALLREDUCE)]
     t_start = time.time()
-    for d in (1 << 20, 4 << 20, 16 << 20, 64 << 20, 256 << 20, 1 << 30):
+    for d in [int(float(x)) for x in a.sizes.split(",")]:
         for p in (2, 4, 8):
             for name, proto in protos:
                 need = 6 * 8 * d * p
@@ -80,7 +80,13 @@ def sweep(a):
                 if d <= (16 << 20):
                     runs.append(("simulator rules (1 thread)", False, 1))
                 for path, threaded, shards in runs:
-                    sec = O.ref_time_rounds(proto, p, d, 1, threaded, h, "pool", shards)
+                    try:
+                        sec = O.ref_time_rounds(proto, p, d, 1, threaded, h, "pool", shards)
+                    except RuntimeError as e:  # e.g. the transport's own receive timeout
+                        print(json.dumps({"config": "configs[4]", "protocol": name, "p": p,
+                                          "d": d, "path": path,
+                                          "error": str(e) or "reference raised"}), flush=True)
+                        continue
                     threads = (p + (1 if proto == O.ELASTIC else 0)) if threaded else shards
                     print(json.dumps({"config": "configs[4]", "protocol": name, "p": p, "d": d,
                                       "path": path, "threads": threads,
@@ -95,6 +101,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--max-seconds", type=float, default=1800)
+    ap.add_argument("--sizes", default=f"{1 << 20},{4 << 20},{16 << 20},{64 << 20},{256 << 20},{1 << 30}")
     a = ap.parse_args()
     if a.sweep:
         return sweep(a)
