@@ -81,7 +81,10 @@ def sweep(a):
                     runs.append(("simulator rules (1 thread)", False, 1))
                 for path, threaded, shards in runs:
                     try:
-                        sec = O.ref_time_rounds(proto, p, d, 1, threaded, h, "pool", shards)
+                        # the transport is timed as (R + 1) - 1 rounds of whole runs:
+                        # R = 3 keeps the difference well above the run-to-run noise
+                        r = 3 if threaded else 1
+                        sec = O.ref_time_rounds(proto, p, d, r, threaded, h, "pool", shards) / r
                     except RuntimeError as e:  # e.g. the transport's own receive timeout
                         print(json.dumps({"config": "configs[4]", "protocol": name, "p": p,
                                           "d": d, "path": path,
