@@ -839,10 +839,13 @@ cudaError_t launch_ar_nvls(const ArNvlsArgs<T>& a, uint32_t grid, cudaStream_t s
   }();
   static const int unroll = [] {  // DSGD_NVLS_UNROLL: switch reductions in flight per thread
     const char* e = getenv("DSGD_NVLS_UNROLL");
-    const int u = e ? atoi(e) : 4;
-    return u >= 8 ? 8 : (u >= 4 ? 4 : 2);
+    // 2 measured best at p = 4, 25M (263 vs 272 / 287 us per round for 4 / 8,
+    // profiles/r2_nvls_knobs.md): more requests in flight congest the switch
+    const int u = e ? atoi(e) : 2;
+    return u >= 8 ? 8 : (u >= 4 ? 4 : (u >= 2 ? 2 : 1));
   }();
   if (pad) {
+    smem_attr(k_ar_nvls<T, 1>, pad);
     smem_attr(k_ar_nvls<T, 2>, pad);
     smem_attr(k_ar_nvls<T, 4>, pad);
     smem_attr(k_ar_nvls<T, 8>, pad);
@@ -851,6 +854,8 @@ cudaError_t launch_ar_nvls(const ArNvlsArgs<T>& a, uint32_t grid, cudaStream_t s
   const int threads = pad ? 1024 : kBlock;
   if (unroll == 8)
     DSGD_PDL_LAUNCH((k_ar_nvls<T, 8>), grid, threads, pad, s, a);
+  else if (unroll == 1)
+    DSGD_PDL_LAUNCH((k_ar_nvls<T, 1>), grid, threads, pad, s, a);
   else if (unroll == 2)
     DSGD_PDL_LAUNCH((k_ar_nvls<T, 2>), grid, threads, pad, s, a);
   else
