@@ -1930,14 +1930,16 @@ __global__ void __launch_bounds__(kBlock) k_ea_chain(const __grid_constant__ EaC
 // shared-memory ring as soon as a stage frees -- they do not depend on the
 // chain -- and the center tile once the previous rank has published it
 // (flag acquire, then proxy fence).  Warps 0-7 run the client update + SGD
-// step out of shared memory and write theta', delta' and the new center
-// back into the stage in place.  Warp 9 (signal) bulk-stores the three
-// tiles -- the center straight into the next rank's c_in over NVLink -- and,
-// once a chunk's bulk group has completed, publishes its flag with a
-// system-scope release; it runs one chunk behind, so neither the NVLink
-// write acknowledgement nor the flag wait ever stalls the arithmetic warps.
-// Per-coordinate operation order is k_ea_chain's (the single-context
-// sweep's) exactly.
+// step out of shared memory, store the new center straight into the next
+// rank's c_in with 16-B SM stores (NVLink) and write theta' / delta' back
+// into the stage; they arrive on the stage's named barrier.  Warp 9
+// (signal) waits there, bulk-stores theta' / delta' to local HBM, recycles
+// the stage and hands the chunk index to warp 10 (publisher), which issues
+// one system fence for every chunk handed over before it and then the
+// chunks' flags with relaxed system-scope stores.  Neither the NVLink write
+// acknowledgement (the fence) nor the flag wait ever sits on the path that
+// recycles stages (profiles/r2_ea_chain.md).  Per-coordinate operation
+// order is k_ea_chain's (the single-context sweep's) exactly.
 constexpr int kEcStages = 4;
 constexpr int kEcThreads = kBlock + 96;  // + producer, signal, publisher warps
 
