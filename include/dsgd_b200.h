@@ -179,7 +179,9 @@ dsgd_status dsgd_set_vector(dsgd_ctx* ctx, uint32_t local, dsgd_buffer which,
  * has fully arrived from rank p-1, so no host barrier is needed first. */
 dsgd_status dsgd_get_vector(dsgd_ctx* ctx, uint32_t local, dsgd_buffer which, double* host);
 /* Raw asynchronous copies in the context dtype on the context stream (host
- * memory should be pinned); used by the end-to-end path. */
+ * memory should be pinned); used by the end-to-end path.  A DSGD_BUF_CENTER
+ * download on rank 0 of a multi-GPU EASGD chain is ordered after the last
+ * round's center chunks on the device (no host wait). */
 dsgd_status dsgd_upload_async(dsgd_ctx* ctx, uint32_t local, dsgd_buffer which,
                               const void* host, uint64_t count);
 dsgd_status dsgd_download_async(dsgd_ctx* ctx, uint32_t local, dsgd_buffer which, void* host,

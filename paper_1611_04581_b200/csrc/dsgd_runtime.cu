@@ -1881,11 +1881,18 @@ dsgd_status dsgd_logistic_set_sample_range(dsgd_ctx* c, uint32_t local, uint64_t
 // Rank 0 of a multi-GPU EASGD chain holds the center in its c_in, written
 // chunk by chunk by rank p-1's last gated round: wait (on the device,
 // bounded) until every chunk of that round has arrived.
-dsgd_status center_arrived(dsgd_ctx* c) {
+// (enqueue only: the context stream waits on the device)
+dsgd_status center_wait_enqueue(dsgd_ctx* c) {
   if (!c->distributed() || c->first != 0 || c->ea_seq == 0 || !c->connected) return DSGD_OK;
   const uint64_t n = (c->d + c->ea_chunk_used - 1) / c->ea_chunk_used;
   DSGD_CUDA(dsgd::launch_wait_chunks(reinterpret_cast<const unsigned long long*>(c->arena + c->off_flags),
                                      n, c->ea_seq, c->timeout_ns, c->error, c->stream));
+  return DSGD_OK;
+}
+
+dsgd_status center_arrived(dsgd_ctx* c) {
+  if (!c->distributed() || c->first != 0 || c->ea_seq == 0 || !c->connected) return DSGD_OK;
+  DSGD_TRY(center_wait_enqueue(c));
   DSGD_CUDA(cudaStreamSynchronize(c->stream));
   unsigned int err = 0;
   DSGD_CUDA(cudaMemcpy(&err, c->error, sizeof(err), cudaMemcpyDeviceToHost));
@@ -1924,6 +1931,7 @@ dsgd_status dsgd_download_async(dsgd_ctx* c, uint32_t local, dsgd_buffer which, 
   char* p = buffer_of(c, local, which);
   if (!p) return set_error(DSGD_ESTATE, "buffer not allocated for this context");
   DeviceGuard g(c->device);
+  if (which == DSGD_BUF_CENTER) DSGD_TRY(center_wait_enqueue(c));  // as dsgd_get_vector
   DSGD_CUDA(cudaMemcpyAsync(host, p, count * c->es, cudaMemcpyDeviceToHost, c->stream));
   return DSGD_OK;
 }
