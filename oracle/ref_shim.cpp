@@ -555,12 +555,6 @@ double time_rounds_impl(int protocol, std::uint32_t p, std::uint64_t d, std::uin
     const Objective& obj = grad_kind == 1 ? static_cast<const Objective&>(*pool)
                                           : static_cast<const Objective&>(quad);
     using clk = std::chrono::steady_clock;
-    if (mode == 2) {  // one run_transport of `rounds` rounds, wall time (sharded runs)
-      cfg.rounds = rounds;
-      const auto t0 = clk::now();
-      (void)run_transport(cfg, obj);
-      return std::chrono::duration<double>(clk::now() - t0).count();
-    }
     if (mode == 1) {
       // run_transport also builds the initial nodes and trace records; time
       // `rounds + 1` and 1 round and keep the difference (per-round cost).
@@ -628,10 +622,8 @@ double ref_time_rounds(int protocol, std::uint32_t p, std::uint64_t d, std::uint
 // The same rounds on every host thread: d split into `shards` coordinate
 // ranges (every rule of this path is coordinate-separable), each shard an
 // independent reference run on its own thread -- the reference's own code
-// using all the cores a host gives it.  Simulator rules (mode 0): the clock
-// spans the rounds of all shards (start / end barriers).  Threaded
-// transport (mode 1): `shards` concurrent run_transport calls of p threads
-// each, (rounds + 1) minus 1 round of wall time, as in ref_time_rounds.
+// using all the cores a host gives it.  Simulator rules only (mode 0): the
+// clock spans the rounds of all shards (start / end barriers).
 double ref_time_rounds_sharded(int protocol, std::uint32_t p, std::uint64_t d,
                                std::uint64_t rounds, int mode, const dsgdo_hyper* hp,
                                int grad_kind, std::uint32_t shards) {
@@ -654,23 +646,10 @@ double ref_time_rounds_sharded(int protocol, std::uint32_t p, std::uint64_t d,
     }
     return m;
   }
-  auto wall = [&](std::uint64_t r) {
-    const auto t0 = clk::now();
-    std::vector<std::thread> th;
-    for (std::uint32_t i = 0; i < shards; ++i)
-      th.emplace_back([&, i] {
-        secs[i] = time_rounds_impl(protocol, p, size_of(i), r, 2, hp, grad_kind, nullptr);
-      });
-    for (auto& t : th) t.join();
-    for (double v : secs)
-      if (v < 0) return -1.0;
-    return std::chrono::duration<double>(clk::now() - t0).count();
-  };
-  // concurrent wall of rounds + 1 rounds minus that of 1 round: the node
-  // construction inside run_transport stays out of the per-round figure
-  const double a = wall(rounds + 1), b = wall(1);
-  if (a < 0 || b < 0) return -1.0;
-  return std::max(0.0, a - b);
+  // the threaded transport is timed unsharded (ref_time_rounds): concurrent
+  // whole run_transport calls cannot keep node construction out of the clock
+  g_err = "sharded timing supports the simulator rules (mode 0) only";
+  return -1.0;
 }
 
 }  // extern "C"

@@ -28,6 +28,21 @@ def test_reference_arm_json_line():
         assert k in j, k
     assert j["value"] > 0 and j["cpu_baseline"]["kind"] == "reference"
     assert j["e2e"]["h2d_bytes_per_step"] == 0 and j["e2e"]["value"] == j["value"]
+    # the reference's own code on every host thread (coordinate shards)
+    assert j["cpu_baseline"]["cores"] == len(os.sched_getaffinity(0))
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_sharded_reference_timing():
+    """ref_time_rounds_sharded: d split into coordinate shards, one reference
+    run (simulator rules) per shard, concurrently; the threaded transport is
+    timed unsharded."""
+    h = O.HyperParams(alpha0=0.1, anneal_at=(), mu=0.9, weight_decay=1e-4, beta_ea=0.1)
+    for proto in (O.ALLREDUCE, O.PULL, O.ELASTIC):
+        assert O.ref_time_rounds(proto, 2, 100_003, 3, False, h, "pool", shards=4) > 0
+        assert O.ref_time_rounds(proto, 2, 100_003, 3, True, h, "pool") > 0
+    with pytest.raises(RuntimeError, match="simulator rules"):
+        O.ref_time_rounds(O.ALLREDUCE, 2, 100_003, 3, True, h, "pool", shards=4)
 
 
 @pytest.mark.gpu
