@@ -483,14 +483,13 @@ __host__ __device__ inline int step_nslots(int quad, bool noise) {
          (S::kGrad ? (quad ? 2 : 1) + (noise ? 1 : 0) : 0);
 }
 
-template <typename T, int MODE>
+template <typename T, int MODE, int kStages>
 __global__ void __launch_bounds__(kBlock) k_step_tma2(const __grid_constant__ StepArgs<T> a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   using S = StepSlots<MODE>;
   constexpr uint64_t TILE = st_tile<T>();
   constexpr uint32_t TB = (uint32_t)(TILE * sizeof(T));
   constexpr int W = Vec<T>::N;
-  constexpr int kStages = 3;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
   T* stage = reinterpret_cast<T*>(smem_raw + 128);
   // programmatic dependent launch: the next launch may be scheduled now;
@@ -614,13 +613,14 @@ __global__ void __launch_bounds__(kBlock) k_step_tma2(const __grid_constant__ St
   block_signal(a.signal);
 }
 
-template <typename T, int MODE>
-cudaError_t launch_step_staged(const StepArgs<T>& a, cudaStream_t s) {
+template <typename T, int MODE, int ST>
+cudaError_t launch_step_staged_st(const StepArgs<T>& a, cudaStream_t s) {
   const int nsl = step_nslots<T, MODE>(a.quad, a.node[0].noise != nullptr);
-  const size_t smem = 128 + (size_t)3 * nsl * st_tile<T>() * sizeof(T);
-  smem_attr(k_step_tma2<T, MODE>, smem);
+  const size_t smem = 128 + (size_t)ST * nsl * st_tile<T>() * sizeof(T);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  smem_attr(k_step_tma2<T, MODE, ST>, smem);
   int resident = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_step_tma2<T, MODE>, kBlock, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_step_tma2<T, MODE, ST>, kBlock, smem);
   if (resident < 1) resident = 1;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -629,7 +629,19 @@ cudaError_t launch_step_staged(const StepArgs<T>& a, cudaStream_t s) {
   uint32_t g = (uint32_t)sms * (uint32_t)resident;
   if (work < g) g = (uint32_t)(work ? work : 1);
   ++g_launches;
-  return launch_pdl(k_step_tma2<T, MODE>, g, kBlock, smem, s, a);
+  return launch_pdl(k_step_tma2<T, MODE, ST>, g, kBlock, smem, s, a);
+}
+
+template <typename T, int MODE>
+cudaError_t launch_step_staged(const StepArgs<T>& a, cudaStream_t s) {
+  static const int stages = [] {  // DSGD_STEP_STAGES: 2, 3 (default) or 4 stages in flight
+    const char* e = getenv("DSGD_STEP_STAGES");
+    const int v = e ? atoi(e) : 3;
+    return v <= 2 ? 2 : (v >= 4 ? 4 : 3);
+  }();
+  if (stages == 2) return launch_step_staged_st<T, MODE, 2>(a, s);
+  if (stages == 4) return launch_step_staged_st<T, MODE, 4>(a, s);
+  return launch_step_staged_st<T, MODE, 3>(a, s);
 }
 
 // Partner-only staging (DSGD_GOSSIP_STAGE_ALL=0), one node per GPU.
