@@ -1970,11 +1970,12 @@ __device__ __forceinline__ void ec_slot_wr(T* p, const T (&v)[Vec<T>::N]) {
   *reinterpret_cast<uint4*>(p) = t.u;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kEcThreads, 1)
+// U: 16-B vectors per update thread per chunk (chunk = kBlock * 16 B * U)
+template <typename T, int U>
+__global__ void __launch_bounds__(kEcThreads, U == 1 ? 2 : 1)
     k_ea_chain_tma(const __grid_constant__ EaChainArgs<T> a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  constexpr uint64_t TILE = st_tile<T>();
+  constexpr uint64_t TILE = (uint64_t)kBlock * Vec<T>::N * U;
   constexpr uint32_t TB = (uint32_t)(TILE * sizeof(T));
   constexpr int W = Vec<T>::N;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
@@ -2082,7 +2083,7 @@ __global__ void __launch_bounds__(kEcThreads, 1)
       mbar_wait(&full[sg], (uint32_t)((j / kEcStages) & 1));
       T* base = stage + (uint64_t)sg * nsl * TILE + (uint64_t)threadIdx.x * W;
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < U; ++u) {
         const uint64_t o = (uint64_t)u * kBlock * W;
         T cv[W], x[W], dp[W], gb[W], sv[W], ov[W], xi[W];
         ec_slot_rd(base + s_c * TILE + o, cv);
@@ -2167,9 +2168,38 @@ __global__ void __launch_bounds__(kEcThreads, 1)
   block_signal(a.signal);
 }
 
+// vectors per update thread per chunk: DSGD_EA_TILE_U = 1 (fp32 only: 1024
+// elements per chunk, two CTAs per SM) or 2 (default: 2048 fp32 / 1024 fp64)
+template <typename T>
+int ea_chain_u() {
+  static const int u = [] {
+    const char* e = getenv("DSGD_EA_TILE_U");
+    return (e && atoi(e) == 1 && sizeof(T) == 4) ? 1 : 2;
+  }();
+  return u;
+}
+
 template <typename T>
 uint64_t ea_chain_tile() {
-  return st_tile<T>();
+  return (uint64_t)kBlock * Vec<T>::N * ea_chain_u<T>();
+}
+
+template <typename T, int U>
+cudaError_t launch_ea_chain_tma(const EaChainArgs<T>& a, cudaStream_t s) {
+  constexpr uint64_t TILE = (uint64_t)kBlock * Vec<T>::N * U;
+  const bool hnoise = a.node.noise != nullptr;
+  const int nsl = (a.quad ? 5 : 4) + (hnoise ? 1 : 0);
+  const size_t smem = 128 + (size_t)kEcStages * nsl * TILE * sizeof(T);
+  smem_attr(k_ea_chain_tma<T, U>, smem);
+  int dev = 0, sms = 148, resident = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_ea_chain_tma<T, U>, kEcThreads, smem);
+  if (resident < 1) resident = 1;
+  const uint64_t nfull = a.d / TILE;
+  const uint32_t g = (uint32_t)std::min<uint64_t>(nfull, (uint64_t)sms * resident);
+  DSGD_PDL_LAUNCH((k_ea_chain_tma<T, U>), g, kEcThreads, smem, s, a);
+  return cudaGetLastError();
 }
 
 template <typename T>
@@ -2182,19 +2212,8 @@ cudaError_t launch_ea_chain(const EaChainArgs<T>& a, int vec, uint32_t grid, cud
       DSGD_COUNTED(k_ea_chain<T, false, true><<<grid, kBlock, 0, s>>>(a));
     return cudaGetLastError();
   }
-  if (vec && a.chunk == st_tile<T>() && a.d >= st_tile<T>() && ea_chain_staged()) {
-    const bool hnoise = a.node.noise != nullptr;
-    const int nsl = (a.quad ? 5 : 4) + (hnoise ? 1 : 0);
-    const size_t smem = 128 + (size_t)kEcStages * nsl * st_tile<T>() * sizeof(T);
-    smem_attr(k_ea_chain_tma<T>, smem);
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const uint64_t nfull = a.d / st_tile<T>();
-    const uint32_t g = (uint32_t)std::min<uint64_t>(nfull, (uint64_t)sms);
-    DSGD_PDL_LAUNCH(k_ea_chain_tma<T>, g, kEcThreads, smem, s, a);
-    return cudaGetLastError();
-  }
+  if (vec && a.chunk == ea_chain_tile<T>() && a.d >= a.chunk && ea_chain_staged())
+    return ea_chain_u<T>() == 1 ? launch_ea_chain_tma<T, 1>(a, s) : launch_ea_chain_tma<T, 2>(a, s);
   if (vec)
     DSGD_COUNTED(k_ea_chain<T, true><<<grid, kBlock, 0, s>>>(a));
   else
