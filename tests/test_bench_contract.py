@@ -72,3 +72,21 @@ def test_bench_json_line_on_gpu():
     assert e["d2h_bytes_per_step"] > 0
     assert j["gpu_launches"] >= 5
     assert j["clocks"]["sm_mhz"] is not None
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_cpu_reference_sweep_tool():
+    """tools/cpu_reference.py --sweep (profiles/r2_cpu_reference_sweep.md) at a
+    tiny size: one JSON line per (protocol, p, path), every figure positive
+    or an explicit error record."""
+    out = subprocess.run([sys.executable, "tools/cpu_reference.py", "--sweep", "--sizes", "4096",
+                          "--max-seconds", "60"], capture_output=True, text=True, cwd=ROOT,
+                         timeout=300)
+    assert out.returncode == 0, out.stderr
+    rows = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    assert "host" in rows[0]
+    runs = [r for r in rows[1:] if "param_updates_per_s" in r]
+    assert len(runs) + sum("error" in r for r in rows[1:]) == 3 * 3 * 3
+    assert all(r["param_updates_per_s"] > 0 for r in runs)
+    assert {r["path"] for r in runs} >= {"simulator rules, all threads (coordinate shards)",
+                                          "simulator rules (1 thread)"}
