@@ -34,7 +34,7 @@ NPD = {"f64": np.float64, "f32": np.float32}
 
 
 def run_group(proto, world, dtype, d, rounds, monkeypatch, backend=None, sigma=0.05,
-              run_id=None):
+              run_id=None, devices=None):
     if backend:
         monkeypatch.setenv("DSGD_ALLREDUCE", backend)
     else:
@@ -54,7 +54,7 @@ def run_group(proto, world, dtype, d, rounds, monkeypatch, backend=None, sigma=0
                        run_id=run_id)
     thetas = D.make_initial_nodes(dcfg, obj)
     gs = Group.inproc(d, world, dtype=dtype, quadratic=True, noise=True,
-                      center=proto == "elastic-avg")
+                      center=proto == "elastic-avg", devices=devices)
     try:
         for r, g in enumerate(gs):
             g.set_quadratic(obj.spectrum)
@@ -165,3 +165,23 @@ def test_inproc_ea_chain_staged_ring_wraps(dtype, monkeypatch):
     4 rounds, bit-exact with the oracle."""
     res = run_group("elastic-avg", 3, dtype, 148 * 6 * 2048 + 13, 4, monkeypatch)
     check(res, "elastic-avg")
+
+
+
+def n_gpus():
+    import torch
+    return torch.cuda.device_count()
+
+
+@pytest.mark.skipif("n_gpus() < 2")
+@pytest.mark.parametrize("proto", sorted(OID))
+def test_inproc_p8_across_gpus(proto, monkeypatch):
+    """p = 8 ranks spread over every visible GPU (rank r on GPU r mod n):
+    the 8-rank kernels -- the 7-hop EASGD chain + ring closure, 8-way
+    gossip flags, the two-shot ring reduce at p = 8 -- with real NVLink
+    traffic between the GPUs (the shape of an 8-GPU box the pool cannot
+    provide), bit-exact with the oracle / the reference's ring order."""
+    n = n_gpus()
+    res = run_group(proto, 8, "f32", 5 * 4096 + 7, 6, monkeypatch,
+                    devices=[r % n for r in range(8)], run_id=f"ipx/{proto}")
+    check(res, proto)
